@@ -1,0 +1,334 @@
+"""Pins for the CPU oracle (-m "not gpu"): the oracle is checked against what the paper and the
+mathematics fix, never against itself. Each test names the pin and the
+passage it follows. A plausible mistake in the oracle (dropped term, wrong sign/index, transposed
+operand, unstable order) fails at least one of these."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.tolerances import rel_err
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ---- P6: top-K rule and weights, SPEC worked examples ----------------------------------------------
+
+@pytest.mark.parametrize("case", _gold("spec_examples.json")["topk_select"], ids=lambda c: c["cite"][:14])
+def test_topk_spec_examples(case):
+    lg = np.array([case["logits"]], np.float64)
+    r = oracle.route(lg, case["K"])
+    assert r["topk_idx"][0].tolist() == case["ids"]
+    np.testing.assert_allclose(r["topk_w"][0], case["weights"], atol=case["tol"], rtol=0)
+    if case["K"] == 1:
+        assert r["topk_w"][0, 0] == 1.0  # bitwise 1 (Q1)
+
+
+def _route_reference_numpy(lg, k):
+    """Independent statement of the same rule through a library stable sort (descending logit,
+    ties -> lower id) and a stable sort of slots by expert (FIFO within an expert queue)."""
+    T, E = lg.shape
+    order = np.argsort(-lg.astype(np.float64), axis=1, kind="stable")[:, :k]
+    flat = order.reshape(-1)
+    src = np.argsort(flat, kind="stable").astype(np.int32)
+    dest = np.empty_like(src)
+    dest[src] = np.arange(src.size, dtype=np.int32)
+    counts = np.bincount(flat, minlength=E).astype(np.int32)
+    return order.astype(np.int32), counts, dest, src
+
+
+@pytest.mark.parametrize("T,E,k,kind", [(257, 8, 1, "normal"), (300, 8, 2, "normal"), (64, 1, 1, "normal"),
+                                        (512, 8, 1, "ties"), (200, 5, 3, "ties"), (128, 256, 4, "normal"),
+                                        (77, 8, 8, "normal")])
+def test_route_matches_stable_sort(T, E, k, kind):
+    lg = synth.router_logits(T, E) if kind == "normal" else synth.near_tie_logits(T, E)
+    r = oracle.route(lg, k)
+    idx, counts, dest, src = _route_reference_numpy(lg, k)
+    assert np.array_equal(r["topk_idx"], idx)
+    assert np.array_equal(r["counts"], counts)
+    assert np.array_equal(r["dest"], dest)
+    assert np.array_equal(r["src"], src)
+
+
+def test_route_invariants_P3():
+    T, E, k = 1000, 8, 2
+    r = oracle.route(synth.router_logits(T, E), k)
+    assert r["counts"].sum() == T * k
+    assert r["offsets"][0] == 0 and r["offsets"][-1] == T * k
+    assert np.array_equal(np.diff(r["offsets"]), r["counts"])
+    assert np.array_equal(np.sort(r["dest"]), np.arange(T * k))  # bijection
+    assert np.array_equal(r["src"][r["dest"]], np.arange(T * k))  # src = dest^-1
+    for e in range(E):  # stability: FIFO inside each expert segment
+        seg = r["src"][r["offsets"][e]:r["offsets"][e + 1]]
+        assert np.all(np.diff(seg) > 0)
+        assert np.all(r["topk_idx"].reshape(-1)[seg] == e)
+    np.testing.assert_allclose(r["topk_w"].sum(axis=1), 1.0, atol=1e-12)
+    assert np.all(np.diff(r["topk_w"], axis=1) <= 0)  # descending logit => descending weight
+
+
+def test_route_k1_weight_exactly_one():
+    r = oracle.route(synth.router_logits(500, 8), 1)
+    assert np.all(r["topk_w"] == 1.0)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_route_rejects_nonfinite(bad):
+    lg = synth.router_logits(10, 8)
+    lg[3, 2] = bad
+    with pytest.raises(oracle.OracleError):
+        oracle.route(lg, 1)
+
+
+def test_route_T0():
+    r = oracle.route(np.zeros((0, 8), np.float32), 1)
+    assert r["counts"].tolist() == [0] * 8 and r["offsets"].tolist() == [0] * 9
+
+
+# ---- P8: ReLU two-layer expert form, SPEC hand examples ----------------------------------------------
+
+def _relu_expert_weights(W1, W2, mask):
+    W1 = np.asarray(W1, np.float64)
+    W2 = np.asarray(W2, np.float64)
+    D, H = W1.shape
+    return oracle.build_experts(W1, W1, W2, np.array([mask], np.int32))
+
+
+@pytest.mark.parametrize("case", _gold("spec_examples.json")["relu_build_expert"], ids=lambda c: c["cite"][:10])
+def test_relu_build_expert_spec(case):
+    eg, eu, ed = _relu_expert_weights(case["W1"], case["W2"], case["mask"])
+    x = np.array([case["x"]], np.float64)
+    y = oracle.expert_ffn(x, np.array([0, 1], np.int32), eg, eu, ed, act="relu")
+    assert y[0].tolist() == case["y"]
+
+
+@pytest.mark.parametrize("case", _gold("spec_examples.json")["relu_dense_forward"], ids=lambda c: c["cite"][:10])
+def test_relu_dense_forward_spec(case):
+    W1 = np.asarray(case["W1"], np.float64)
+    y = oracle.dense_ffn(np.array([case["x"]]), W1, W1, np.asarray(case["W2"], np.float64), act="relu")
+    assert y[0].tolist() == case["y"]
+
+
+def test_relu_pregated_combination_spec():
+    case = _gold("spec_examples.json")["relu_pregated_combination"][0]
+    W1 = np.asarray(case["W1"], np.float64)
+    W2 = np.asarray(case["W2"], np.float64)
+    eg, eu, ed = oracle.build_experts(W1, W1, W2, np.array(case["masks"], np.int32))
+    y, plan = oracle.moe_layer(np.array([case["x"]]), np.array([case["logits"]]), case["K"], eg, eu, ed,
+                               act="relu")
+    np.testing.assert_allclose(y[0], case["y"], atol=case["tol"], rtol=0)
+    yb = oracle.bruteforce(np.array([case["x"]]), np.array([case["logits"]]), case["K"], W1, W1, W2,
+                           np.array(case["masks"], np.int32), act="relu")
+    np.testing.assert_allclose(yb[0], case["y"], atol=case["tol"], rtol=0)
+
+
+# ---- P7: SwiGLU closed forms ----------------------------------------------------------------------
+
+def test_swiglu_closed_forms():
+    g = _gold("swiglu_closed_forms.json")
+    tol = g["tol_abs"]
+    for c in g["cases"]:
+        y = oracle.expert_ffn(np.array([c["x"]]), np.array([0, 1], np.int32),
+                              np.array([c["w_gate"]], np.float64), np.array([c["w_up"]], np.float64),
+                              np.array([c["w_down"]], np.float64))
+        np.testing.assert_allclose(y[0], c["y"], atol=tol, rtol=0, err_msg=c["cite"])
+    ex = g["experts_of_identity"]
+    dn = ex["dense"]
+    wg, wu, wd = (np.asarray(dn[k], np.float64) for k in ("w_gate", "w_up", "w_down"))
+    eg, eu, ed = oracle.build_experts(wg, wu, wd, np.array([[0], [1]], np.int32))
+    x = np.array([ex["x"]])
+    for e in (0, 1):
+        off = np.array([0, 1, 1] if e == 0 else [0, 0, 1], np.int32)
+        y = oracle.expert_ffn(x, off, eg, eu, ed)
+        np.testing.assert_allclose(y[0], ex["single"][str(e)], atol=tol, rtol=0)
+    y, _ = oracle.moe_layer(x, np.array([ex["logits"]]), ex["K"], eg, eu, ed)
+    np.testing.assert_allclose(y[0], ex["y"], atol=tol, rtol=0)
+
+
+# ---- P1: full-FFN expert == dense FFN ---------------------------------------------------------------
+
+@pytest.mark.parametrize("E", [1, 4])
+def test_full_expert_equals_dense_P1(E):
+    T, H, D = 40, 24, 48
+    wg, wu, wd = synth.dense_ffn_weights(D, H, D, seed=11)
+    S = synth.neuron_sets(E, D, D, mode="full")
+    eg, eu, ed = oracle.build_experts(wg, wu, wd, S)
+    x = synth.tokens(T, H, seed=12)
+    lg = synth.router_logits(T, E, seed=13)
+    y, _ = oracle.moe_layer(x, lg, 1, eg, eu, ed)
+    yd = oracle.dense_ffn(x, wg, wu, wd)
+    assert np.array_equal(y, yd)  # same accumulation order -> bitwise
+
+
+# ---- P2: partition identity sum_e F_e(x) = F_0(x) ----------------------------------------------------
+
+def test_partition_identity_P2():
+    T, H, D, E = 16, 32, 64, 8
+    d = D // E
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=21)
+    S = synth.neuron_sets(E, D, d, mode="partition", seed=22)
+    eg, eu, ed = oracle.build_experts(wg, wu, wd, S)
+    x = synth.tokens(T, H, seed=23)
+    acc = np.zeros((T, H))
+    for e in range(E):  # force every token to expert e
+        off = np.array([0] * (e + 1) + [T] * (E - e), np.int32)
+        acc += oracle.expert_ffn(x, off, eg, eu, ed)
+    yd = oracle.dense_ffn(x, wg, wu, wd)
+    assert rel_err(acc, yd) < 1e-12
+
+
+def test_build_experts_slices():
+    D, H, E, d = 20, 12, 3, 7
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=31)
+    S = synth.neuron_sets(E, D, d, seed=32)
+    eg, eu, ed = oracle.build_experts(wg, wu, wd, S)
+    for e in range(E):
+        assert np.array_equal(eg[e], wg[S[e]].astype(np.float64))
+        assert np.array_equal(eu[e], wu[S[e]].astype(np.float64))
+        assert np.array_equal(ed[e], wd[:, S[e]].astype(np.float64))
+    bad = S.copy()
+    bad[0, 1] = bad[0, 0]  # not strictly increasing
+    with pytest.raises(oracle.OracleError):
+        oracle.build_experts(wg, wu, wd, bad)
+
+
+# ---- P3/a5: dispatch is a bit copy through the permutation --------------------------------------------
+
+def test_dispatch_bit_copy():
+    T, H, E, k = 50, 16, 8, 2
+    x = synth.to_torch(synth.tokens(T, H), "bf16")
+    r = oracle.route(synth.router_logits(T, E), k)
+    xs = oracle.dispatch(x, r["dest"], k)
+    xf = x.double().numpy()
+    for s in range(T * k):
+        assert np.array_equal(xs[r["dest"][s]], xf[s // k])
+
+
+# ---- P5: brute force on tiny inputs -----------------------------------------------------------------
+
+@pytest.mark.parametrize("E,k", [(1, 1), (2, 1), (2, 2), (8, 1), (8, 2)])
+def test_bruteforce_P5(E, k):
+    T, H, D, d = 48, 16, 32, 16
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=41 + E)
+    S = synth.neuron_sets(E, D, d, seed=42 + E)
+    eg, eu, ed = oracle.build_experts(wg, wu, wd, S)
+    x = synth.tokens(T, H, seed=43)
+    lg = synth.near_tie_logits(T, E, seed=44) if E > 1 else synth.router_logits(T, E, seed=44)
+    y, _ = oracle.moe_layer(x, lg, k, eg, eu, ed)
+    yb = oracle.bruteforce(x, lg, k, wg, wu, wd, S)
+    assert rel_err(y, yb) < 1e-12
+
+
+# ---- P4: permutation equivariance -------------------------------------------------------------------
+
+def test_permutation_equivariance_P4():
+    T, H, E, d, k = 96, 16, 8, 24, 2
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=51)
+    x = synth.tokens(T, H, seed=52)
+    lg = synth.router_logits(T, E, seed=53)
+    y, plan = oracle.moe_layer(x, lg, k, eg, eu, ed)
+    perm = synth.rng(54, 0).permutation(T)
+    yp, planp = oracle.moe_layer(x[perm], lg[perm], k, eg, eu, ed)
+    assert np.array_equal(yp, y[perm])
+    assert np.array_equal(planp["counts"], plan["counts"])
+    assert np.array_equal(planp["offsets"], plan["offsets"])
+
+
+# ---- P9: zero / edge cases ---------------------------------------------------------------------------
+
+def test_zero_and_edges_P9():
+    H, E, d = 8, 4, 6
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=61)
+    y, _ = oracle.moe_layer(np.zeros((5, H)), synth.router_logits(5, E), 1, eg, eu, ed)
+    assert np.all(y == 0.0)
+    y, plan = oracle.moe_layer(np.zeros((0, H)), np.zeros((0, E)), 1, eg, eu, ed)
+    assert y.shape == (0, H) and plan["offsets"].tolist() == [0] * (E + 1)
+    # k = E selects every expert with softmax weights over all logits
+    lg = synth.router_logits(3, E, seed=62).astype(np.float64)
+    r = oracle.route(lg, E)
+    sm = np.exp(lg - lg.max(axis=1, keepdims=True))
+    sm /= sm.sum(axis=1, keepdims=True)
+    for t in range(3):
+        np.testing.assert_allclose(r["topk_w"][t], sm[t, r["topk_idx"][t]], rtol=1e-14)
+        assert sorted(r["topk_idx"][t].tolist()) == list(range(E))
+
+
+# ---- P10: power-of-two scaling of W_down is exact -----------------------------------------------------
+
+def test_scaling_P10():
+    T, H, E, d = 30, 16, 8, 12
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=71)
+    x = synth.tokens(T, H, seed=72)
+    lg = synth.router_logits(T, E, seed=73)
+    y, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed)
+    y8, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed.astype(np.float64) * 8.0)
+    assert np.array_equal(y8, y * 8.0)
+
+
+def test_residual_added():
+    T, H, E, d = 10, 8, 4, 6
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=81)
+    x = synth.tokens(T, H, seed=82)
+    res = synth.residual(T, H, seed=83)
+    lg = synth.router_logits(T, E, seed=84)
+    y, _ = oracle.moe_layer(x, lg, 1, eg, eu, ed)
+    yr, _ = oracle.moe_layer(x, lg, 1, eg, eu, ed, residual=res)
+    np.testing.assert_allclose(yr - res.astype(np.float64), y, atol=1e-14, rtol=0)
+
+
+# ---- P11: route once, reuse across layers ------------------------------------------------------------
+
+def test_route_once_P11():
+    T, H, E, d, L, k = 40, 16, 8, 12, 3, 1
+    lg = synth.router_logits(T, E, seed=91)
+    x0 = synth.tokens(T, H, seed=92)
+    layers = [synth.expert_weights(E, d, H, seed=93, layer=l) for l in range(L)]
+    # (a) re-route every layer from the same pre-gating logits
+    xa = x0.astype(np.float64)
+    plans = []
+    for (eg, eu, ed) in layers:
+        y, plan = oracle.moe_layer(xa, lg, k, eg, eu, ed)
+        plans.append(plan)
+        xa = xa + y
+    # (b) route once, reuse the plan (dispatch / FFN / combine per layer)
+    plan = oracle.route(lg, k)
+    xb = x0.astype(np.float64)
+    for (eg, eu, ed) in layers:
+        xs = oracle.dispatch(xb, plan["dest"], k)
+        ys = oracle.expert_ffn(xs, plan["offsets"], eg, eu, ed)
+        xb = xb + oracle.combine(ys, plan["dest"], plan["topk_w"], k)
+    for p in plans:
+        for key in ("topk_idx", "counts", "offsets", "dest", "src"):
+            assert np.array_equal(p[key], plan[key])
+    assert np.array_equal(xa, xb)
+
+
+# ---- P12: expert-parallel simulation == single layer ---------------------------------------------------
+
+@pytest.mark.parametrize("G,k", [(1, 1), (2, 1), (4, 2), (8, 1)])
+def test_ep_sim_equals_layer_P12(G, k):
+    T, H, E, d = 64, 16, 8, 12
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=101)
+    x = synth.to_torch(synth.tokens(T, H, seed=102), "bf16")
+    lg = synth.router_logits(T, E, seed=103)
+    y, _ = oracle.moe_layer(x, lg, k, eg, eu, ed)
+    ye = oracle.ep_sim(G, x, lg, k, eg, eu, ed)
+    assert np.array_equal(y, ye)
+
+
+def test_thread_count_invariance():
+    T, H, E, d = 33, 16, 8, 20
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=111)
+    x = synth.tokens(T, H, seed=112)
+    lg = synth.router_logits(T, E, seed=113)
+    y1, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed, nthreads=1)
+    y8, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed, nthreads=8)
+    assert np.array_equal(y1, y8)
