@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""bench.py — READ-ME pre-gated MoE layer throughput on B200 (the BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl readme|reference] [--config 2]
+
+A step is one pass of the whole hot path (route -> dispatch -> grouped gate/up GEMM
+(+SiLU) -> grouped down GEMM -> combine) over one batch of synthetic tokens, through the C ABI
+(libreadme_b200.so). N=1 runs BASELINE config 2 (one Llama-2-7B-shaped MoE layer, T=8192 prefill
+tokens, 8 experts of d=5504 neurons, top-1, bf16). N>1 (launched by torchrun) runs the expert-parallel
+layer (config 5 per rank: 8192 tokens per rank, experts sharded over ranks, NCCL all-to-all), weak
+scaling; value = all ranks' tokens / max-over-ranks time.
+
+Rank 0 prints ONE JSON line. `--impl reference` times the CPU oracle (the tier's reference arm) on a
+bounded token sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/s @ Llama-2-7B shape, 1/2/4/8 B200; % bf16 TC peak / % HBM BW"
+UNIT = "tokens/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="readme", choices=["readme", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tokens", type=int, default=None, help="override T per rank")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return FALLBACK_PEAKS, "fallback"
+
+
+# ---- clocks sampler (nvidia-smi during the timed region) ----------------------------------------------
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- workload -------------------------------------------------------------------------------------
+
+def make_inputs(cfg: dict, T: int, rank: int, device, E_local=None, expert_base=0):
+    """Synthetic Llama-2-7B-shaped inputs (recipe: DESIGN.md §Inputs). Experts are sliced on the device
+    from the dense FFN by readme_build_experts (setup, untimed)."""
+    import torch
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+    H, D, d, E = cfg["H"], cfg["D"], cfg["d"], cfg["E"]
+    seed = synth.MASTER_SEED + 2
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
+    S = synth.neuron_sets(E, D, d, seed=seed)
+    if E_local is not None:
+        S = S[expert_base:expert_base + E_local]
+    dense = [synth.to_torch(w, "bf16").to(device) for w in (wg, wu, wd)]
+    del wg, wu, wd
+    eg, eu, ed = rd.build_experts(*dense, torch.from_numpy(np.ascontiguousarray(S)).to(device))
+    dense_cpu = None
+    x = synth.to_torch(synth.tokens(T, H, seed=seed + 1000 * rank), "bf16")
+    lg = synth.router_logits(T, E, seed=seed + 1000 * rank)
+    return dict(x=x, logits=lg, w=(eg, eu, ed), dense=dense, S=S, dense_cpu=dense_cpu)
+
+
+def cpu_baseline(cfg, inp, budget_s=15.0):
+    """The oracle (test infrastructure) timed on this host's cores on a bounded, expert-stratified token
+    sample of the same workload; tokens are independent, so tokens/s scales linearly."""
+    import oracle
+    import synth
+    E = cfg["E"]
+    lg = inp["logits"]
+    idx = lg.argmax(axis=1)
+    dense = [t.cpu() for t in inp["dense"]]
+    eg, eu, ed = (t.cpu() for t in inp["w"])
+    g = synth.rng(7, 7)
+    threads = oracle.default_threads()
+
+    def run(n_per_expert):
+        sample = np.concatenate([g.choice(np.nonzero(idx == e)[0], size=n_per_expert, replace=False)
+                                 for e in range(E)])
+        t0 = time.perf_counter()
+        oracle.moe_layer(inp["x"][sample], lg[sample], cfg["k"], eg, eu, ed, nthreads=threads)
+        return time.perf_counter() - t0, sample.size
+
+    dt, n = run(1)
+    per_tok = dt / n
+    n_e = max(1, min(64, int(budget_s / per_tok / E)))
+    dt, n = run(n_e)
+    del dense
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{n} tokens ({n_e} per expert) of config {cfg['name']}, full layer (route+dispatch+FFN+"
+                      f"combine) in fp64, {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    cfg = dict(synth.CONFIGS[args.config])
+    T, H, D, d, E = cfg["T"], cfg["H"], cfg["D"], cfg["d"], cfg["E"]
+    seed = synth.MASTER_SEED + 2
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
+    S = synth.neuron_sets(E, D, d, seed=seed)
+    dense = [synth.to_torch(w, "bf16") for w in (wg, wu, wd)]
+    eg, eu, ed = oracle.build_experts(*dense, S)
+    del wg, wu, wd
+    x = synth.to_torch(synth.tokens(T, H, seed=seed), "bf16")
+    lg = synth.router_logits(T, E, seed=seed)
+    per_step = 8  # tokens per step (one per expert on average): a bounded sample of the workload
+    threads = oracle.default_threads()
+    g = synth.rng(5, 5)
+    times = []
+    for i in range(args.warmup + args.steps):
+        sample = g.choice(T, size=per_step, replace=False)
+        t0 = time.perf_counter()
+        oracle.moe_layer(x[sample], lg[sample], cfg["k"], eg, eu, ed, nthreads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = per_step * len(times) / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"config{args.config}_{cfg['name']}", "T": T, "H": H, "E": E, "d": d,
+                       "k": cfg["k"], "tokens_per_step_sampled": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{per_step} random tokens per step of config {args.config}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = dict(synth.CONFIGS[args.config if world == 1 else 5])
+    T = args.tokens or (cfg["T"] if world == 1 else 8192)
+    H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
+
+    if world > 1:
+        from paper_2410_19123_b200 import ep
+        layer = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
+        step_fn = layer.step
+        x_dev = layer.x
+        inp = None
+    else:
+        inp = make_inputs(cfg, T, rank, dev)
+        eg, eu, ed = inp["w"]
+        x_dev = inp["x"].to(dev)
+        lg_dev = torch.from_numpy(inp["logits"]).to(dev)
+        plan = rd.new_plan(T, E, k, dev)
+        xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
+        ys = torch.empty_like(xs)
+        y = torch.empty_like(x_dev)
+        ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
+        ws_f = torch.empty(rd.expert_ffn_workspace_bytes(T * k, H, E, d, torch.bfloat16), dtype=torch.uint8,
+                           device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+        def step_fn(record=False):
+            if record:
+                ev[0].record()
+            rd.route(lg_dev, k, plan=plan, ws=ws_r)
+            if record:
+                ev[1].record()
+            rd.dispatch(x_dev, plan.dest, k, out=xs)
+            if record:
+                ev[2].record()
+            rd.expert_ffn(xs, plan.offsets, eg, eu, ed, out=ys, ws=ws_f)
+            if record:
+                ev[3].record()
+            rd.combine(ys, plan.dest, plan.topk_w, k, out=y)
+            if record:
+                ev[4].record()
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x L2
+    for _ in range(args.warmup):
+        step_fn()
+    torch.cuda.synchronize()
+
+    stage_ms = {"route": 0.0, "dispatch": 0.0, "expert_ffn": 0.0, "combine": 0.0}
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        per_stage = []
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            starts[i].record()
+            if world > 1:
+                step_fn()
+            else:
+                step_fn(record=True)
+            ends[i].record()
+            if world == 1:
+                torch.cuda.synchronize()
+                per_stage.append([ev[j].elapsed_time(ev[j + 1]) for j in range(4)])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = T * world / (ms_per_step * 1e-3)
+
+    pk, pk_src = peaks()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": (f"config{args.config}_{cfg['name']}" if world == 1 else "config5_expert_parallel"),
+                       "T_per_gpu": T, "H": H, "D": cfg["D"], "E": E, "d": d, "k": k,
+                       "parallelism": "single" if world == 1 else f"ep{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"}}
+    if world == 1:
+        st = np.array(per_stage)
+        med = {n: float(np.median(st[:, j])) for j, n in enumerate(stage_ms)}
+        line["stage_ms_median"] = med
+        flops = 6.0 * T * k * H * d
+        ffn_ms = float(np.mean(st[:, 2]))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("expert_ffn_bytes_per_launch")
+        line["roofline"] = {"bound": "tensor", "kernel": "grouped expert GEMMs (gate/up+SiLU, down) = readme_expert_ffn",
+                            "achieved": flops / (ffn_ms * 1e-3) / 1e12, "peak": pk["bf16_tflops"],
+                            "unit": "TFLOP/s", "frac": flops / (ffn_ms * 1e-3) / 1e12 / pk["bf16_tflops"],
+                            "traffic": traffic, "peak_source": f"{pk_src} bf16 burst",
+                            "algorithmic": f"6*T*k*H*d = {flops:.4g} FLOP per launch pair"}
+        hbm = pk["hbm_gbs"]
+        disp_bytes = 2.0 * T * k * H * 2
+        comb_bytes = (k + 1.0) * T * H * 2
+        line["hbm"] = {"dispatch_GBps": disp_bytes / (med["dispatch"] * 1e-3) / 1e9,
+                       "combine_GBps": comb_bytes / (med["combine"] * 1e-3) / 1e9, "peak_GBps": hbm,
+                       "dispatch_frac": disp_bytes / (med["dispatch"] * 1e-3) / 1e9 / hbm,
+                       "combine_frac": comb_bytes / (med["combine"] * 1e-3) / 1e9 / hbm}
+        line["gpu_launches"] = 6 * args.steps  # route(2) + dispatch(1) + expert_ffn(2) + combine(1) per step
+    else:
+        line["gpu_launches"] = None
+    line["clocks"] = clk.summary()
+
+    if world == 1 and not args.no_e2e:
+        # e2e through the public API (readme_moe_layer) with pinned host buffers: H2D inputs, D2H result.
+        x_h = inp["x"].pin_memory()
+        lg_h = torch.from_numpy(inp["logits"]).pin_memory()
+        y_h = torch.empty_like(x_h).pin_memory()
+        x_d = torch.empty_like(x_dev)
+        lg_d = torch.empty_like(lg_dev)
+        ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
+        y_d = torch.empty_like(x_dev)
+
+        def e2e_step():
+            x_d.copy_(x_h, non_blocking=True)
+            lg_d.copy_(lg_h, non_blocking=True)
+            rd.moe_layer(x_d, eg, eu, ed, k=k, logits=lg_d, plan=plan, out=y_d, ws=ws)
+            y_h.copy_(y_d, non_blocking=True)
+
+        for _ in range(max(2, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            e2e_step()
+            e.record()
+            torch.cuda.synchronize()
+            e_ms.append(s.elapsed_time(e))
+        line["e2e"] = {"value": T / (np.mean(e_ms) * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": x_h.numel() * 2 + lg_h.numel() * 4,
+                       "d2h_bytes_per_step": y_h.numel() * 2, "ms_per_step": float(np.mean(e_ms))}
+
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, inp)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

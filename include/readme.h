@@ -1,0 +1,152 @@
+/* include/readme.h — C ABI of the B200-native READ-ME pre-gated MoE layer (libreadme_b200.so).
+ *
+ * READ-ME (arXiv 2410.19123) refactors a dense FFN into N experts, each a subset of the dense FFN's
+ * neurons (§3: F_i(x) = W_2 M_i^T sigma(M_i W_1 x)), and routes every token ONCE with a
+ * pre-gating router G that is independent of the layer (§2.3, Eq. 2):
+ *
+ *     y_t = sum_i 1( |{j : G(x_<=t)_j >= G(x_<=t)_i}| <= K ) * G(x_<=t)_i * F_i^(l)(x_t)
+ *
+ * This library implements the data-parallel hot path of one such layer on an NVIDIA B200 (sm_100a):
+ *   readme_route      a1-a4  top-K + gate weights, per-expert histogram, exclusive scan, stable permutation
+ *   readme_dispatch   a5     scatter tokens into expert-contiguous rows
+ *   readme_expert_ffn a6-a7  grouped SwiGLU expert GEMMs (tcgen05/TMEM for bf16, SIMT fp32 for f32)
+ *   readme_combine    a8     gather back to token order, weight, add residual
+ *   readme_moe_layer  a1-a8  the whole layer; with logits == NULL it reuses a routing plan (a9: route
+ *                            once, reuse across all L layers)
+ *   readme_build_experts     setup: slice expert stacks out of the dense FFN
+ * Readings of the paper (Q1..Q14) are listed in DESIGN.md; they are cited below where they decide a
+ * behaviour.
+ *
+ * Conventions for every entry point:
+ *   - Tensor pointers are CUDA DEVICE pointers (unless stated), row-major, contiguous, 16-byte aligned.
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t), never synchronise the host, never allocate
+ *     device or host memory, and retain no pointer after returning: they are CUDA-graph capturable.
+ *   - Ownership: the caller owns every buffer and the workspace; the library borrows them for the
+ *     stream-ordered duration of the call. Outputs are fully overwritten (no pre-zeroing needed).
+ *   - Errors: argument errors are reported synchronously by the return code and nothing is launched;
+ *     readme_last_error() gives a thread-local message. Data errors only visible on the device
+ *     (non-finite logits, out-of-range ids in a caller-supplied plan) are OR-ed as README_DEV_* bits into
+ *     *dev_status (if non-NULL); indices are clamped so nothing faults. No exception crosses the ABI and
+ *     nothing calls exit/abort.
+ *   - T == 0 is a valid no-op (counts/offsets are still written as zeros).
+ *   - Thread safety: reentrant. The only global state is per-device kernel attributes and cached driver
+ *     entry points, initialised once under std::call_once.
+ */
+#ifndef README_B200_H_
+#define README_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t (struct CUstream_st*); NULL = the legacy default stream. */
+typedef struct CUstream_st* readme_stream_t;
+
+typedef enum {
+  README_OK = 0,
+  README_ERR_INVALID_ARG = 1,  /* null required pointer, bad size, misalignment */
+  README_ERR_UNSUPPORTED = 2,  /* a dtype / shape combination this build does not provide */
+  README_ERR_WORKSPACE = 3,    /* ws_bytes smaller than the matching *_workspace_bytes() */
+  README_ERR_CUDA = 4          /* a CUDA launch or driver call failed (see readme_last_error) */
+} readme_status;
+
+typedef enum { README_F32 = 0, README_BF16 = 1 } readme_dtype;
+
+#define README_DEV_NONFINITE_LOGIT 0x1u /* some logit was NaN/Inf (Q3: NaN ranks as -inf) */
+#define README_DEV_BAD_INDEX 0x2u       /* a caller-supplied plan held an id/row out of range */
+
+#define README_MAX_EXPERTS 256
+
+/* ---------------------------------------------------------------------------------------------- */
+/* a1-a4: routing plan.  PAPER.md:136-138 (Eq. 2 indicator), Alg. 1 ReqQueueByExpert.
+ *
+ * logits   [T,E] f32 or bf16 (logits_dt): G(x_<=t), produced once per token by the pre-gating router.
+ * topk_idx [T,k] int32 out: the k experts of each token in descending logit order; ties go to the
+ *          lower expert id (Q2). Exactly k distinct ids per token.
+ * topk_w   [T,k] f32 out: softmax over the k selected logits (Q1); k == 1 gives exactly 1.0f.
+ * counts   [E]   int32 out: #{(t,j) : topk_idx[t,j] == e}.
+ * offsets  [E+1] int32 out: exclusive prefix sum of counts; offsets[E] == T*k.
+ * dest     [T*k] int32 out: for flat slot s = t*k + j, the row of x_sorted that holds it:
+ *          dest[s] = offsets[e] + #{s' < s : expert(s') == e}  (stable / FIFO within an expert, Q7).
+ * src      [T*k] int32 out, nullable: inverse permutation, src[dest[s]] = s.
+ * dev_status nullable: README_DEV_NONFINITE_LOGIT is OR-ed in if any logit is NaN/Inf.
+ * ws       device workspace of readme_route_workspace_bytes(T,E,k) bytes (zeroed by the call itself).
+ * Requires 1 <= E <= 256, 1 <= k <= E, T*k < 2^31.
+ */
+size_t readme_route_workspace_bytes(int64_t T, int32_t E, int32_t k);
+readme_status readme_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
+                           int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
+                           int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                           readme_stream_t stream);
+
+/* a5: dispatch.  x_sorted[dest[s]] = x[s / k] for every slot s < T*k (a bit copy of whole rows).
+ * x [T,H] and x_sorted [T*k,H] of dtype dt; H*sizeof(dt) must be a multiple of 16 bytes.
+ * Out-of-range dest entries set README_DEV_BAD_INDEX in dev_status (nullable) and are skipped. */
+readme_status readme_dispatch(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                              const int32_t* dest, void* x_sorted, uint32_t* dev_status,
+                              readme_stream_t stream);
+
+/* a6-a7: grouped expert FFN over expert-contiguous rows (PAPER.md:159 with sigma = SwiGLU, Q4):
+ *     for segment g, rows r in [offsets[g], offsets[g+1]), expert e = g % E:
+ *         h_r = silu(x_r W_gate[e]^T) * (x_r W_up[e]^T)      silu(z) = z / (1 + e^-z)
+ *         y_sorted_r = h_r W_down[e]^T
+ * n_src segment groups of E segments each (n_src = 1 on one GPU; n_src = G for the expert-parallel
+ * receive buffer, which is ordered by source rank then expert).
+ * x_sorted [rows,H], w_gate/w_up [E,d,H] (the expert's neurons = rows of the dense W_gate/W_up),
+ * w_down [E,H,d] (columns of the dense W_down), y_sorted [rows,H]; all of dtype dt.
+ * offsets: DEVICE int32 [n_src*E+1], non-decreasing, offsets[0] == 0, offsets[n_src*E] == rows.
+ * bf16: tcgen05 tensor cores, fp32 accumulation in TMEM, fp32 SiLU, h rounded once to bf16 (Q11), y
+ *       rounded once to bf16; requires H % 8 == 0 and d % 8 == 0.
+ * f32:  CUDA-core FMA in fp32 (no TF32), for the tiny config.
+ * Segments with no rows read no weights. ws: readme_expert_ffn_workspace_bytes(...) bytes. */
+size_t readme_expert_ffn_workspace_bytes(int64_t rows, int32_t H, int32_t E, int32_t d, readme_dtype dt);
+readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
+                                const void* w_up, const void* w_down, void* y_sorted, void* ws,
+                                size_t ws_bytes, readme_stream_t stream);
+
+/* a8: combine (Eq. 2's weighted sum):
+ *     y[t] = residual[t] + sum_{j<k} topk_w[t,j] * y_sorted[dest[t*k+j]]   (j ascending, fp32, Q8)
+ * topk_w is nullable iff k == 1 (weight 1); residual [T,H] nullable. With k == 1 and no residual the
+ * result is a bit copy. y_sorted [T*k,H], y [T,H] of dtype dt (residual too). */
+readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                             const int32_t* dest, const float* topk_w, const void* residual, void* y,
+                             uint32_t* dev_status, readme_stream_t stream);
+
+/* The whole layer (a1-a8).  If logits != NULL the plan (topk_idx..src) is computed and written; if
+ * logits == NULL the plan arrays are INPUTS from an earlier call (plan-in mode: route once per batch,
+ * reuse for every layer). x, residual, y: [T,H] of dtype dt; weights as in
+ * readme_expert_ffn. ws: readme_moe_layer_workspace_bytes(...) bytes. */
+size_t readme_moe_layer_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t d, int32_t k, readme_dtype dt);
+readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
+                               readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, const void* w_gate,
+                               const void* w_up, const void* w_down, const void* residual, void* y,
+                               int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
+                               int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                               readme_stream_t stream);
+
+/* Setup (once per model load, not on the timed path): expert slicing, PAPER.md:159-163 (M_i is a
+ * selection matrix without replacement).  dense_w_gate/up [D,H], dense_w_down [H,D] of dtype dt;
+ * neuron_idx DEVICE int32 [E,d], each row strictly increasing in [0,D) (violations set
+ * README_DEV_BAD_INDEX and the offending rows are zero-filled). Outputs w_gate/w_up [E,d,H],
+ * w_down [E,H,d]. Bit copies. */
+readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,
+                                   readme_dtype dt, int32_t D, int32_t H, int32_t E, int32_t d,
+                                   const int32_t* neuron_idx, void* w_gate, void* w_up, void* w_down,
+                                   uint32_t* dev_status, readme_stream_t stream);
+
+/* Helpers. */
+/* The library links its own (static) CUDA runtime: bind the calling host thread to `device` before
+ * calling the entry points above from that thread (the Python binding does this per call). */
+readme_status readme_set_device(int device);
+const char* readme_status_string(readme_status s);
+const char* readme_last_error(void); /* thread-local detail for the last non-OK return */
+int readme_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* README_B200_H_ */

@@ -1,0 +1,257 @@
+// capi.cu — the C ABI of libreadme_b200.so (include/readme.h): argument validation, workspace sizing
+// and stream-ordered launches of the kernels in route.cu / permute.cu / ffn_*.cu. No allocation, no host
+// synchronisation, no exception crosses the boundary.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <exception>
+#include <mutex>
+
+#include "kernels.h"
+
+#define README_VERSION 1
+
+namespace readme {
+
+namespace {
+thread_local char g_err[512] = {0};
+}
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+readme_status cuda_fail(cudaError_t e, const char* where) {
+  set_error("%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+  return README_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+namespace {
+
+readme_status check_route_args(int64_t T, int32_t E, int32_t k) {
+  README_CHECK_ARG(T >= 0, "T must be >= 0 (got %lld)", static_cast<long long>(T));
+  README_CHECK_ARG(E >= 1 && E <= README_MAX_EXPERTS, "E must be in [1, %d] (got %d)", README_MAX_EXPERTS, E);
+  README_CHECK_ARG(k >= 1 && k <= E, "k must be in [1, E] (got k=%d, E=%d)", k, E);
+  README_CHECK_ARG(T * static_cast<int64_t>(k) < (int64_t(1) << 31), "T*k must be < 2^31");
+  return README_OK;
+}
+
+readme_status check_rows(readme_dtype dt, int32_t H) {
+  if (dt != README_F32 && dt != README_BF16) {
+    set_error("unknown dtype %d", static_cast<int>(dt));
+    return README_ERR_UNSUPPORTED;
+  }
+  README_CHECK_ARG(H >= 8 && H % 8 == 0, "H must be a positive multiple of 8 (got %d)", H);
+  return README_OK;
+}
+
+#define README_TRY(expr)                \
+  do {                                  \
+    readme_status s_ = (expr);          \
+    if (s_ != README_OK) return s_;     \
+  } while (0)
+
+size_t ffn_ws_bytes(int64_t rows, int32_t d, readme_dtype dt) {
+  return align_up(static_cast<size_t>(rows) * d * dt_size(dt), 256) + 256;
+}
+
+}  // namespace
+}  // namespace readme
+
+using namespace readme;
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* readme_status_string(readme_status s) {
+  switch (s) {
+    case README_OK: return "README_OK";
+    case README_ERR_INVALID_ARG: return "README_ERR_INVALID_ARG";
+    case README_ERR_UNSUPPORTED: return "README_ERR_UNSUPPORTED";
+    case README_ERR_WORKSPACE: return "README_ERR_WORKSPACE";
+    case README_ERR_CUDA: return "README_ERR_CUDA";
+  }
+  return "README_ERR_UNKNOWN";
+}
+
+const char* readme_last_error(void) { return g_err; }
+
+int readme_version(void) { return README_VERSION; }
+
+readme_status readme_set_device(int device) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == device) return README_OK;
+  README_CUDA(cudaSetDevice(device));
+  return README_OK;
+}
+
+size_t readme_route_workspace_bytes(int64_t T, int32_t E, int32_t k) { return route_ws_bytes(T, E, k); }
+
+readme_status readme_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
+                           int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
+                           int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                           readme_stream_t stream) {
+  try {
+    README_TRY(check_route_args(T, E, k));
+    README_CHECK_ARG(counts && offsets, "counts and offsets are required");
+    if (T > 0) {
+      README_CHECK_ARG(logits && topk_idx && topk_w && dest, "logits, topk_idx, topk_w, dest are required");
+      README_CHECK_ARG(logits_dt == README_F32 || logits_dt == README_BF16, "logits_dt must be F32 or BF16");
+      README_CHECK_ARG(ws != nullptr, "workspace is required");
+      if (ws_bytes < route_ws_bytes(T, E, k)) {
+        set_error("route workspace too small: %zu < %zu", ws_bytes, route_ws_bytes(T, E, k));
+        return README_ERR_WORKSPACE;
+      }
+    }
+    return launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status, ws,
+                        reinterpret_cast<cudaStream_t>(stream));
+  } catch (const std::exception& e) {
+    set_error("exception: %s", e.what());
+    return README_ERR_CUDA;
+  } catch (...) {
+    set_error("unknown exception");
+    return README_ERR_CUDA;
+  }
+}
+
+readme_status readme_dispatch(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                              const int32_t* dest, void* x_sorted, uint32_t* dev_status, readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(T >= 0 && k >= 1 && T * static_cast<int64_t>(k) < (int64_t(1) << 31), "bad T/k");
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(x && dest && x_sorted, "x, dest and x_sorted are required");
+  README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x and x_sorted must be 16-byte aligned");
+  return launch_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, dest, x_sorted, dev_status,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t readme_expert_ffn_workspace_bytes(int64_t rows, int32_t H, int32_t E, int32_t d, readme_dtype dt) {
+  (void)H;
+  (void)E;
+  return ffn_ws_bytes(rows < 0 ? 0 : rows, d < 0 ? 0 : d, dt);
+}
+
+readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
+                                const void* w_up, const void* w_down, void* y_sorted, void* ws, size_t ws_bytes,
+                                readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(rows >= 0 && rows < (int64_t(1) << 31), "rows out of range");
+  README_CHECK_ARG(E >= 1 && E <= README_MAX_EXPERTS, "E must be in [1, %d]", README_MAX_EXPERTS);
+  README_CHECK_ARG(n_src >= 1 && static_cast<int64_t>(n_src) * E <= 512, "n_src*E must be in [1, 512]");
+  README_CHECK_ARG(d >= 8 && d % 8 == 0, "d must be a positive multiple of 8 (got %d)", d);
+  README_CHECK_ARG(offsets != nullptr, "offsets are required");
+  if (rows == 0) return README_OK;
+  README_CHECK_ARG(x_sorted && w_gate && w_up && w_down && y_sorted && ws, "null pointer argument");
+  README_CHECK_ARG(aligned16(x_sorted) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) &&
+                       aligned16(y_sorted) && aligned16(ws),
+                   "all tensors must be 16-byte aligned");
+  if (ws_bytes < ffn_ws_bytes(rows, d, dt)) {
+    set_error("expert_ffn workspace too small: %zu < %zu", ws_bytes, ffn_ws_bytes(rows, d, dt));
+    return README_ERR_WORKSPACE;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nseg = n_src * E;
+  if (dt == README_BF16) {
+    return launch_ffn_bf16(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, nseg, offsets,
+                           static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
+                           static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(y_sorted),
+                           static_cast<__nv_bfloat16*>(ws), st);
+  }
+  return launch_ffn_f32(static_cast<const float*>(x_sorted), rows, H, E, d, nseg, offsets,
+                        static_cast<const float*>(w_gate), static_cast<const float*>(w_up),
+                        static_cast<const float*>(w_down), static_cast<float*>(y_sorted), static_cast<float*>(ws),
+                        st);
+}
+
+readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                             const int32_t* dest, const float* topk_w, const void* residual, void* y,
+                             uint32_t* dev_status, readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(T >= 0 && k >= 1 && T * static_cast<int64_t>(k) < (int64_t(1) << 31), "bad T/k");
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(y_sorted && dest && y, "y_sorted, dest and y are required");
+  README_CHECK_ARG(k == 1 || topk_w, "topk_w is required when k > 1");
+  README_CHECK_ARG(aligned16(y_sorted) && aligned16(y) && (!residual || aligned16(residual)),
+                   "tensors must be 16-byte aligned");
+  return launch_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t readme_moe_layer_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t d, int32_t k, readme_dtype dt) {
+  if (T < 0 || k < 1 || H < 0) return 0;
+  const int64_t rows = T * k;
+  const size_t act = align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
+  return align_up(route_ws_bytes(T, E, k), 256) + 2 * act + ffn_ws_bytes(rows, d, dt);
+}
+
+readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
+                               readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, const void* w_gate,
+                               const void* w_up, const void* w_down, const void* residual, void* y,
+                               int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
+                               int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                               readme_stream_t stream) {
+  README_TRY(check_route_args(T, E, k));
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(d >= 8 && d % 8 == 0, "d must be a positive multiple of 8 (got %d)", d);
+  README_CHECK_ARG(counts && offsets, "counts and offsets are required");
+  if (T == 0) {
+    if (logits) return readme_route(nullptr, logits_dt, 0, E, k, nullptr, nullptr, counts, offsets, nullptr,
+                                    nullptr, dev_status, ws, ws_bytes, stream);
+    return README_OK;
+  }
+  README_CHECK_ARG(x && y && topk_idx && topk_w && dest && w_gate && w_up && w_down && ws,
+                   "null pointer argument");
+  const size_t need = readme_moe_layer_workspace_bytes(T, H, E, d, k, dt);
+  if (ws_bytes < need) {
+    set_error("moe_layer workspace too small: %zu < %zu", ws_bytes, need);
+    return README_ERR_WORKSPACE;
+  }
+  const int64_t rows = T * k;
+  char* w = static_cast<char*>(ws);
+  void* ws_route = w;
+  w += align_up(route_ws_bytes(T, E, k), 256);
+  void* x_sorted = w;
+  w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
+  void* y_sorted = w;
+  w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
+  void* ws_ffn = w;
+  if (logits) {
+    README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                            ws_route, route_ws_bytes(T, E, k), stream));
+  }
+  README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
+  README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
+                               ffn_ws_bytes(rows, d, dt), stream));
+  return readme_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status, stream);
+}
+
+readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,
+                                   readme_dtype dt, int32_t D, int32_t H, int32_t E, int32_t d,
+                                   const int32_t* neuron_idx, void* w_gate, void* w_up, void* w_down,
+                                   uint32_t* dev_status, readme_stream_t stream) {
+  README_CHECK_ARG(dt == README_F32 || dt == README_BF16, "dt must be F32 or BF16");
+  README_CHECK_ARG(D >= 1 && H >= 1 && E >= 1 && d >= 1 && d <= D, "bad D/H/E/d");
+  README_CHECK_ARG(dense_w_gate && dense_w_up && dense_w_down && neuron_idx && w_gate && w_up && w_down,
+                   "null pointer argument");
+  return launch_build_experts(dense_w_gate, dense_w_up, dense_w_down, dt, D, H, E, d, neuron_idx, w_gate, w_up,
+                              w_down, dev_status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,34 @@
+// kernels.h — internal launchers (host functions) behind the C ABI in capi.cu. Not exported.
+#pragma once
+#include "common.cuh"
+
+namespace readme {
+
+// route.cu
+size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
+readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
+                           int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
+                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st);
+
+// permute.cu
+readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
+                              void* x_sorted, uint32_t* dev_status, cudaStream_t st);
+readme_status launch_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                             const int32_t* dest, const float* topk_w, const void* residual, void* y,
+                             uint32_t* dev_status, cudaStream_t st);
+readme_status launch_build_experts(const void* wg, const void* wu, const void* wd, readme_dtype dt, int32_t D,
+                                   int32_t H, int32_t E, int32_t d, const int32_t* nidx, void* eg, void* eu,
+                                   void* ed, uint32_t* dev_status, cudaStream_t st);
+
+// ffn_f32.cu (SIMT fp32, no TF32)
+readme_status launch_ffn_f32(const float* xs, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                             const int32_t* offsets, const float* wg, const float* wu, const float* wd,
+                             float* ys, float* h_ws, cudaStream_t st);
+
+// ffn_sm100.cu (tcgen05 / TMEM / TMA grouped GEMMs, bf16)
+readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                              int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                              const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
+                              __nv_bfloat16* h_ws, cudaStream_t st);
+
+}  // namespace readme

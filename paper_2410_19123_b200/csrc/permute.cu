@@ -1,0 +1,219 @@
+// permute.cu — a5 dispatch, a8 combine and the setup-time expert slicing.
+//
+// dispatch  x_sorted[dest[s]] = x[s / k]                         (tokens grouped per expert)
+// combine   y[t] = res[t] + sum_{j<k} w[t,j] * y_sorted[dest[t*k+j]]   (Eq. 2's weighted sum)
+// slicing   W_gate,e = W_gate[S_e, :], W_up,e = W_up[S_e, :], W_down,e = W_down[:, S_e]
+//
+// All three are HBM-bound row moves. One warp per row; each lane keeps kUnroll 128-bit loads in flight
+// before storing (Little's law: ~6.4 TB/s x ~1 us needs ~45 KB in flight per SM; 64 warps x 32 lanes x
+// 4 x 16 B = 128 KB), L1 bypassed for the streamed source.
+#include "kernels.h"
+
+namespace readme {
+
+namespace {
+
+constexpr int kPermThreads = 256;
+constexpr int kUnroll = 4;
+
+// One warp moves one row of `vec` uint4 from src_row to dst_row.
+__device__ __forceinline__ void copy_row(const uint4* __restrict__ s, uint4* __restrict__ d, int vec, int lane) {
+  int i = lane;
+  for (; i + (kUnroll - 1) * kWarp < vec; i += kUnroll * kWarp) {
+    uint4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) r[u] = ld_nc_v4(s + i + u * kWarp);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_v4(d + i + u * kWarp, r[u]);
+  }
+  for (; i < vec; i += kWarp) st_v4(d + i, ld_nc_v4(s + i));
+}
+
+__global__ void __launch_bounds__(kPermThreads)
+dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, const int32_t* __restrict__ dest,
+                uint4* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; s < nslots;
+       s += warps) {
+    const int32_t r = __ldg(dest + s);
+    if (r < 0 || r >= nslots) {
+      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+      continue;
+    }
+    copy_row(x + (s / k) * vec, xs + static_cast<int64_t>(r) * vec, vec, lane);
+  }
+}
+
+// k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
+__global__ void __launch_bounds__(kPermThreads)
+gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
+              uint4* __restrict__ y, uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; t < T;
+       t += warps) {
+    const int32_t r = __ldg(dest + t);
+    if (r < 0 || r >= T) {
+      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+      continue;
+    }
+    copy_row(ys + static_cast<int64_t>(r) * vec, y + t * vec, vec, lane);
+  }
+}
+
+// General combine in fp32, j ascending (Q8), one rounding at the end. 8 elements per lane step.
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 v = ld_nc_v4(reinterpret_cast<const uint4*>(p));
+  f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+  f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z); f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 v;
+  v.x = pack_bf16x2(f[0], f[1]); v.y = pack_bf16x2(f[2], f[3]);
+  v.z = pack_bf16x2(f[4], f[5]); v.w = pack_bf16x2(f[6], f[7]);
+  st_v4(reinterpret_cast<uint4*>(p), v);
+}
+__device__ __forceinline__ void load8(const float* p, float (&f)[8]) {
+  const uint4 a = ld_nc_v4(reinterpret_cast<const uint4*>(p));
+  const uint4 b = ld_nc_v4(reinterpret_cast<const uint4*>(p) + 1);
+  f[0] = __uint_as_float(a.x); f[1] = __uint_as_float(a.y); f[2] = __uint_as_float(a.z); f[3] = __uint_as_float(a.w);
+  f[4] = __uint_as_float(b.x); f[5] = __uint_as_float(b.y); f[6] = __uint_as_float(b.z); f[7] = __uint_as_float(b.w);
+}
+__device__ __forceinline__ void store8(float* p, const float (&f)[8]) {
+  st_v4(reinterpret_cast<uint4*>(p), make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                                                __float_as_uint(f[2]), __float_as_uint(f[3])));
+  st_v4(reinterpret_cast<uint4*>(p) + 1, make_uint4(__float_as_uint(f[4]), __float_as_uint(f[5]),
+                                                    __float_as_uint(f[6]), __float_as_uint(f[7])));
+}
+
+template <typename Elt>
+__global__ void __launch_bounds__(kPermThreads)
+combine_kernel(const Elt* __restrict__ ys, int H, int64_t T, int k, const int32_t* __restrict__ dest,
+               const float* __restrict__ w, const Elt* __restrict__ res, Elt* __restrict__ y,
+               uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  const int groups = H / 8;
+  const int64_t nrows = T * k;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; t < T;
+       t += warps) {
+    for (int g = lane; g < groups; g += kWarp) {
+      float acc[8];
+      if (res) {
+        load8(res + t * H + g * 8, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      }
+      for (int j = 0; j < k; ++j) {
+        int32_t r = __ldg(dest + t * k + j);
+        if (r < 0 || r >= nrows) {
+          if (dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+          continue;
+        }
+        const float wj = w ? __ldg(w + t * k + j) : 1.0f;
+        float v[8];
+        load8(ys + static_cast<int64_t>(r) * H + g * 8, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wj, v[i], acc[i]);
+      }
+      store8(y + t * H + g * 8, acc);
+    }
+  }
+}
+
+// Expert slicing (setup, not on the timed path). Grid: (E*d) rows for gate/up, (E*H) rows for down.
+template <typename Elt>
+__global__ void slice_rows_kernel(const Elt* __restrict__ wg, const Elt* __restrict__ wu, int D, int H, int E,
+                                  int d, const int32_t* __restrict__ nidx, Elt* __restrict__ eg,
+                                  Elt* __restrict__ eu, uint32_t* __restrict__ dev_status) {
+  const int64_t row = blockIdx.x;  // e*d + n
+  const int e = static_cast<int>(row / d), n = static_cast<int>(row % d);
+  const int32_t s = nidx[row];
+  const bool ok = s >= 0 && s < D && (n == 0 || s > nidx[row - 1]);
+  if (!ok && threadIdx.x == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+  (void)e;
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    eg[row * H + c] = ok ? wg[static_cast<int64_t>(s) * H + c] : Elt(0.f);
+    eu[row * H + c] = ok ? wu[static_cast<int64_t>(s) * H + c] : Elt(0.f);
+  }
+}
+
+template <typename Elt>
+__global__ void slice_cols_kernel(const Elt* __restrict__ wd, int D, int H, int E, int d,
+                                  const int32_t* __restrict__ nidx, Elt* __restrict__ ed) {
+  const int64_t row = blockIdx.x;  // e*H + c
+  const int e = static_cast<int>(row / H), c = static_cast<int>(row % H);
+  for (int n = threadIdx.x; n < d; n += blockDim.x) {
+    const int32_t s = nidx[static_cast<int64_t>(e) * d + n];
+    const bool ok = s >= 0 && s < D && (n == 0 || s > nidx[static_cast<int64_t>(e) * d + n - 1]);
+    ed[row * d + n] = ok ? wd[static_cast<int64_t>(c) * D + s] : Elt(0.f);
+  }
+}
+
+int grid_for_rows(int64_t rows) {
+  const int64_t want = (rows + (kPermThreads / kWarp) - 1) / (kPermThreads / kWarp);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;  // 8 CTAs x 8 warps = 64 warps per SM
+  return static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+}  // namespace
+
+readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
+                              void* x_sorted, uint32_t* dev_status, cudaStream_t st) {
+  const int64_t nslots = T * k;
+  if (nslots == 0) return README_OK;
+  dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
+      static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
+      static_cast<uint4*>(x_sorted), dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                             const int32_t* dest, const float* topk_w, const void* residual, void* y,
+                             uint32_t* dev_status, cudaStream_t st) {
+  if (T == 0) return README_OK;
+  const int grid = grid_for_rows(T);
+  if (k == 1 && residual == nullptr) {
+    gather_kernel<<<grid, kPermThreads, 0, st>>>(static_cast<const uint4*>(y_sorted),
+                                                 static_cast<int>(H * dt_size(dt) / 16), T, dest,
+                                                 static_cast<uint4*>(y), dev_status);
+  } else if (dt == README_BF16) {
+    combine_kernel<__nv_bfloat16><<<grid, kPermThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(y_sorted), H, T, k, dest, topk_w,
+        static_cast<const __nv_bfloat16*>(residual), static_cast<__nv_bfloat16*>(y), dev_status);
+  } else {
+    combine_kernel<float><<<grid, kPermThreads, 0, st>>>(static_cast<const float*>(y_sorted), H, T, k, dest,
+                                                         topk_w, static_cast<const float*>(residual),
+                                                         static_cast<float*>(y), dev_status);
+  }
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_build_experts(const void* wg, const void* wu, const void* wd, readme_dtype dt, int32_t D,
+                                   int32_t H, int32_t E, int32_t d, const int32_t* nidx, void* eg, void* eu,
+                                   void* ed, uint32_t* dev_status, cudaStream_t st) {
+  const unsigned rows_gu = static_cast<unsigned>(static_cast<int64_t>(E) * d);
+  const unsigned rows_d = static_cast<unsigned>(static_cast<int64_t>(E) * H);
+  if (dt == README_BF16) {
+    slice_rows_kernel<__nv_bfloat16><<<rows_gu, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(wg), static_cast<const __nv_bfloat16*>(wu), D, H, E, d, nidx,
+        static_cast<__nv_bfloat16*>(eg), static_cast<__nv_bfloat16*>(eu), dev_status);
+    slice_cols_kernel<__nv_bfloat16><<<rows_d, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(wd), D, H, E, d,
+                                                             nidx, static_cast<__nv_bfloat16*>(ed));
+  } else {
+    slice_rows_kernel<float><<<rows_gu, 256, 0, st>>>(static_cast<const float*>(wg), static_cast<const float*>(wu),
+                                                     D, H, E, d, nidx, static_cast<float*>(eg),
+                                                     static_cast<float*>(eu), dev_status);
+    slice_cols_kernel<float><<<rows_d, 256, 0, st>>>(static_cast<const float*>(wd), D, H, E, d, nidx,
+                                                     static_cast<float*>(ed));
+  }
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+}  // namespace readme

@@ -1,0 +1,254 @@
+"""Thin Python binding over libreadme_b200.so (include/readme.h). Argument marshalling only: every step
+of the path runs in the library's CUDA kernels; PyTorch supplies device memory and streams.
+
+There is no CPU fallback: if the library is missing, or a tensor is not on a CUDA device, the call
+raises. Names follow the C ABI (route, dispatch, expert_ffn, combine, moe_layer, build_experts).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libreadme_b200.so")
+
+README_F32, README_BF16 = 0, 1
+README_DEV_NONFINITE_LOGIT, README_DEV_BAD_INDEX = 0x1, 0x2
+STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTED", 3: "README_ERR_WORKSPACE",
+          4: "README_ERR_CUDA"}
+
+# Every symbol include/readme.h declares (tests check the library exports exactly these).
+EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
+           "readme_expert_ffn", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
+           "readme_build_experts", "readme_set_device", "readme_status_string", "readme_last_error",
+           "readme_version")
+
+
+class ReadmeError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} -> {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+_tls = threading.local()
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_SIGS = {
+    "readme_route_workspace_bytes": (_sz, [_i64, _i32, _i32]),
+    "readme_route": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                    _vp]),
+    "readme_dispatch": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "readme_expert_ffn_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, ctypes.c_int]),
+    "readme_expert_ffn": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                                         _vp, _sz, _vp]),
+    "readme_combine": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "readme_moe_layer_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, _i32, ctypes.c_int]),
+    "readme_moe_layer": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _vp, ctypes.c_int, _i32, _i32, _i32, _vp, _vp,
+                                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "readme_build_experts": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                                            _vp, _vp]),
+    "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
+    "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "readme_last_error": (ctypes.c_char_p, []),
+    "readme_version": (ctypes.c_int, []),
+}
+
+
+def lib():
+    """Load libreadme_b200.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2410_19123_b200.build` "
+                                  "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_LOCAL)
+            for name, (res, args) in _SIGS.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(fn: str, rc: int):
+    if rc != 0:
+        raise ReadmeError(fn, rc, lib().readme_last_error().decode(errors="replace"))
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return README_BF16
+    if t.dtype == torch.float32:
+        return README_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _prep(*tensors):
+    """All tensors must be contiguous CUDA tensors on one device; binds the library's thread to it and
+    returns the current torch stream handle."""
+    dev = None
+    for t in tensors:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("readme: tensors must live on a CUDA device (no CPU path exists)")
+        if not t.is_contiguous():
+            raise ValueError("readme: tensors must be contiguous")
+        if dev is None:
+            dev = t.device.index
+        elif t.device.index != dev:
+            raise ValueError("readme: tensors on different devices")
+    if dev is None:
+        dev = torch.cuda.current_device()
+    if getattr(_tls, "dev", None) != dev:
+        _check("readme_set_device", lib().readme_set_device(dev))
+        _tls.dev = dev
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+@dataclass
+class Plan:
+    """The routing plan (a1-a4): computed once per batch, reused by every layer (a9)."""
+    topk_idx: torch.Tensor   # [T,k] int32
+    topk_w: torch.Tensor     # [T,k] f32
+    counts: torch.Tensor     # [E] int32
+    offsets: torch.Tensor    # [E+1] int32
+    dest: torch.Tensor       # [T*k] int32
+    src: torch.Tensor        # [T*k] int32
+    dev_status: torch.Tensor  # [1] int32 (uint32 bits)
+
+    @property
+    def k(self) -> int:
+        return self.topk_idx.shape[1]
+
+
+def new_plan(T: int, E: int, k: int, device) -> Plan:
+    i32 = dict(dtype=torch.int32, device=device)
+    return Plan(torch.empty((T, k), **i32), torch.empty((T, k), dtype=torch.float32, device=device),
+                torch.empty(E, **i32), torch.empty(E + 1, **i32), torch.empty(T * k, **i32),
+                torch.empty(T * k, **i32), torch.zeros(1, **i32))
+
+
+def route_workspace_bytes(T: int, E: int, k: int) -> int:
+    return int(lib().readme_route_workspace_bytes(T, E, k))
+
+
+def route(logits: torch.Tensor, k: int, plan: Plan | None = None, ws: torch.Tensor | None = None) -> Plan:
+    """a1-a4 on the device: top-k ids/weights, counts, offsets, dest, src (readme_route)."""
+    T, E = logits.shape
+    plan = plan or new_plan(T, E, k, logits.device)
+    need = route_workspace_bytes(T, E, k)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
+    st = _prep(logits, plan.topk_idx, ws)
+    _check("readme_route", lib().readme_route(
+        _ptr(logits), _dt(logits), T, E, k, _ptr(plan.topk_idx), _ptr(plan.topk_w), _ptr(plan.counts),
+        _ptr(plan.offsets), _ptr(plan.dest), _ptr(plan.src), _ptr(plan.dev_status), _ptr(ws), ws.numel(), st))
+    return plan
+
+
+def dispatch(x: torch.Tensor, dest: torch.Tensor, k: int, out: torch.Tensor | None = None,
+             dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """a5: x_sorted[dest[s]] = x[s // k] (readme_dispatch)."""
+    T, H = x.shape
+    out = out if out is not None else torch.empty((T * k, H), dtype=x.dtype, device=x.device)
+    st = _prep(x, dest, out, dev_status)
+    _check("readme_dispatch", lib().readme_dispatch(_ptr(x), _dt(x), T, H, k, _ptr(dest), _ptr(out),
+                                                    _ptr(dev_status), st))
+    return out
+
+
+def expert_ffn_workspace_bytes(rows: int, H: int, E: int, d: int, dtype: torch.dtype) -> int:
+    return int(lib().readme_expert_ffn_workspace_bytes(rows, H, E, d,
+                                                       README_BF16 if dtype == torch.bfloat16 else README_F32))
+
+
+def expert_ffn(x_sorted: torch.Tensor, offsets: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor,
+               w_down: torch.Tensor, n_src: int = 1, out: torch.Tensor | None = None,
+               ws: torch.Tensor | None = None) -> torch.Tensor:
+    """a6-a7: grouped SwiGLU expert FFN over expert-contiguous rows (readme_expert_ffn)."""
+    rows, H = x_sorted.shape
+    E, d, H2 = w_gate.shape
+    if H2 != H or tuple(w_up.shape) != (E, d, H) or tuple(w_down.shape) != (E, H, d):
+        raise ValueError("weight shapes must be w_gate/w_up [E,d,H] and w_down [E,H,d]")
+    if not (x_sorted.dtype == w_gate.dtype == w_up.dtype == w_down.dtype):
+        raise TypeError("x_sorted and weights must share a dtype")
+    out = out if out is not None else torch.empty((rows, H), dtype=x_sorted.dtype, device=x_sorted.device)
+    need = expert_ffn_workspace_bytes(rows, H, E, d, x_sorted.dtype)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x_sorted.device)
+    st = _prep(x_sorted, offsets, w_gate, w_up, w_down, out, ws)
+    _check("readme_expert_ffn", lib().readme_expert_ffn(
+        _ptr(x_sorted), _dt(x_sorted), rows, H, E, d, n_src, _ptr(offsets), _ptr(w_gate), _ptr(w_up),
+        _ptr(w_down), _ptr(out), _ptr(ws), ws.numel(), st))
+    return out
+
+
+def combine(y_sorted: torch.Tensor, dest: torch.Tensor, topk_w: torch.Tensor | None, k: int,
+            residual: torch.Tensor | None = None, out: torch.Tensor | None = None,
+            dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """a8: y[t] = residual[t] + sum_j w[t,j] * y_sorted[dest[t*k+j]] (readme_combine)."""
+    rows, H = y_sorted.shape
+    T = rows // k
+    out = out if out is not None else torch.empty((T, H), dtype=y_sorted.dtype, device=y_sorted.device)
+    st = _prep(y_sorted, dest, topk_w, residual, out, dev_status)
+    _check("readme_combine", lib().readme_combine(_ptr(y_sorted), _dt(y_sorted), T, H, k, _ptr(dest), _ptr(topk_w),
+                                                  _ptr(residual), _ptr(out), _ptr(dev_status), st))
+    return out
+
+
+def moe_layer_workspace_bytes(T: int, H: int, E: int, d: int, k: int, dtype: torch.dtype) -> int:
+    return int(lib().readme_moe_layer_workspace_bytes(T, H, E, d, k,
+                                                      README_BF16 if dtype == torch.bfloat16 else README_F32))
+
+
+def moe_layer(x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor, k: int = 1,
+              logits: torch.Tensor | None = None, plan: Plan | None = None, residual: torch.Tensor | None = None,
+              out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> tuple[torch.Tensor, Plan]:
+    """The whole layer (readme_moe_layer). With `logits` the plan is computed (into `plan` if given);
+    with logits=None, `plan` is an input (route once, reuse for every layer)."""
+    T, H = x.shape
+    E, d, _ = w_gate.shape
+    if logits is None and plan is None:
+        raise ValueError("moe_layer needs logits or a plan")
+    if plan is None:
+        plan = new_plan(T, E, k, x.device)
+    k = plan.k
+    out = out if out is not None else torch.empty_like(x)
+    need = moe_layer_workspace_bytes(T, H, E, d, k, x.dtype)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    st = _prep(x, w_gate, w_up, w_down, logits, residual, out, ws, plan.dest)
+    _check("readme_moe_layer", lib().readme_moe_layer(
+        _ptr(x), _dt(x), T, H, _ptr(logits), _dt(logits) if logits is not None else README_F32, E, k, d,
+        _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(residual), _ptr(out), _ptr(plan.topk_idx),
+        _ptr(plan.topk_w), _ptr(plan.counts), _ptr(plan.offsets), _ptr(plan.dest), _ptr(plan.src),
+        _ptr(plan.dev_status), _ptr(ws), ws.numel(), st))
+    return out, plan
+
+
+def build_experts(dense_w_gate: torch.Tensor, dense_w_up: torch.Tensor, dense_w_down: torch.Tensor,
+                  neuron_idx: torch.Tensor, dev_status: torch.Tensor | None = None):
+    """Setup: slice expert stacks from the dense FFN (readme_build_experts). Returns (w_gate, w_up, w_down)."""
+    D, H = dense_w_gate.shape
+    E, d = neuron_idx.shape
+    kw = dict(dtype=dense_w_gate.dtype, device=dense_w_gate.device)
+    wg = torch.empty((E, d, H), **kw)
+    wu = torch.empty((E, d, H), **kw)
+    wd = torch.empty((E, H, d), **kw)
+    st = _prep(dense_w_gate, dense_w_up, dense_w_down, neuron_idx, wg, wu, wd, dev_status)
+    _check("readme_build_experts", lib().readme_build_experts(
+        _ptr(dense_w_gate), _ptr(dense_w_up), _ptr(dense_w_down), _dt(dense_w_gate), D, H, E, d, _ptr(neuron_idx),
+        _ptr(wg), _ptr(wu), _ptr(wd), _ptr(dev_status), st))
+    return wg, wu, wd

@@ -1,0 +1,337 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI, against the CPU oracle on the same
+seeded inputs. Rules (BASELINE.json north_star):
+  routing integers (topk_idx, counts, offsets, dest, src): bit-exact;
+  dispatch and k=1 combine: bit copies;
+  FP outputs: per-token inf-norm relative error <= 2e-2 (bf16) / <= 1e-4 (fp32); topk_w fp32 rule,
+  and exactly 1.0f for k=1.
+Sizes span several tiles and ragged tails; full-size config 2 is checked on sampled tokens."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.tolerances import BF16_TOL, F32_TOL, rel_err
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def rd():
+    from paper_2410_19123_b200 import build, readme
+    build.build()
+    readme.lib()
+    return readme
+
+
+def _np(t):
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        t = t.float()
+    return t.numpy()
+
+
+def _check_plan(plan, ref, k):
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(plan.topk_idx), ref["topk_idx"])
+    assert np.array_equal(_np(plan.counts), ref["counts"])
+    assert np.array_equal(_np(plan.offsets), ref["offsets"])
+    assert np.array_equal(_np(plan.dest), ref["dest"])
+    assert np.array_equal(_np(plan.src), ref["src"])
+    w = _np(plan.topk_w).astype(np.float64)
+    if k == 1:
+        assert np.all(w == 1.0)
+    else:
+        assert np.max(np.abs(w - ref["topk_w"])) <= F32_TOL
+
+
+# ---- a1-a4 route -----------------------------------------------------------------------------------
+
+ROUTE_CASES = [
+    (8192, 8, 1, "normal", "f32"),
+    (8192, 8, 1, "ties", "f32"),
+    (1000, 8, 2, "normal", "f32"),   # T not a multiple of the tile
+    (1, 8, 1, "normal", "f32"),
+    (4097, 1, 1, "normal", "f32"),   # E = 1
+    (3000, 256, 4, "normal", "f32"),  # max experts
+    (777, 5, 5, "ties", "f32"),      # k = E
+    (5000, 8, 1, "normal", "bf16"),
+    (65536, 8, 1, "normal", "f32"),
+    (2000, 33, 3, "ties", "bf16"),
+]
+
+
+@pytest.mark.parametrize("T,E,k,kind,ldt", ROUTE_CASES)
+def test_route_bit_exact(rd, T, E, k, kind, ldt):
+    lg = synth.router_logits(T, E, seed=T + E) if kind == "normal" else synth.near_tie_logits(T, E, seed=T + E)
+    lg_t = synth.to_torch(lg, ldt)
+    ref = oracle.route(lg_t, k)  # the oracle sees exactly the bits the GPU sees
+    plan = rd.route(lg_t.to(DEV), k)
+    _check_plan(plan, ref, k)
+    assert int(plan.dev_status.item()) == 0
+
+
+def test_route_locality_runs(rd):
+    ids = synth.assignments_markov(4, 4096, 8, 0.672)
+    lg = synth.logits_for_assignments(ids, 8)
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 1)
+    _check_plan(plan, oracle.route(lg, 1), 1)
+    assert np.array_equal(_np(plan.topk_idx)[:, 0], ids)
+
+
+def test_route_single_expert_all_tokens(rd):
+    lg = np.zeros((3000, 8), np.float32)
+    lg[:, 5] = 1.0
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 1)
+    _check_plan(plan, oracle.route(lg, 1), 1)
+
+
+def test_route_T0(rd):
+    plan = rd.new_plan(0, 8, 1, DEV)
+    plan.counts.fill_(7)
+    plan.offsets.fill_(7)
+    rd.route(torch.zeros((0, 8), device=DEV), 1, plan=plan)
+    torch.cuda.synchronize()
+    assert plan.counts.tolist() == [0] * 8 and plan.offsets.tolist() == [0] * 9
+
+
+def test_route_nonfinite_flag(rd):
+    lg = synth.router_logits(600, 8)
+    lg[17, 3] = np.nan
+    lg[400, 0] = np.inf
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 2)
+    torch.cuda.synchronize()
+    assert int(plan.dev_status.item()) & rd.README_DEV_NONFINITE_LOGIT
+    idx = _np(plan.topk_idx)
+    assert idx.min() >= 0 and idx.max() < 8
+    # permutation still valid
+    assert np.array_equal(np.sort(_np(plan.dest)), np.arange(1200))
+
+
+def test_route_deterministic(rd):
+    lg = torch.from_numpy(synth.router_logits(20000, 8)).to(DEV)
+    a = rd.route(lg, 2)
+    b = rd.route(lg, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(a.dest, b.dest) and torch.equal(a.topk_w, b.topk_w)
+
+
+# ---- a5 dispatch / a8 combine -----------------------------------------------------------------------
+
+@pytest.mark.parametrize("T,H,k,dt", [(1000, 4096, 1, "bf16"), (333, 264, 2, "bf16"), (256, 64, 1, "f32"),
+                                      (100, 72, 3, "f32")])
+def test_dispatch_bit_exact(rd, T, H, k, dt):
+    x = synth.to_torch(synth.tokens(T, H, seed=T), dt)
+    ref_plan = oracle.route(synth.router_logits(T, 8, seed=T + 1), k)
+    dest = torch.from_numpy(ref_plan["dest"]).to(DEV)
+    xs = rd.dispatch(x.to(DEV), dest, k)
+    ref = oracle.dispatch(x, ref_plan["dest"], k)
+    assert np.array_equal(_np(xs).astype(np.float64), ref)
+
+
+def test_combine_k1_is_bit_gather(rd):
+    T, H = 2000, 4096
+    ys = synth.to_torch(synth.tokens(T, H, seed=3), "bf16").to(DEV)
+    plan = oracle.route(synth.router_logits(T, 8, seed=4), 1)
+    y = rd.combine(ys, torch.from_numpy(plan["dest"]).to(DEV), None, 1)
+    ys_np = _np(ys)
+    assert np.array_equal(_np(y), ys_np[plan["dest"]])
+
+
+@pytest.mark.parametrize("dt,k", [("bf16", 2), ("f32", 2), ("bf16", 1), ("f32", 4)])
+def test_combine_weighted_residual(rd, dt, k):
+    T, H, E = 700, 256, 8
+    ys = synth.to_torch(synth.tokens(T * k, H, seed=5), dt)
+    res = synth.to_torch(synth.residual(T, H, seed=6), dt)
+    plan = oracle.route(synth.router_logits(T, E, seed=7), k)
+    gplan = rd.route(torch.from_numpy(synth.router_logits(T, E, seed=7)).to(DEV), k)
+    y = rd.combine(ys.to(DEV), gplan.dest, gplan.topk_w, k, residual=res.to(DEV))
+    # teacher-forced: the oracle combines the same y_sorted with its own (bit-identical) plan
+    ref = oracle.combine(ys.double().numpy(), plan["dest"], plan["topk_w"], k, residual=res)
+    assert rel_err(_np(y), ref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+# ---- a6-a7 expert FFN --------------------------------------------------------------------------------
+
+def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
+    x = synth.to_torch(synth.tokens(T, H, seed=seed), dt)
+    if skew == "empty":
+        ids = synth.assignments_unique(T, max(1, E // 2), E, seed=seed)
+        lg = synth.logits_for_assignments(ids, E, seed=seed)
+    elif skew == "zipf":
+        lg = synth.logits_for_assignments(synth.assignments_zipf(T, E, 2.0, seed=seed), E, seed=seed)
+    else:
+        lg = synth.router_logits(T, E, seed=seed)
+    wg, wu, wd = (synth.to_torch(w, dt) for w in synth.expert_weights(E, d, H, seed=seed))
+    return x, lg, wg, wu, wd
+
+
+@pytest.mark.parametrize("T,H,d,E,k,skew", [
+    (1000, 256, 384, 8, 1, None),      # several M/N tiles, ragged segments
+    (700, 512, 264, 8, 2, "empty"),    # empty experts, N tails (264 = 2*128 + 8), k = 2
+    (300, 128, 136, 3, 1, "zipf"),     # H < BN, K = 2 x 64
+    (2048, 4096, 512, 8, 1, None),     # Llama-2 H, K = 64 x 64
+    (129, 72, 40, 2, 1, None),         # K tail (72 = 64 + 8), d tiny
+])
+def test_expert_ffn_bf16_teacher_forced(rd, T, H, d, E, k, skew):
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + H, skew=skew)
+    plan = rd.route(torch.from_numpy(lg).to(DEV), k)
+    xs = rd.dispatch(x.to(DEV), plan.dest, k)
+    ys = rd.expert_ffn(xs, plan.offsets, wg.to(DEV), wu.to(DEV), wd.to(DEV))
+    torch.cuda.synchronize()
+    ref = oracle.expert_ffn(xs.cpu(), plan.offsets.cpu().numpy(), wg, wu, wd)
+    assert rel_err(_np(ys), ref) <= BF16_TOL
+
+
+def test_expert_ffn_f32_config1(rd):
+    c = synth.CONFIGS[1]
+    T, H, d, E, k = c["T"], c["H"], c["d"], c["E"], c["k"]
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "f32", seed=synth.MASTER_SEED + 1)
+    plan = rd.route(torch.from_numpy(lg).to(DEV), k)
+    xs = rd.dispatch(x.to(DEV), plan.dest, k)
+    ys = rd.expert_ffn(xs, plan.offsets, wg.to(DEV), wu.to(DEV), wd.to(DEV))
+    ref = oracle.expert_ffn(xs.cpu(), plan.offsets.cpu().numpy(), wg, wu, wd)
+    assert rel_err(_np(ys), ref) <= F32_TOL
+
+
+def test_expert_ffn_segments_n_src(rd):
+    """EP receive layout: n_src groups of E segments, expert = segment % E."""
+    H, d, E, G = 256, 128, 4, 3
+    rows = 900
+    xs = synth.to_torch(synth.tokens(rows, H, seed=9), "bf16")
+    wg, wu, wd = (synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=10))
+    cuts = np.sort(synth.rng(11, 0).integers(0, rows, size=G * E - 1))
+    off = np.concatenate([[0], cuts, [rows]]).astype(np.int32)
+    ys = rd.expert_ffn(xs.to(DEV), torch.from_numpy(off).to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), n_src=G)
+    ref = oracle.expert_ffn(xs, off, wg, wu, wd, n_src=G)
+    assert rel_err(_np(ys), ref) <= BF16_TOL
+
+
+# ---- whole layer -------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
+                                           ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2)])
+def test_moe_layer_end_to_end(rd, dt, T, H, d, E, k):
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
+    res = synth.to_torch(synth.residual(T, H, seed=12), dt)
+    y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k,
+                           logits=torch.from_numpy(lg).to(DEV), residual=res.to(DEV))
+    yref, pref = oracle.moe_layer(x, lg, k, wg, wu, wd, residual=res)
+    _check_plan(plan, pref, k)
+    assert rel_err(_np(y), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+def test_moe_layer_plan_in_equals_route(rd):
+    T, H, d, E = 800, 256, 256, 8
+    x, lg, wg, wu, wd = (t.to(DEV) if isinstance(t, torch.Tensor) else t
+                         for t in _ffn_case(T, H, d, E, 1, "bf16", seed=21))
+    y1, plan = rd.moe_layer(x, wg, wu, wd, logits=torch.from_numpy(lg).to(DEV))
+    y2, _ = rd.moe_layer(x, wg, wu, wd, plan=plan)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+
+
+def test_full_expert_equals_dense_gpu(rd):
+    """P1 on the GPU: experts whose neuron set is the whole dense FFN reproduce the dense FFN."""
+    T, H, D, E = 512, 256, 384, 4
+    wg, wu, wd = synth.dense_ffn_weights(D, H, D, seed=31)
+    S = synth.neuron_sets(E, D, D, mode="full")
+    g = [synth.to_torch(w, "bf16").to(DEV) for w in (wg, wu, wd)]
+    eg, eu, ed = rd.build_experts(*g, torch.from_numpy(S).to(DEV))
+    x = synth.to_torch(synth.tokens(T, H, seed=32), "bf16")
+    y, _ = rd.moe_layer(x.to(DEV), eg, eu, ed, logits=torch.from_numpy(synth.router_logits(T, E, seed=33)).to(DEV))
+    yd = oracle.dense_ffn(x, *(t.cpu() for t in g))
+    assert rel_err(_np(y), yd) <= BF16_TOL
+
+
+def test_build_experts_bit_exact(rd):
+    D, H, E, d = 1000, 264, 8, 504
+    wg, wu, wd = (synth.to_torch(w, "bf16") for w in synth.dense_ffn_weights(D, H, d, seed=41))
+    S = synth.neuron_sets(E, D, d, seed=42)
+    eg, eu, ed = rd.build_experts(wg.to(DEV), wu.to(DEV), wd.to(DEV), torch.from_numpy(S).to(DEV))
+    ref = oracle.build_experts(wg, wu, wd, S)
+    for got, want in zip((eg, eu, ed), ref):
+        assert np.array_equal(_np(got).astype(np.float64), want)
+
+
+def test_permutation_equivariance_bitwise_gpu(rd):
+    """P4/P13: permuting tokens permutes outputs bitwise (fixed K order, no split-K)."""
+    T, H, d, E = 1200, 512, 384, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=51)
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    y, plan = rd.moe_layer(x.to(DEV), *W, logits=torch.from_numpy(lg).to(DEV))
+    perm = torch.from_numpy(synth.rng(52, 0).permutation(T))
+    yp, planp = rd.moe_layer(x[perm].to(DEV), *W, logits=torch.from_numpy(lg[perm.numpy()]).to(DEV))
+    torch.cuda.synchronize()
+    assert torch.equal(yp.cpu(), y.cpu()[perm])
+    assert torch.equal(plan.counts, planp.counts)
+
+
+def test_scaling_exact_gpu(rd):
+    """P10: W_down * 2 -> y * 2 exactly."""
+    T, H, d, E = 500, 256, 256, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=61)
+    lgt = torch.from_numpy(lg).to(DEV)
+    y, _ = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), logits=lgt)
+    y2, _ = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), (wd * 2).to(DEV), logits=lgt)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y * 2)
+
+
+def test_zero_input_gpu(rd):
+    T, H, d, E = 300, 256, 128, 8
+    _, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=71)
+    y, _ = rd.moe_layer(torch.zeros((T, H), dtype=torch.bfloat16, device=DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV),
+                        logits=torch.from_numpy(lg).to(DEV))
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(y).item() == 0
+
+
+def test_cuda_graph_capture(rd):
+    T, H, d, E = 1024, 512, 256, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=81)
+    x, wg, wu, wd = (t.to(DEV) for t in (x, wg, wu, wd))
+    lgt = torch.from_numpy(lg).to(DEV)
+    plan = rd.new_plan(T, E, 1, DEV)
+    out = torch.empty_like(x)
+    ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, 1, x.dtype), dtype=torch.uint8, device=DEV)
+    y_eager, _ = rd.moe_layer(x, wg, wu, wd, logits=lgt)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        rd.moe_layer(x, wg, wu, wd, logits=lgt, plan=plan, out=out, ws=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rd.moe_layer(x, wg, wu, wd, logits=lgt, plan=plan, out=out, ws=ws)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, y_eager)
+
+
+# ---- full size (config 2) on sampled tokens ------------------------------------------------------------
+
+def test_config2_full_size_sampled(rd):
+    c = synth.CONFIGS[2]
+    T, H, D, d, E = c["T"], c["H"], c["D"], c["d"], c["E"]
+    seed = synth.MASTER_SEED + 2
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
+    S = synth.neuron_sets(E, D, d, seed=seed)
+    dense = [synth.to_torch(w, "bf16") for w in (wg, wu, wd)]
+    del wg, wu, wd
+    eg, eu, ed = rd.build_experts(*(t.to(DEV) for t in dense), torch.from_numpy(S).to(DEV))
+    x = synth.to_torch(synth.tokens(T, H, seed=seed), "bf16")
+    lg = synth.router_logits(T, E, seed=seed)
+    y, plan = rd.moe_layer(x.to(DEV), eg, eu, ed, logits=torch.from_numpy(lg).to(DEV))
+    torch.cuda.synchronize()
+    pref = oracle.route(lg, 1)
+    _check_plan(plan, pref, 1)
+    # 8 sampled tokens per expert, evaluated by brute force straight from the dense weights
+    idx = pref["topk_idx"][:, 0]
+    g = synth.rng(seed, 99)
+    sample = np.concatenate([g.choice(np.nonzero(idx == e)[0], size=8, replace=False) for e in range(E)])
+    yb = oracle.bruteforce(x[sample], lg[sample], 1, *dense, S)
+    assert rel_err(_np(y)[sample], yb) <= BF16_TOL
