@@ -152,9 +152,10 @@ def cpu_baseline(cfg, inp, budget_s=15.0):
         oracle.moe_layer(inp["x"][sample], lg[sample], cfg["k"], eg, eu, ed, nthreads=threads)
         return time.perf_counter() - t0, sample.size
 
-    dt, n = run(1)
+    dt, n = run(4)  # calibration (32 tokens)
     per_tok = dt / n
-    n_e = max(1, min(64, int(budget_s / per_tok / E)))
+    cap = int(min(np.bincount(idx, minlength=E)))
+    n_e = max(1, min(cap, int(budget_s / per_tok / E)))
     dt, n = run(n_e)
     del dense
     return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "oracle",

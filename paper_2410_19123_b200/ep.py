@@ -1,0 +1,142 @@
+"""Expert parallelism over one NVLink/NVSwitch box: experts sharded by GPU, tokens
+data-parallel, dispatch/combine as NCCL all-to-all.
+
+Partitioning: rank r holds its own batch of T_r tokens and routes them locally with the (replicated)
+pre-gating logits; rank q owns experts [q*E/G, (q+1)*E/G) and only their weights. Because the router is
+independent of the layer, the per-destination split sizes are fixed for the
+whole batch: ONE count exchange (C1) per batch, then per layer one all-to-all each way (C2 dispatch,
+C3 combine). This is the system advantage the paper claims over layer-wise routers.
+
+Local route sorts rows by expert, which (experts contiguous per rank) is already by destination rank, so
+the send buffer is x_sorted itself. Rows arrive in source-rank order; the receive buffer is therefore
+G groups of E_local segments, segment g -> local expert g % E_local, which readme_expert_ffn takes
+directly through its n_src argument (no second local permutation). Each expert's rows arrive in global
+token order, so EP output equals the single-GPU output bit for bit (P12).
+
+Host logic (plan_from_counts, exchange) is device-agnostic and is exercised with gloo on CPU in
+tests/test_ep_gloo.py; the GPU layer (EPMoELayer) runs every compute step in libreadme_b200 kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class EPPlan:
+    G: int
+    rank: int
+    E: int
+    E_local: int
+    send_splits: list      # rows this rank sends to each rank q (= its rows for q's experts)
+    recv_splits: list      # rows this rank receives from each source p
+    recv_counts: np.ndarray  # [G, E_local] rows from source p for local expert e
+    seg_offsets: np.ndarray  # [G*E_local + 1] exclusive scan of recv_counts (source-major)
+
+    @property
+    def rows_in(self) -> int:
+        return int(self.seg_offsets[-1])
+
+
+def plan_from_counts(counts_local, group=None) -> EPPlan:
+    """C1: exchange per-expert counts once per batch. `counts_local` is this rank's [E] int32 histogram
+    (any device the process group's backend accepts). Returns host-side split lists and segment table."""
+    G = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    E = counts_local.numel()
+    if E % G:
+        raise ValueError(f"E={E} experts cannot be sharded over {G} ranks")
+    El = E // G
+    send = counts_local.reshape(G, El).contiguous()
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)  # recv[p, e] = rows source p has for my expert e
+    send_h = send.cpu().numpy().astype(np.int64)
+    recv_h = recv.cpu().numpy().astype(np.int64)
+    seg = np.zeros(G * El + 1, np.int64)
+    seg[1:] = np.cumsum(recv_h.reshape(-1))
+    return EPPlan(G=G, rank=rank, E=E, E_local=El, send_splits=send_h.sum(axis=1).tolist(),
+                  recv_splits=recv_h.sum(axis=1).tolist(), recv_counts=recv_h, seg_offsets=seg)
+
+
+def exchange(rows: torch.Tensor, plan: EPPlan, reverse: bool = False, out: torch.Tensor | None = None,
+             group=None) -> torch.Tensor:
+    """C2 (dispatch, reverse=False): send my expert-sorted rows to their experts' owners, receive rows in
+    source-rank order. C3 (combine, reverse=True): the mirror image."""
+    in_s, out_s = (plan.recv_splits, plan.send_splits) if reverse else (plan.send_splits, plan.recv_splits)
+    n_out = int(sum(out_s))
+    if out is None:
+        out = torch.empty((n_out,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    dist.all_to_all_single(out, rows, output_split_sizes=out_s, input_split_sizes=in_s, group=group)
+    return out
+
+
+class EPMoELayer:
+    """One expert-parallel pre-gated MoE layer on this rank's GPU (NCCL process group)."""
+
+    def __init__(self, x, logits, w_gate, w_up, w_down, E: int, k: int, group=None):
+        from . import readme as rd
+        self.rd = rd
+        self.group = group
+        self.x, self.logits = x, logits
+        self.w = (w_gate, w_up, w_down)
+        self.E, self.k = E, k
+        T, H = x.shape
+        self.T, self.H = T, H
+        self.d = w_gate.shape[1]
+        dev = x.device
+        self.plan = rd.new_plan(T, E, k, dev)
+        self.ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
+        self.xs = torch.empty((T * k, H), dtype=x.dtype, device=dev)
+        self.ys = torch.empty_like(self.xs)
+        self.y = torch.empty_like(x)
+        self.ep = None
+
+    @classmethod
+    def from_config(cls, cfg: dict, T: int, group, device):
+        """Synthetic config-5 layer: this rank's tokens/logits and its shard of the experts."""
+        import synth
+        from . import readme as rd
+        G, rank = dist.get_world_size(group), dist.get_rank(group)
+        H, D, d, E, k = cfg["H"], cfg["D"], cfg["d"], cfg["E"], cfg["k"]
+        El = E // G
+        seed = synth.MASTER_SEED + 5
+        wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
+        S = synth.neuron_sets(E, D, d, seed=seed)[rank * El:(rank + 1) * El]
+        dense = [synth.to_torch(w, "bf16").to(device) for w in (wg, wu, wd)]
+        del wg, wu, wd
+        eg, eu, ed = rd.build_experts(*dense, torch.from_numpy(np.ascontiguousarray(S)).to(device))
+        del dense
+        x = synth.to_torch(synth.tokens(T, H, seed=seed + 1000 * rank), "bf16").to(device)
+        lg = torch.from_numpy(synth.router_logits(T, E, seed=seed + 1000 * rank)).to(device)
+        return cls(x, lg, eg, eu, ed, E, k, group)
+
+    def route(self):
+        """Once per batch: local routing plan + C1 count exchange (the only device->host sync)."""
+        self.rd.route(self.logits, self.k, plan=self.plan, ws=self.ws_r)
+        self.ep = plan_from_counts(self.plan.counts, self.group)
+        self.seg_dev = torch.from_numpy(self.ep.seg_offsets.astype(np.int32)).to(self.x.device)
+        rows = self.ep.rows_in
+        self.x_recv = torch.empty((rows, self.H), dtype=self.x.dtype, device=self.x.device)
+        self.y_recv = torch.empty_like(self.x_recv)
+        self.ws_f = torch.empty(self.rd.expert_ffn_workspace_bytes(max(rows, 1), self.H, self.ep.E_local, self.d,
+                                                                   self.x.dtype), dtype=torch.uint8,
+                                device=self.x.device)
+
+    def layer(self, x=None, residual=None):
+        """Per layer (plan reused): dispatch -> C2 -> grouped FFN over (source, local expert) segments -> C3
+        -> combine."""
+        rd, ep = self.rd, self.ep
+        x = self.x if x is None else x
+        rd.dispatch(x, self.plan.dest, self.k, out=self.xs)
+        exchange(self.xs, ep, out=self.x_recv, group=self.group)
+        if ep.rows_in:
+            rd.expert_ffn(self.x_recv, self.seg_dev, *self.w, n_src=ep.G, out=self.y_recv, ws=self.ws_f)
+        exchange(self.y_recv, ep, reverse=True, out=self.ys, group=self.group)
+        return rd.combine(self.ys, self.plan.dest, self.plan.topk_w, self.k, residual=residual, out=self.y)
+
+    def step(self):
+        self.route()
+        return self.layer()

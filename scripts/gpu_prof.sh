@@ -1,0 +1,11 @@
+#!/bin/bash
+# ncu evidence: launch list of one bench step, and full-set captures of the hot kernels.
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+python -m paper_2410_19123_b200.build > gpurun_out/build.log 2>&1
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "launch rc=$?"
+EXTRA=sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum
+timeout 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:ffn_gemm -s 2 -c 2 -o gpurun_out/prof_gemm $B > gpurun_out/ncu_gemm.log 2>&1; echo "gemm rc=$?"
+timeout 600 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"dispatch|gather|route" -s 3 -c 4 -o gpurun_out/prof_perm $B > gpurun_out/ncu_perm.log 2>&1; echo "perm rc=$?"
+ls -la gpurun_out
