@@ -180,8 +180,8 @@ def run_reference(args):
     del wg, wu, wd
     x = synth.to_torch(synth.tokens(T, H, seed=seed), "bf16")
     lg = synth.router_logits(T, E, seed=seed)
-    per_step = 8  # tokens per step (one per expert on average): a bounded sample of the workload
     threads = oracle.default_threads()
+    per_step = max(8, threads)  # tokens per step: a bounded sample of the workload, one per oracle thread
     g = synth.rng(5, 5)
     times = []
     for i in range(args.warmup + args.steps):
