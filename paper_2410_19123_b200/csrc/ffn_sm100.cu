@@ -22,13 +22,17 @@
 // grid, so co-resident CTAs share the expert's weight tile in L2. The tile list is derived on the device
 // from `offsets` (no host synchronisation; CUDA-graph capturable). No split-K: every output element has a
 // fixed K order, so results are bitwise batch-invariant and permutation-equivariant (P4, P13).
-#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <mutex>
 
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace readme {
+
+using namespace tc;
 
 namespace {
 
@@ -56,97 +60,6 @@ struct __align__(8) Smem {
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;  // + alignment slack (swizzle-128B needs 1024 B)
 
-// ---- PTX wrappers ----------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-// D[tmem] (+)= A[smem] . B[smem]^T, both K-major.
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// Shared-memory matrix descriptor for a K-major operand tile stored by TMA with 128-byte swizzle:
-// rows of 128 B, 8-row core groups 1024 B apart (SBO), LBO unused for swizzled K-major (=1),
-// version 1 (sm_100), layout type 2 = SWIZZLE_128B. Advancing K by 16 bf16 = +32 B on the start address.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>(1u) << 16;           // LBO (16 B units)
-  d |= static_cast<uint64_t>(1024u >> 4) << 32;   // SBO (16 B units)
-  d |= static_cast<uint64_t>(1u) << 46;           // descriptor version (sm_100)
-  d |= static_cast<uint64_t>(2u) << 61;           // SWIZZLE_128B
-  return d;
-}
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
-}
-
 struct Tile {
   int g;       // segment
   int m0;      // first row (global row index into the expert-contiguous buffer)
@@ -169,7 +82,6 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int t, int nseg, int 
   return tl;
 }
 
-__device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
 
 template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -191,10 +103,7 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (kMode == 0) prefetch_tmap(&tmB1);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s.tmem_base)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tmem_alloc<1>(&s.tmem_base, kTmemCols);
   }
   __syncthreads();
   if (tid == 0) {
@@ -214,9 +123,9 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  tc_fence_before();
+  fence_before();
   __syncthreads();
-  tc_fence_after();
+  fence_after();
   const int ntiles = s.tile_start[nseg];
   const uint32_t tmem_base = s.tmem_base;
 
@@ -257,24 +166,24 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
         mbar_wait(&s.tempty[acc], (use & 1u) ^ 1u);
-        tc_fence_after();
+        fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&s.full[stage], phase);
-          tc_fence_after();
+          fence_after();
           const uint32_t a0 = smem_u32(s.a[stage]), b0 = smem_u32(s.b[stage]);
 #pragma unroll
           for (int kk = 0; kk < kBK / kUK; ++kk) {
-            tc_mma(d_tmem, sdesc_sw128(a0 + kk * kUK * 2), sdesc_sw128(b0 + kk * kUK * 2), idesc,
+            mma_f16<1>(d_tmem, sdesc_sw128(a0 + kk * kUK * 2), sdesc_sw128(b0 + kk * kUK * 2), idesc,
                    (kb | kk) != 0 ? 1u : 0u);
           }
-          tc_commit(&s.empty[stage]);
+          commit(&s.empty[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&s.tfull[acc]);
+        commit(&s.tfull[acc]);
       }
     }
   } else {
@@ -287,7 +196,7 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       mbar_wait(&s.tfull[acc], use & 1u);
-      tc_fence_after();
+      fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * kBN);
       const bool valid = row < tl.mrows;
       __nv_bfloat16* orow = out + static_cast<int64_t>(tl.m0 + row) * N;
@@ -304,14 +213,14 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int j = 0; j < 32; j += 8) {
               if (col0 + j < N) {
                 uint4 v;
-                v.x = pack_bf16x2(silu_f(__uint_as_float(gr[j + 0])) * __uint_as_float(ur[j + 0]),
-                                  silu_f(__uint_as_float(gr[j + 1])) * __uint_as_float(ur[j + 1]));
-                v.y = pack_bf16x2(silu_f(__uint_as_float(gr[j + 2])) * __uint_as_float(ur[j + 2]),
-                                  silu_f(__uint_as_float(gr[j + 3])) * __uint_as_float(ur[j + 3]));
-                v.z = pack_bf16x2(silu_f(__uint_as_float(gr[j + 4])) * __uint_as_float(ur[j + 4]),
-                                  silu_f(__uint_as_float(gr[j + 5])) * __uint_as_float(ur[j + 5]));
-                v.w = pack_bf16x2(silu_f(__uint_as_float(gr[j + 6])) * __uint_as_float(ur[j + 6]),
-                                  silu_f(__uint_as_float(gr[j + 7])) * __uint_as_float(ur[j + 7]));
+                v.x = pack_bf16x2(silu(__uint_as_float(gr[j + 0])) * __uint_as_float(ur[j + 0]),
+                                  silu(__uint_as_float(gr[j + 1])) * __uint_as_float(ur[j + 1]));
+                v.y = pack_bf16x2(silu(__uint_as_float(gr[j + 2])) * __uint_as_float(ur[j + 2]),
+                                  silu(__uint_as_float(gr[j + 3])) * __uint_as_float(ur[j + 3]));
+                v.z = pack_bf16x2(silu(__uint_as_float(gr[j + 4])) * __uint_as_float(ur[j + 4]),
+                                  silu(__uint_as_float(gr[j + 5])) * __uint_as_float(ur[j + 5]));
+                v.w = pack_bf16x2(silu(__uint_as_float(gr[j + 6])) * __uint_as_float(ur[j + 6]),
+                                  silu(__uint_as_float(gr[j + 7])) * __uint_as_float(ur[j + 7]));
                 st_v4(reinterpret_cast<uint4*>(orow + col0 + j), v);
               }
             }
@@ -339,22 +248,24 @@ ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
         }
       }
-      tc_fence_before();
+      fence_before();
       mbar_arrive(&s.tempty[acc]);
     }
   }
 
   // ---- teardown ----
-  tc_fence_before();
+  fence_before();
   __syncthreads();
-  tc_fence_after();
+  fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
-                 : "memory");
+    tmem_dealloc<1>(tmem_base, kTmemCols);
   }
 }
 
 // ---- host: tensor maps ------------------------------------------------------------------------------
+}  // namespace
+namespace tc {
+namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -367,6 +278,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   });
   return fn;
 }
+}  // namespace
 
 bool make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in,
                  uint32_t box_out) {
@@ -393,7 +305,9 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t mid,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+}  // namespace tc
 
+namespace {
 readme_status set_smem_attr() {
   static std::once_flag once[64];
   static cudaError_t err[64];
@@ -413,11 +327,10 @@ readme_status set_smem_attr() {
 
 }  // namespace
 
-readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+readme_status launch_ffn_bf16_1cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                               const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
                               __nv_bfloat16* h_ws, cudaStream_t st) {
-  if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
     return README_ERR_UNSUPPORTED;
@@ -425,8 +338,8 @@ readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, 
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
   CUtensorMap mA1, mG, mU, mA2, mD;
-  bool ok = make_map_2d(&mA1, xs, H, rows, kBK, kBM) && make_map_3d(&mG, wg, H, d, E, kBK, kBN / 2) &&
-            make_map_3d(&mU, wu, H, d, E, kBK, kBN / 2) && make_map_2d(&mA2, h_ws, d, rows, kBK, kBM) &&
+  bool ok = tc::make_map_2d(&mA1, xs, H, rows, kBK, kBM) && tc::make_map_3d(&mG, wg, H, d, E, kBK, kBN / 2) &&
+            make_map_3d(&mU, wu, H, d, E, kBK, kBN / 2) && tc::make_map_2d(&mA2, h_ws, d, rows, kBK, kBM) &&
             make_map_3d(&mD, wd, d, H, E, kBK, kBN);
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
@@ -443,6 +356,19 @@ readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, 
   ffn_gemm_kernel<1><<<g2, kThreads, kSmemBytes, st>>>(mA2, mD, mD, d, H, E, nseg, offsets, ys);
   README_CUDA(cudaGetLastError());
   return README_OK;
+}
+
+// Kernel choice: the CTA-pair kernel by default; README_FFN_KERNEL=1cta selects the single-CTA one
+// (kept for A/B measurement and as the small-batch variant).
+readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                              int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                              const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
+                              __nv_bfloat16* h_ws, cudaStream_t st) {
+  if (rows == 0) return README_OK;
+  const char* v = getenv("README_FFN_KERNEL");
+  if (v && strcmp(v, "1cta") == 0)
+    return launch_ffn_bf16_1cta(xs, rows, H, E, d, nseg, offsets, wg, wu, wd, ys, h_ws, st);
+  return launch_ffn_bf16_2cta(xs, rows, H, E, d, nseg, offsets, wg, wu, wd, ys, h_ws, st);
 }
 
 }  // namespace readme

@@ -1,0 +1,319 @@
+// ffn_sm100_2cta.cu — a6/a7 grouped expert GEMMs on CTA pairs (tcgen05.mma.cta_group::2), bf16.
+//
+// Same math as ffn_sm100.cu (SwiGLU reading Q4):
+//     kMode 0:  h_r = silu(x_r . W_gate[e]^T) * (x_r . W_up[e]^T)      kMode 1:  y_r = h_r . W_down[e]^T
+// but each tile is computed by a CLUSTER OF TWO CTAs on two SMs of a TPC: one tcgen05.mma.cta_group::2
+// (issued by the even CTA) multiplies A rows held in both CTAs' shared memory by a 256-column B tile
+// whose halves live in the two CTAs, accumulating into both CTAs' TMEM. Per SM this halves the B bytes
+// staged per MMA (32 KB per 64-deep K stage instead of 48 KB), so a 6-deep TMA ring fits and the L2->SM
+// traffic per FLOP drops by a third — the v1 profile showed the MMA warp waiting on TMA data ~13 % of
+// the time with a 4-deep ring (profiles/SUMMARY.md).
+//
+// Tiles: 256 rows x 256 accumulator columns (M=256 MMA, each CTA 128 rows, TMEM lane = row). The last
+// tile of an expert with <= 128 remaining rows runs as an M=128 MMA (each CTA 64 rows; CUTLASS's "2x2"
+// TMEM layout: lanes 0-63 hold accumulator columns [0,128), lanes 64-127 columns [128,256) of the same
+// rows), so padding waste stays at the 128-row granularity of v1.
+// GEMM1 B operand per CTA r: 64 rows of W_gate then the same 64 rows of W_up (neurons n0+64r ..), so in
+// accumulator column space gate column c pairs with up column c+64 inside every 128-column window.
+#include <mutex>
+
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace readme {
+
+namespace {
+
+constexpr int kBK = 64;
+constexpr int kUK = 16;
+constexpr int kStages = 6;
+constexpr int kThreads = 192;
+constexpr int kMaxSeg = 512;
+constexpr int kStageA = 128 * 128;  // up to 128 rows x 128 B per CTA
+constexpr int kStageB = 128 * 128;  // 128 rows x 128 B per CTA (its half of N = 256)
+constexpr int kTmemCols = 512;      // two accumulators of 256 columns
+
+struct __align__(8) Smem {
+  uint8_t a[kStages][kStageA];
+  uint8_t b[kStages][kStageB];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int seg_off[kMaxSeg + 1];
+  int tile_start[kMaxSeg + 1];
+};
+constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+
+struct Tile {
+  int g, m0, rows, n0;
+  bool m256;
+};
+
+__device__ __forceinline__ Tile decode_tile(const Smem& s, int t, int nseg, int bn_out, int& gcur) {
+  while (gcur + 1 < nseg && s.tile_start[gcur + 1] <= t) ++gcur;
+  const int g = gcur;
+  const int cnt = s.seg_off[g + 1] - s.seg_off[g];
+  const int mt_g = (cnt + 255) / 256;
+  const int local = t - s.tile_start[g];
+  const int nt = local / mt_g, mt = local % mt_g;
+  Tile tl;
+  tl.g = g;
+  tl.m0 = s.seg_off[g] + mt * 256;
+  tl.rows = min(256, cnt - mt * 256);
+  tl.m256 = tl.rows > 128;
+  tl.n0 = nt * bn_out;
+  return tl;
+}
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int ncols_left) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    if (j < ncols_left) {
+      uint4 w;
+      w.x = pack_bf16x2(v[j + 0], v[j + 1]);
+      w.y = pack_bf16x2(v[j + 2], v[j + 3]);
+      w.z = pack_bf16x2(v[j + 4], v[j + 5]);
+      w.w = pack_bf16x2(v[j + 6], v[j + 7]);
+      st_v4(reinterpret_cast<uint4*>(dst + j), w);
+    }
+  }
+}
+
+template <int kMode>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                 const __grid_constant__ CUtensorMap tmB1, int K, int N, int E, int nseg,
+                 const int32_t* __restrict__ offsets, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
+  const uint32_t cta = tc::cluster_ctarank();
+  const bool leader = cta == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr int kBnOut = kMode == 0 ? 128 : 256;
+  const int NT = (N + kBnOut - 1) / kBnOut;
+  const int KB = (K + kBK - 1) / kBK;
+
+  for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = offsets[i];
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB0);
+    if (kMode == 0) tc::prefetch_tmap(&tmB1);
+  }
+  if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int g = 0; g < nseg; ++g) {
+      s.tile_start[g] = acc;
+      acc += (s.seg_off[g + 1] - s.seg_off[g] + 255) / 256 * NT;
+    }
+    s.tile_start[nseg] = acc;
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.full[i], 1);   // the leader's producer arms it with both CTAs' bytes
+      tc::mbar_init(&s.empty[i], 1);  // one multicast commit per consumed stage
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.tfull[i], 1);
+      tc::mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  const int ntiles = s.tile_start[nseg];
+  const uint32_t tmem_base = s.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      int gcur = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+        const int e = tl.g % E;
+        const int a_rows = tl.m256 ? 128 : 64;
+        const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
+        const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait(&s.empty[stage], phase ^ 1);
+          if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
+          const uint32_t fb = tc::mapa(&s.full[stage], 0);
+          const int k0 = kb * kBK;
+          tc::tma_load_2d_2sm(&tmA, s.a[stage], fb, k0, a_row0);
+          if (tl.m256) tc::tma_load_2d_2sm(&tmA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
+          if (kMode == 0) {
+            tc::tma_load_3d_2sm(&tmB0, s.b[stage], fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
+            tc::tma_load_3d_2sm(&tmB1, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
+          } else {
+            tc::tma_load_3d_2sm(&tmB0, s.b[stage], fb, k0, tl.n0 + 128 * static_cast<int>(cta), e);
+            tc::tma_load_3d_2sm(&tmB0, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 128 * static_cast<int>(cta) + 64, e);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer (leader CTA, one thread) =====
+      constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
+      constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
+      int stage = 0;
+      uint32_t phase = 0;
+      int gcur = 0, i = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++i) {
+        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+        const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
+        const int acc = i & 1;
+        const uint32_t use = static_cast<uint32_t>(i >> 1);
+        tc::mbar_wait_cluster(&s.tempty[acc], (use & 1u) ^ 1u);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait_cluster(&s.full[stage], phase);
+          tc::fence_after();
+          const uint32_t a0 = tc::smem_u32(s.a[stage]), b0 = tc::smem_u32(s.b[stage]);
+#pragma unroll
+          for (int kk = 0; kk < kBK / kUK; ++kk)
+            tc::mma_f16<2>(d_tmem, tc::sdesc_sw128(a0 + kk * kUK * 2), tc::sdesc_sw128(b0 + kk * kUK * 2), idesc,
+                           (kb | kk) != 0 ? 1u : 0u);
+          tc::commit_2sm_mc(&s.empty[stage], 0x3);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 of both CTAs; warp's TMEM lane quarter = warp % 4 =====
+    const int q = warp & 3;
+    int gcur = 0, i = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++i) {
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+      const int acc = i & 1;
+      const uint32_t use = static_cast<uint32_t>(i >> 1);
+      tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
+      tc::fence_after();
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      int row_in_tile, col_base, n_windows, out_off;
+      if (tl.m256) {  // "4x1": lane = row, all 256 columns
+        row_in_tile = static_cast<int>(cta) * 128 + q * 32 + lane;
+        col_base = 0;
+        n_windows = 2;
+        out_off = 0;
+      } else {  // "2x2": lanes 0-63 -> columns [0,128), lanes 64-127 -> columns [128,256), same 64 rows
+        row_in_tile = static_cast<int>(cta) * 64 + (q & 1) * 32 + lane;
+        col_base = 0;
+        n_windows = 1;
+        out_off = (q >> 1) * (kBnOut / 2);
+      }
+      const bool valid = row_in_tile < tl.rows;
+      __nv_bfloat16* orow = out + static_cast<int64_t>(tl.m0 + row_in_tile) * N;
+      for (int w = 0; w < n_windows; ++w) {
+        const uint32_t wbase = tacc + static_cast<uint32_t>(col_base + w * 128);
+        if (kMode == 0) {
+          // window of 128 accumulator columns: gate [0,64), up [64,128) -> 64 h columns
+          const int hcol0 = tl.n0 + out_off + w * 64;
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 32) {
+            uint32_t gr[32], ur[32];
+            tc::tmem_ld32(wbase + c, gr);
+            tc::tmem_ld32(wbase + 64 + c, ur);
+            tc::tmem_wait_ld();
+            if (valid) {
+              float v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+              store_bf16x32(orow + hcol0 + c, v, N - (hcol0 + c));
+            }
+          }
+        } else {
+          const int col0 = tl.n0 + out_off + w * 128;
+#pragma unroll 1
+          for (int c = 0; c < 128; c += 32) {
+            uint32_t vr[32];
+            tc::tmem_ld32(wbase + c, vr);
+            tc::tmem_wait_ld();
+            if (valid) {
+              float v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+              store_bf16x32(orow + col0 + c, v, N - (col0 + c));
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(&s.tempty[acc], 0);
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
+}
+
+readme_status set_smem_attr() {
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  int dev = 0;
+  README_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [&] {
+    err[dev] = cudaFuncSetAttribute(ffn_gemm2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemBytes));
+    if (err[dev] == cudaSuccess)
+      err[dev] = cudaFuncSetAttribute(ffn_gemm2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kSmemBytes));
+  });
+  if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
+  return README_OK;
+}
+
+}  // namespace
+
+readme_status launch_ffn_bf16_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
+                                   __nv_bfloat16* h_ws, cudaStream_t st) {
+  if (nseg > kMaxSeg) {
+    set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
+    return README_ERR_UNSUPPORTED;
+  }
+  readme_status rs = set_smem_attr();
+  if (rs != README_OK) return rs;
+  CUtensorMap mA1, mG, mU, mA2, mD;
+  bool ok = tc::make_map_2d(&mA1, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, E, kBK, 64) &&
+            tc::make_map_3d(&mU, wu, H, d, E, kBK, 64) && tc::make_map_2d(&mA2, h_ws, d, rows, kBK, 64) &&
+            tc::make_map_3d(&mD, wd, d, H, E, kBK, 64);
+  if (!ok) {
+    set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
+    return README_ERR_CUDA;
+  }
+  const int64_t mt_ub = nseg + (rows + 255) / 256;
+  const int pairs = num_sms() / 2;
+  const int64_t t1 = mt_ub * ((d + 127) / 128);
+  const int64_t t2 = mt_ub * ((H + 255) / 256);
+  const int g1 = 2 * static_cast<int>(t1 < pairs ? t1 : pairs);
+  const int g2 = 2 * static_cast<int>(t2 < pairs ? t2 : pairs);
+  ffn_gemm2_kernel<0><<<g1, kThreads, kSmemBytes, st>>>(mA1, mG, mU, H, d, E, nseg, offsets, h_ws);
+  README_CUDA(cudaGetLastError());
+  ffn_gemm2_kernel<1><<<g2, kThreads, kSmemBytes, st>>>(mA2, mD, mD, d, H, E, nseg, offsets, ys);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+}  // namespace readme

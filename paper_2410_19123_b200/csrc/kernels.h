@@ -25,7 +25,15 @@ readme_status launch_ffn_f32(const float* xs, int64_t rows, int32_t H, int32_t E
                              const int32_t* offsets, const float* wg, const float* wu, const float* wd,
                              float* ys, float* h_ws, cudaStream_t st);
 
-// ffn_sm100.cu (tcgen05 / TMEM / TMA grouped GEMMs, bf16)
+// ffn_sm100.cu / ffn_sm100_2cta.cu (tcgen05 / TMEM / TMA grouped GEMMs, bf16)
+readme_status launch_ffn_bf16_1cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
+                                   __nv_bfloat16* h_ws, cudaStream_t st);
+readme_status launch_ffn_bf16_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
+                                   __nv_bfloat16* h_ws, cudaStream_t st);
 readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                               const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,

@@ -174,8 +174,12 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
     (300, 128, 136, 3, 1, "zipf"),     # H < BN, K = 2 x 64
     (2048, 4096, 512, 8, 1, None),     # Llama-2 H, K = 64 x 64
     (129, 72, 40, 2, 1, None),         # K tail (72 = 64 + 8), d tiny
+    (4000, 512, 256, 8, 1, "zipf"),    # many 256-row tiles, 128-row and 256-row tails
+    (1024, 256, 128, 4, 1, None),      # counts ~256 -> exact and near-exact tiles
 ])
-def test_expert_ffn_bf16_teacher_forced(rd, T, H, d, E, k, skew):
+@pytest.mark.parametrize("kernel", ["2cta", "1cta"])
+def test_expert_ffn_bf16_teacher_forced(rd, monkeypatch, kernel, T, H, d, E, k, skew):
+    monkeypatch.setenv("README_FFN_KERNEL", kernel)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + H, skew=skew)
     plan = rd.route(torch.from_numpy(lg).to(DEV), k)
     xs = rd.dispatch(x.to(DEV), plan.dest, k)
@@ -194,6 +198,21 @@ def test_expert_ffn_f32_config1(rd):
     ys = rd.expert_ffn(xs, plan.offsets, wg.to(DEV), wu.to(DEV), wd.to(DEV))
     ref = oracle.expert_ffn(xs.cpu(), plan.offsets.cpu().numpy(), wg, wu, wd)
     assert rel_err(_np(ys), ref) <= F32_TOL
+
+
+@pytest.mark.parametrize("kernel", ["2cta", "1cta"])
+def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
+    """Segment sizes on every tile boundary: empty, 1 row, 64/128/256 +- 1 (M=128 vs M=256 tails)."""
+    monkeypatch.setenv("README_FFN_KERNEL", kernel)
+    counts = [0, 1, 63, 64, 65, 127, 128, 129, 255, 256, 257, 383, 384, 385, 511, 512]
+    E, H, d = len(counts), 128, 136
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(off[-1])
+    xs = synth.to_torch(synth.tokens(rows, H, seed=13), "bf16")
+    wg, wu, wd = (synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=14))
+    ys = rd.expert_ffn(xs.to(DEV), torch.from_numpy(off).to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV))
+    ref = oracle.expert_ffn(xs, off, wg, wu, wd)
+    assert rel_err(_np(ys), ref) <= BF16_TOL
 
 
 def test_expert_ffn_segments_n_src(rd):
