@@ -225,70 +225,57 @@ def main():
     T = args.tokens or (cfg["T"] if world == 1 else 8192)
     H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
 
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x L2
+
+    def timed(fn, n):
+        """n steps, L2 flushed before each (outside the events), CUDA events on the launching stream."""
+        out = []
+        for _ in range(n):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            fn()
+            s1.record()
+            out.append((s0, s1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in out]
+
     if world > 1:
         from paper_2410_19123_b200 import ep
         layer = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
         step_fn = layer.step
-        x_dev = layer.x
-        inp = None
     else:
         inp = make_inputs(cfg, T, rank, dev)
         eg, eu, ed = inp["w"]
         x_dev = inp["x"].to(dev)
         lg_dev = torch.from_numpy(inp["logits"]).to(dev)
         plan = rd.new_plan(T, E, k, dev)
-        xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
-        ys = torch.empty_like(xs)
         y = torch.empty_like(x_dev)
-        ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
-        ws_f = torch.empty(rd.expert_ffn_workspace_bytes(T * k, H, E, d, torch.bfloat16), dtype=torch.uint8,
-                           device=dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
 
-        def step_fn(record=False):
-            if record:
-                ev[0].record()
-            rd.route(lg_dev, k, plan=plan, ws=ws_r)
-            if record:
-                ev[1].record()
-            rd.dispatch(x_dev, plan.dest, k, out=xs)
-            if record:
-                ev[2].record()
-            rd.expert_ffn(xs, plan.offsets, eg, eu, ed, out=ys, ws=ws_f)
-            if record:
-                ev[3].record()
-            rd.combine(ys, plan.dest, plan.topk_w, k, out=y)
-            if record:
-                ev[4].record()
+        def step_fn():  # the whole hot path through the public C entry (route + fused grouped GEMMs)
+            rd.moe_layer(x_dev, eg, eu, ed, k=k, logits=lg_dev, plan=plan, out=y, ws=ws)
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x L2
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
-
-    stage_ms = {"route": 0.0, "dispatch": 0.0, "expert_ffn": 0.0, "combine": 0.0}
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
-        per_stage = []
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            starts[i].record()
-            if world > 1:
-                step_fn()
-            else:
-                step_fn(record=True)
-            ends[i].record()
-            if world == 1:
-                torch.cuda.synchronize()
-                per_stage.append([ev[j].elapsed_time(ev[j + 1]) for j in range(4)])
-        torch.cuda.synchronize()
+        step_ms = timed(step_fn, args.steps)
+        if world == 1:
+            # breakdown (same protocol): route alone; plan-in layer = the two fused grouped-GEMM kernels
+            ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
+            xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
+            hbuf = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
+            y2 = torch.empty_like(x_dev)
+            route_ms = timed(lambda: rd.route(lg_dev, k, plan=plan, ws=ws_r), args.steps)
+            disp_ms = timed(lambda: rd.dispatch(x_dev, plan.dest, k, out=xs), args.steps)
+            gu_ms = timed(lambda: rd.expert_gate_up(xs, plan.offsets, eg, eu, out=hbuf), args.steps)
+            dn_ms = timed(lambda: rd.expert_down(hbuf, plan.offsets, ed, src=plan.src, out=y2), args.steps)
     if world > 1:
         dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     tot_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev)
@@ -306,29 +293,40 @@ def main():
                        "parallelism": "single" if world == 1 else f"ep{world}",
                        "l2": "flushed between timed steps (256 MiB write)"}}
     if world == 1:
-        st = np.array(per_stage)
-        med = {n: float(np.median(st[:, j])) for j, n in enumerate(stage_ms)}
-        line["stage_ms_median"] = med
-        flops = 6.0 * T * k * H * d
-        ffn_ms = float(np.mean(st[:, 2]))
+        med = lambda a: float(np.median(a))
+        line["stage_ms_median"] = {"step": med(step_ms), "route": med(route_ms), "dispatch": med(disp_ms),
+                                   "gate_up": med(gu_ms), "down_combine": med(dn_ms)}
+        f_gu, f_dn = 4.0 * T * k * H * d, 2.0 * T * k * H * d
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("expert_ffn_bytes_per_launch")
-        line["roofline"] = {"bound": "tensor", "kernel": "grouped expert GEMMs (gate/up+SiLU, down) = readme_expert_ffn",
-                            "achieved": flops / (ffn_ms * 1e-3) / 1e12, "peak": pk["bf16_tflops"],
-                            "unit": "TFLOP/s", "frac": flops / (ffn_ms * 1e-3) / 1e12 / pk["bf16_tflops"],
-                            "traffic": traffic, "peak_source": f"{pk_src} bf16 burst",
-                            "algorithmic": f"6*T*k*H*d = {flops:.4g} FLOP per launch pair"}
+                traffic = json.load(f).get("gate_up_bytes_per_launch")
+        ach = f_gu / (float(np.mean(gu_ms)) * 1e-3) / 1e12
+        ach_dn = f_dn / (float(np.mean(dn_ms)) * 1e-3) / 1e12
+        line["roofline"] = {"bound": "tensor",
+                            "kernel": "a6 grouped gate/up GEMM + SiLU*up (ffn_gemm2_kernel<0>, tcgen05 cta_group::2), "
+                                      "one launch = readme_expert_gate_up",
+                            "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                            "frac": ach / pk["bf16_tflops"], "traffic": traffic,
+                            "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)",
+                            "algorithmic": f"4*T*k*H*d = {f_gu:.4g} FLOP per launch",
+                            "down_combine": {"achieved": ach_dn, "frac": ach_dn / pk["bf16_tflops"],
+                                             "algorithmic": f"2*T*k*H*d = {f_dn:.4g} FLOP per launch"},
+                            "both_gemms_frac": (f_gu + f_dn) / ((float(np.mean(gu_ms)) + float(np.mean(dn_ms))) * 1e-3)
+                                               / 1e12 / pk["bf16_tflops"]}
+        # the standalone permutation entries (readme_dispatch / readme_combine), HBM-bound
+        ys = torch.empty_like(xs)
+        comb_ms = timed(lambda: rd.combine(ys, plan.dest, plan.topk_w, k, out=y2), args.steps)
         hbm = pk["hbm_gbs"]
         disp_bytes = 2.0 * T * k * H * 2
         comb_bytes = (k + 1.0) * T * H * 2
-        line["hbm"] = {"dispatch_GBps": disp_bytes / (med["dispatch"] * 1e-3) / 1e9,
-                       "combine_GBps": comb_bytes / (med["combine"] * 1e-3) / 1e9, "peak_GBps": hbm,
-                       "dispatch_frac": disp_bytes / (med["dispatch"] * 1e-3) / 1e9 / hbm,
-                       "combine_frac": comb_bytes / (med["combine"] * 1e-3) / 1e9 / hbm}
-        line["gpu_launches"] = 6 * args.steps  # route(2) + dispatch(1) + expert_ffn(2) + combine(1) per step
+        dg = disp_bytes / (med(disp_ms) * 1e-3) / 1e9
+        cg = comb_bytes / (med(comb_ms) * 1e-3) / 1e9
+        line["hbm"] = {"dispatch_GBps": dg, "combine_GBps": cg, "peak_GBps": hbm, "dispatch_frac": dg / hbm,
+                       "combine_frac": cg / hbm, "note": "readme_dispatch is on the step; readme_combine is the "
+                       "standalone entry (inside readme_moe_layer, k=1, it is fused into the down GEMM epilogue)"}
+        line["gpu_launches"] = (5 if k == 1 else 6) * args.steps  # route(2)+dispatch+gate_up+down(+combine if k>1)
     else:
         line["gpu_launches"] = None
     line["clocks"] = clk.summary()
@@ -340,7 +338,6 @@ def main():
         y_h = torch.empty_like(x_h).pin_memory()
         x_d = torch.empty_like(x_dev)
         lg_d = torch.empty_like(lg_dev)
-        ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
         y_d = torch.empty_like(x_dev)
 
         def e2e_step():
@@ -352,15 +349,7 @@ def main():
         for _ in range(max(2, args.warmup)):
             e2e_step()
         torch.cuda.synchronize()
-        e_ms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            e2e_step()
-            e.record()
-            torch.cuda.synchronize()
-            e_ms.append(s.elapsed_time(e))
+        e_ms = timed(e2e_step, args.steps)
         line["e2e"] = {"value": T / (np.mean(e_ms) * 1e-3), "unit": UNIT,
                        "h2d_bytes_per_step": x_h.numel() * 2 + lg_h.numel() * 4,
                        "d2h_bytes_per_step": y_h.numel() * 2, "ms_per_step": float(np.mean(e_ms))}

@@ -9,7 +9,8 @@
  * This library implements the data-parallel hot path of one such layer on an NVIDIA B200 (sm_100a):
  *   readme_route      a1-a4  top-K + gate weights, per-expert histogram, exclusive scan, stable permutation
  *   readme_dispatch   a5     scatter tokens into expert-contiguous rows
- *   readme_expert_ffn a6-a7  grouped SwiGLU expert GEMMs (tcgen05/TMEM for bf16, SIMT fp32 for f32)
+ *   readme_expert_ffn a6-a7  grouped SwiGLU expert GEMMs (tcgen05/TMEM for bf16, SIMT fp32 for f32), also
+ *                            split as readme_expert_gate_up (a6) and readme_expert_down (a7, optional fused a8)
  *   readme_combine    a8     gather back to token order, weight, add residual
  *   readme_moe_layer  a1-a8  the whole layer; with logits == NULL it reuses a routing plan (a9: route
  *                            once, reuse across all L layers)
@@ -108,6 +109,20 @@ readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t r
                                 const void* w_up, const void* w_down, void* y_sorted, void* ws,
                                 size_t ws_bytes, readme_stream_t stream);
 
+/* a6 alone: h = silu(x_sorted W_gate[e]^T) * (x_sorted W_up[e]^T) per segment; h [rows,d] of dtype dt (bf16 h is
+ * rounded once, Q11). Same arguments as readme_expert_ffn; no workspace. */
+readme_status readme_expert_gate_up(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                    int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
+                                    const void* w_up, void* h, readme_stream_t stream);
+
+/* a7 alone: y_sorted_r = h_r W_down[e]^T per segment, out [rows,H]. With src != NULL (a layer with k == 1, whose
+ * combine weight is exactly 1) row r is instead written to out[src[r]] + residual[src[r]] (residual nullable;
+ * out is then y [T = rows, H]): the combine a8 fused into the epilogue, fp32 add, one rounding. Rows whose
+ * src is out of range are skipped. residual without src is an argument error. */
+readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                 int32_t n_src, const int32_t* offsets, const void* w_down, const int32_t* src,
+                                 const void* residual, void* out, readme_stream_t stream);
+
 /* a8: combine (Eq. 2's weighted sum):
  *     y[t] = residual[t] + sum_{j<k} topk_w[t,j] * y_sorted[dest[t*k+j]]   (j ascending, fp32, Q8)
  * topk_w is nullable iff k == 1 (weight 1); residual [T,H] nullable. With k == 1 and no residual the
@@ -116,10 +131,12 @@ readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, i
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
                              uint32_t* dev_status, readme_stream_t stream);
 
-/* The whole layer (a1-a8).  If logits != NULL the plan (topk_idx..src) is computed and written; if
+/* The whole layer (a1-a8).  If logits != NULL the plan (topk_idx..src) is computed and written (src may be
+ * NULL: the library then keeps it in the workspace); if
  * logits == NULL the plan arrays are INPUTS from an earlier call (plan-in mode: route once per batch,
  * reuse for every layer). x, residual, y: [T,H] of dtype dt; weights as in
- * readme_expert_ffn. ws: readme_moe_layer_workspace_bytes(...) bytes. */
+ * readme_expert_ffn. ws: readme_moe_layer_workspace_bytes(...) bytes. With k == 1 and a src available, the
+ * combine is fused into the down projection's epilogue (one rounding of residual + y instead of two). */
 size_t readme_moe_layer_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t d, int32_t k, readme_dtype dt);
 readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
                                readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, const void* w_gate,

@@ -165,6 +165,38 @@ def expert_ffn(x_sorted, offsets, w_gate, w_up, w_down, n_src: int = 1, act: str
     return out
 
 
+def expert_hidden(x_sorted, offsets, w_gate, w_up, n_src: int = 1, nthreads: int | None = None):
+    """a6 alone: h = silu(x W_gate[e]^T) * (x W_up[e]^T), fp64 [rows, d]."""
+    lib = _load()
+    xa, xdt = _as_input(x_sorted)
+    rows, H = xa.shape
+    (wg, wu), wdt = _weights(w_gate, w_up)
+    E, d, _ = wg.shape
+    offsets = _i32(offsets)
+    out = np.empty((rows, d), np.float64)
+    rc = lib.oracle_expert_hidden(_p(xa), ctypes.c_int32(xdt), ctypes.c_int64(rows), ctypes.c_int32(H),
+                                  ctypes.c_int32(E), ctypes.c_int32(d), ctypes.c_int32(n_src), _p(offsets), _p(wg),
+                                  _p(wu), ctypes.c_int32(wdt), _p(out), ctypes.c_int32(nthreads or default_threads()))
+    _check(rc, "oracle_expert_hidden")
+    return out
+
+
+def expert_down(h, offsets, w_down, n_src: int = 1, nthreads: int | None = None):
+    """a7 alone: y = h W_down[e]^T, fp64 [rows, H]."""
+    lib = _load()
+    ha, hdt = _as_input(h)
+    rows, d = ha.shape
+    wd, wdt = _as_input(w_down)
+    E, H, _ = wd.shape
+    offsets = _i32(offsets)
+    out = np.empty((rows, H), np.float64)
+    rc = lib.oracle_expert_down(_p(ha), ctypes.c_int32(hdt), ctypes.c_int64(rows), ctypes.c_int32(H),
+                                ctypes.c_int32(E), ctypes.c_int32(d), ctypes.c_int32(n_src), _p(offsets), _p(wd),
+                                ctypes.c_int32(wdt), _p(out), ctypes.c_int32(nthreads or default_threads()))
+    _check(rc, "oracle_expert_down")
+    return out
+
+
 def combine(y_sorted, dest, topk_w, k: int, residual=None):
     """a8: y[t] = res[t] + sum_j w[t,j] * y_sorted[dest[t*k+j]] (j ascending)."""
     lib = _load()

@@ -180,6 +180,57 @@ int oracle_expert_ffn(const void* x_sorted, int32_t xdt, int64_t rows, int32_t H
     return ORACLE_OK;
 }
 
+// ---- a6 alone: h_r = silu(W_gate,e x_r) * (W_up,e x_r) (the hidden activation of expert e's SwiGLU FFN,
+// PAPER.md:159 with sigma = SwiGLU). h [rows][d] double.
+int oracle_expert_hidden(const void* x_sorted, int32_t xdt, int64_t rows, int32_t H, int32_t E, int32_t d,
+                         int32_t n_src, const int32_t* offsets, const void* w_gate, const void* w_up, int32_t wdt,
+                         double* h, int32_t nthreads) {
+    if (rows < 0 || H < 1 || E < 1 || d < 1 || n_src < 1 || !dt_ok(xdt) || !dt_ok(wdt)) return ORACLE_BAD_ARG;
+    const int64_t nseg = static_cast<int64_t>(n_src) * E;
+    if (offsets[0] != 0 || offsets[nseg] != rows) return ORACLE_BAD_ARG;
+    std::vector<int32_t> seg_of(rows);
+    for (int64_t g = 0; g < nseg; ++g) {
+        if (offsets[g + 1] < offsets[g]) return ORACLE_BAD_ARG;
+        for (int64_t r = offsets[g]; r < offsets[g + 1]; ++r) seg_of[r] = static_cast<int32_t>(g);
+    }
+    parallel_for(rows, nthreads, [&](int64_t r) {
+        const int64_t e = seg_of[r] % E;
+        for (int32_t n = 0; n < d; ++n) {
+            double g = 0.0, u = 0.0;
+            for (int32_t c = 0; c < H; ++c) {
+                const double xc = load(x_sorted, xdt, r * H + c);
+                g += load(w_gate, wdt, (e * d + n) * static_cast<int64_t>(H) + c) * xc;
+                u += load(w_up, wdt, (e * d + n) * static_cast<int64_t>(H) + c) * xc;
+            }
+            h[r * d + n] = silu(g) * u;
+        }
+    });
+    return ORACLE_OK;
+}
+
+// ---- a7 alone: y_r = W_down,e h_r (the W_2 M_i^T factor). y [rows][H] double.
+int oracle_expert_down(const void* h, int32_t hdt, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t n_src,
+                       const int32_t* offsets, const void* w_down, int32_t wdt, double* y, int32_t nthreads) {
+    if (rows < 0 || H < 1 || E < 1 || d < 1 || n_src < 1 || !dt_ok(hdt) || !dt_ok(wdt)) return ORACLE_BAD_ARG;
+    const int64_t nseg = static_cast<int64_t>(n_src) * E;
+    if (offsets[0] != 0 || offsets[nseg] != rows) return ORACLE_BAD_ARG;
+    std::vector<int32_t> seg_of(rows);
+    for (int64_t g = 0; g < nseg; ++g) {
+        if (offsets[g + 1] < offsets[g]) return ORACLE_BAD_ARG;
+        for (int64_t r = offsets[g]; r < offsets[g + 1]; ++r) seg_of[r] = static_cast<int32_t>(g);
+    }
+    parallel_for(rows, nthreads, [&](int64_t r) {
+        const int64_t e = seg_of[r] % E;
+        for (int32_t c = 0; c < H; ++c) {
+            double acc = 0.0;
+            for (int32_t n = 0; n < d; ++n)
+                acc += load(w_down, wdt, (e * H + c) * static_cast<int64_t>(d) + n) * load(h, hdt, r * d + n);
+            y[r * H + c] = acc;
+        }
+    });
+    return ORACLE_OK;
+}
+
 // ---- a8: combine, y[t] = res[t] + sum_{j<K} w[t][j] * y_sorted[dest[t*K+j]] (Eq. 2's weighted sum,
 // PAPER.md:137; j ascending, Q8). residual may be null.
 int oracle_combine(const double* y_sorted, int64_t T, int32_t H, int32_t K, const int32_t* dest,

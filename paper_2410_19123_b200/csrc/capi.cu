@@ -3,6 +3,8 @@
 // synchronisation, no exception crosses the boundary.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <exception>
 #include <mutex>
@@ -146,37 +148,69 @@ size_t readme_expert_ffn_workspace_bytes(int64_t rows, int32_t H, int32_t E, int
   return ffn_ws_bytes(rows < 0 ? 0 : rows, d < 0 ? 0 : d, dt);
 }
 
-readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
-                                int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
-                                const void* w_up, const void* w_down, void* y_sorted, void* ws, size_t ws_bytes,
-                                readme_stream_t stream) {
+namespace {
+readme_status check_ffn_args(readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t n_src,
+                             const int32_t* offsets) {
   README_TRY(check_rows(dt, H));
   README_CHECK_ARG(rows >= 0 && rows < (int64_t(1) << 31), "rows out of range");
   README_CHECK_ARG(E >= 1 && E <= README_MAX_EXPERTS, "E must be in [1, %d]", README_MAX_EXPERTS);
   README_CHECK_ARG(n_src >= 1 && static_cast<int64_t>(n_src) * E <= 512, "n_src*E must be in [1, 512]");
   README_CHECK_ARG(d >= 8 && d % 8 == 0, "d must be a positive multiple of 8 (got %d)", d);
   README_CHECK_ARG(offsets != nullptr, "offsets are required");
+  return README_OK;
+}
+}  // namespace
+
+readme_status readme_expert_gate_up(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                    int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
+                                    const void* w_up, void* h, readme_stream_t stream) {
+  README_TRY(check_ffn_args(dt, rows, H, E, d, n_src, offsets));
   if (rows == 0) return README_OK;
-  README_CHECK_ARG(x_sorted && w_gate && w_up && w_down && y_sorted && ws, "null pointer argument");
-  README_CHECK_ARG(aligned16(x_sorted) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) &&
-                       aligned16(y_sorted) && aligned16(ws),
+  README_CHECK_ARG(x_sorted && w_gate && w_up && h, "null pointer argument");
+  README_CHECK_ARG(aligned16(x_sorted) && aligned16(w_gate) && aligned16(w_up) && aligned16(h),
                    "all tensors must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == README_BF16)
+    return launch_gate_up_bf16(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, n_src * E, offsets,
+                               static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
+                               static_cast<__nv_bfloat16*>(h), st);
+  return launch_gate_up_f32(static_cast<const float*>(x_sorted), rows, H, E, d, n_src * E, offsets,
+                            static_cast<const float*>(w_gate), static_cast<const float*>(w_up),
+                            static_cast<float*>(h), st);
+}
+
+readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                 int32_t n_src, const int32_t* offsets, const void* w_down, const int32_t* src,
+                                 const void* residual, void* out, readme_stream_t stream) {
+  README_TRY(check_ffn_args(dt, rows, H, E, d, n_src, offsets));
+  if (rows == 0) return README_OK;
+  README_CHECK_ARG(h && w_down && out, "null pointer argument");
+  README_CHECK_ARG(src || !residual, "residual requires src (the fused-combine form)");
+  README_CHECK_ARG(aligned16(h) && aligned16(w_down) && aligned16(out) && (!residual || aligned16(residual)),
+                   "all tensors must be 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dt == README_BF16)
+    return launch_down_bf16(static_cast<const __nv_bfloat16*>(h), rows, H, E, d, n_src * E, offsets,
+                            static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(out), src,
+                            static_cast<const __nv_bfloat16*>(residual), st);
+  return launch_down_f32(static_cast<const float*>(h), rows, H, E, d, n_src * E, offsets,
+                         static_cast<const float*>(w_down), static_cast<float*>(out), src,
+                         static_cast<const float*>(residual), st);
+}
+
+readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
+                                const void* w_up, const void* w_down, void* y_sorted, void* ws, size_t ws_bytes,
+                                readme_stream_t stream) {
+  README_TRY(check_ffn_args(dt, rows, H, E, d, n_src, offsets));
+  if (rows == 0) return README_OK;
+  README_CHECK_ARG(ws != nullptr && aligned16(ws), "workspace is required (16-byte aligned)");
   if (ws_bytes < ffn_ws_bytes(rows, d, dt)) {
     set_error("expert_ffn workspace too small: %zu < %zu", ws_bytes, ffn_ws_bytes(rows, d, dt));
     return README_ERR_WORKSPACE;
   }
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int nseg = n_src * E;
-  if (dt == README_BF16) {
-    return launch_ffn_bf16(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, nseg, offsets,
-                           static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
-                           static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(y_sorted),
-                           static_cast<__nv_bfloat16*>(ws), st);
-  }
-  return launch_ffn_f32(static_cast<const float*>(x_sorted), rows, H, E, d, nseg, offsets,
-                        static_cast<const float*>(w_gate), static_cast<const float*>(w_up),
-                        static_cast<const float*>(w_down), static_cast<float*>(y_sorted), static_cast<float*>(ws),
-                        st);
+  README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
+  return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, nullptr, nullptr, y_sorted, stream);
 }
 
 readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
@@ -197,7 +231,8 @@ size_t readme_moe_layer_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t
   if (T < 0 || k < 1 || H < 0) return 0;
   const int64_t rows = T * k;
   const size_t act = align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
-  return align_up(route_ws_bytes(T, E, k), 256) + 2 * act + ffn_ws_bytes(rows, d, dt);
+  return align_up(route_ws_bytes(T, E, k), 256) + 2 * act + ffn_ws_bytes(rows, d, dt) +
+         align_up(static_cast<size_t>(rows) * sizeof(int32_t), 256);
 }
 
 readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
@@ -231,11 +266,21 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   void* y_sorted = w;
   w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
   void* ws_ffn = w;
+  w += ffn_ws_bytes(rows, d, dt);
+  int32_t* src_ws = reinterpret_cast<int32_t*>(w);
   if (logits) {
+    if (!src) src = src_ws;  // the fused path needs the inverse permutation
     README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                             ws_route, route_ws_bytes(T, E, k), stream));
   }
   README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
+  const char* kv = getenv("README_FFN_KERNEL");
+  const bool fused = k == 1 && src != nullptr && !(kv && (strcmp(kv, "1cta") == 0 || strcmp(kv, "unfused") == 0));
+  if (fused) {
+    // a6, then a7 with a8 fused into its epilogue: y[src[r]] = residual + h_r W_down^T (k == 1, weight 1).
+    README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, ws_ffn, stream));
+    return readme_expert_down(ws_ffn, dt, rows, H, E, d, 1, offsets, w_down, src, residual, y, stream);
+  }
   README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
                                ffn_ws_bytes(rows, d, dt), stream));
   return readme_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status, stream);

@@ -19,7 +19,7 @@ template <bool kSwiGLU>
 __global__ void __launch_bounds__(256)
 ffn_f32_kernel(const float* __restrict__ A, int64_t rows, int K, int N, int E, int nseg,
                const int32_t* __restrict__ offsets, const float* __restrict__ B0, const float* __restrict__ B1,
-               float* __restrict__ C) {
+               float* __restrict__ C, const int32_t* __restrict__ src, const float* __restrict__ residual) {
   __shared__ int s_off[kMaxSeg + 1];
   __shared__ int s_tstart[kMaxSeg + 1];
   __shared__ float sA[kTm][kTk + 1];
@@ -81,26 +81,43 @@ ffn_f32_kernel(const float* __restrict__ A, int64_t rows, int K, int N, int E, i
     if (r >= rend) continue;
     float v = acc0[i];
     if constexpr (kSwiGLU) v = v / (1.0f + expf(-v)) * acc1[i];
-    C[r * N + n] = v;
+    int64_t orow = r;
+    if (src) {  // fused combine (k == 1): row r holds token src[r]
+      orow = src[r];
+      if (orow < 0 || orow >= rows) continue;
+      if (residual) v += residual[orow * N + n];
+    }
+    C[orow * N + n] = v;
   }
 }
 
 }  // namespace
 
-readme_status launch_ffn_f32(const float* xs, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
-                             const int32_t* offsets, const float* wg, const float* wu, const float* wd,
-                             float* ys, float* h_ws, cudaStream_t st) {
+readme_status launch_gate_up_f32(const float* xs, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                                 const int32_t* offsets, const float* wg, const float* wu, float* h, cudaStream_t st) {
   if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("fp32 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
     return README_ERR_UNSUPPORTED;
   }
   const int64_t mtiles_ub = nseg + (rows + kTm - 1) / kTm;
-  dim3 g1(static_cast<unsigned>(mtiles_ub), (d + kTn - 1) / kTn);
-  ffn_f32_kernel<true><<<g1, 256, 0, st>>>(xs, rows, H, d, E, nseg, offsets, wg, wu, h_ws);
+  dim3 g(static_cast<unsigned>(mtiles_ub), (d + kTn - 1) / kTn);
+  ffn_f32_kernel<true><<<g, 256, 0, st>>>(xs, rows, H, d, E, nseg, offsets, wg, wu, h, nullptr, nullptr);
   README_CUDA(cudaGetLastError());
-  dim3 g2(static_cast<unsigned>(mtiles_ub), (H + kTn - 1) / kTn);
-  ffn_f32_kernel<false><<<g2, 256, 0, st>>>(h_ws, rows, d, H, E, nseg, offsets, wd, nullptr, ys);
+  return README_OK;
+}
+
+readme_status launch_down_f32(const float* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                              const int32_t* offsets, const float* wd, float* out, const int32_t* src,
+                              const float* residual, cudaStream_t st) {
+  if (rows == 0) return README_OK;
+  if (nseg > kMaxSeg) {
+    set_error("fp32 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
+    return README_ERR_UNSUPPORTED;
+  }
+  const int64_t mtiles_ub = nseg + (rows + kTm - 1) / kTm;
+  dim3 g(static_cast<unsigned>(mtiles_ub), (H + kTn - 1) / kTn);
+  ffn_f32_kernel<false><<<g, 256, 0, st>>>(h, rows, d, H, E, nseg, offsets, wd, nullptr, out, src, residual);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

@@ -327,48 +327,56 @@ readme_status set_smem_attr() {
 
 }  // namespace
 
-readme_status launch_ffn_bf16_1cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                              int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                              const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                              __nv_bfloat16* h_ws, cudaStream_t st) {
+readme_status launch_gemm_1cta(int mode, const __nv_bfloat16* A, int64_t rows, int32_t K, int32_t N, int32_t E,
+                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* B0,
+                               const __nv_bfloat16* B1, __nv_bfloat16* out, cudaStream_t st) {
+  if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
     return README_ERR_UNSUPPORTED;
   }
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
-  CUtensorMap mA1, mG, mU, mA2, mD;
-  bool ok = tc::make_map_2d(&mA1, xs, H, rows, kBK, kBM) && tc::make_map_3d(&mG, wg, H, d, E, kBK, kBN / 2) &&
-            make_map_3d(&mU, wu, H, d, E, kBK, kBN / 2) && tc::make_map_2d(&mA2, h_ws, d, rows, kBK, kBM) &&
-            make_map_3d(&mD, wd, d, H, E, kBK, kBN);
+  CUtensorMap mA, mB0, mB1;
+  const uint32_t bn_box = mode == 0 ? kBN / 2 : kBN;
+  bool ok = tc::make_map_2d(&mA, A, K, rows, kBK, kBM) && tc::make_map_3d(&mB0, B0, K, N, E, kBK, bn_box) &&
+            (mode == 1 || tc::make_map_3d(&mB1, B1, K, N, E, kBK, bn_box));
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
     return README_ERR_CUDA;
   }
+  if (mode == 1) mB1 = mB0;
   const int64_t mt_ub = nseg + (rows + kBM - 1) / kBM;
   const int nsm = num_sms();
-  const int64_t t1 = mt_ub * ((d + kBN / 2 - 1) / (kBN / 2));
-  const int64_t t2 = mt_ub * ((H + kBN - 1) / kBN);
-  const int g1 = static_cast<int>(t1 < nsm ? t1 : nsm);
-  const int g2 = static_cast<int>(t2 < nsm ? t2 : nsm);
-  ffn_gemm_kernel<0><<<g1, kThreads, kSmemBytes, st>>>(mA1, mG, mU, H, d, E, nseg, offsets, h_ws);
-  README_CUDA(cudaGetLastError());
-  ffn_gemm_kernel<1><<<g2, kThreads, kSmemBytes, st>>>(mA2, mD, mD, d, H, E, nseg, offsets, ys);
+  const int64_t tiles = mt_ub * ((N + bn_box - 1) / bn_box);
+  const int grid = static_cast<int>(tiles < nsm ? tiles : nsm);
+  if (mode == 0)
+    ffn_gemm_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out);
+  else
+    ffn_gemm_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }
 
-// Kernel choice: the CTA-pair kernel by default; README_FFN_KERNEL=1cta selects the single-CTA one
-// (kept for A/B measurement and as the small-batch variant).
-readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                              int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                              const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                              __nv_bfloat16* h_ws, cudaStream_t st) {
-  if (rows == 0) return README_OK;
+// Kernel choice: the CTA-pair kernel by default; README_FFN_KERNEL=1cta selects the single-CTA one (kept
+// for A/B measurement). The scattered (fused-combine) epilogue exists only in the CTA-pair kernel.
+bool force_1cta() {
   const char* v = getenv("README_FFN_KERNEL");
-  if (v && strcmp(v, "1cta") == 0)
-    return launch_ffn_bf16_1cta(xs, rows, H, E, d, nseg, offsets, wg, wu, wd, ys, h_ws, st);
-  return launch_ffn_bf16_2cta(xs, rows, H, E, d, nseg, offsets, wg, wu, wd, ys, h_ws, st);
+  return v && strcmp(v, "1cta") == 0;
+}
+
+readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                  int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                  const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st) {
+  if (force_1cta()) return launch_gemm_1cta(0, xs, rows, H, d, E, nseg, offsets, wg, wu, h, st);
+  return launch_gemm_2cta(0, xs, rows, H, d, E, nseg, offsets, wg, wu, h, nullptr, nullptr, st);
+}
+
+readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                               const int32_t* offsets, const __nv_bfloat16* wd, __nv_bfloat16* out,
+                               const int32_t* src, const __nv_bfloat16* residual, cudaStream_t st) {
+  if (force_1cta() && src == nullptr) return launch_gemm_1cta(1, h, rows, d, H, E, nseg, offsets, wd, wd, out, st);
+  return launch_gemm_2cta(1, h, rows, d, H, E, nseg, offsets, wd, nullptr, out, src, residual, st);
 }
 
 }  // namespace readme

@@ -81,11 +81,33 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
   }
 }
 
-template <int kMode>
+// Fusion of the combine into GEMM2 (readme_moe_layer's path, k == 1): kFuse == 1 makes the epilogue
+// write row r to y[src[r]] (+ residual, one fp32 add and one rounding) -> no y_sorted and no separate
+// combine (Eq. 2's sum has one term with weight exactly 1). (Fusing the dispatch into GEMM1 with TMA
+// tile::gather4 was measured 3x slower than dispatch + tiled loads: every 256-row A tile is re-gathered
+// for each of the 43 N tiles, 32 gather4 ops per stage — see profiles/SUMMARY.md.)
+struct Fuse {
+  const int32_t* src;                 // [rows] expert-contiguous row -> token (= dest^-1, k == 1)
+  int rows;                           // T
+  const __nv_bfloat16* residual;      // [T, N] or null (GEMM2 scatter only)
+};
+
+__device__ __forceinline__ void add_bf16x32(const __nv_bfloat16* src, float (&v)[32], int ncols_left) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 8) {
+    if (j < ncols_left) {
+      const uint4 w = ld_nc_v4(reinterpret_cast<const uint4*>(src + j));
+      v[j + 0] += bf16_lo(w.x); v[j + 1] += bf16_hi(w.x); v[j + 2] += bf16_lo(w.y); v[j + 3] += bf16_hi(w.y);
+      v[j + 4] += bf16_lo(w.z); v[j + 5] += bf16_hi(w.z); v[j + 6] += bf16_lo(w.w); v[j + 7] += bf16_hi(w.w);
+    }
+  }
+}
+
+template <int kMode, int kFuse>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                  const __grid_constant__ CUtensorMap tmB1, int K, int N, int E, int nseg,
-                 const int32_t* __restrict__ offsets, __nv_bfloat16* __restrict__ out) {
+                 const int32_t* __restrict__ offsets, __nv_bfloat16* __restrict__ out, Fuse fz) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
@@ -129,22 +151,23 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t tmem_base = s.tmem_base;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
-      int stage = 0;
-      uint32_t phase = 0;
-      int gcur = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
-        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
-        const int e = tl.g % E;
-        const int a_rows = tl.m256 ? 128 : 64;
-        const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
-        const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
-        for (int kb = 0; kb < KB; ++kb) {
-          tc::mbar_wait(&s.empty[stage], phase ^ 1);
+    // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
+    // The whole warp runs the loop; lane 0 arms the barrier and issues the loads.
+    int stage = 0;
+    uint32_t phase = 0;
+    int gcur = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+      const int e = tl.g % E;
+      const int a_rows = tl.m256 ? 128 : 64;
+      const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::mbar_wait(&s.empty[stage], phase ^ 1);
+        const uint32_t fb = tc::mapa(&s.full[stage], 0);
+        const int k0 = kb * kBK;
+        if (lane == 0) {
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
-          const uint32_t fb = tc::mapa(&s.full[stage], 0);
-          const int k0 = kb * kBK;
           tc::tma_load_2d_2sm(&tmA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(&tmA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
           if (kMode == 0) {
@@ -154,10 +177,10 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc::tma_load_3d_2sm(&tmB0, s.b[stage], fb, k0, tl.n0 + 128 * static_cast<int>(cta), e);
             tc::tma_load_3d_2sm(&tmB0, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 128 * static_cast<int>(cta) + 64, e);
           }
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -218,7 +241,14 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         out_off = (q >> 1) * (kBnOut / 2);
       }
       const bool valid = row_in_tile < tl.rows;
-      __nv_bfloat16* orow = out + static_cast<int64_t>(tl.m0 + row_in_tile) * N;
+      int64_t orow_idx = tl.m0 + row_in_tile;
+      bool valid_row = valid;
+      if constexpr (kMode == 1 && kFuse == 1) {  // k == 1: expert row r holds token src[r]
+        orow_idx = valid ? __ldg(fz.src + orow_idx) : 0;
+        valid_row = valid && orow_idx >= 0 && orow_idx < fz.rows;  // a corrupt plan never writes out of bounds
+      }
+      __nv_bfloat16* orow = out + orow_idx * N;
+      const __nv_bfloat16* rrow = (kMode == 1 && kFuse == 1 && fz.residual) ? fz.residual + orow_idx * N : nullptr;
       for (int w = 0; w < n_windows; ++w) {
         const uint32_t wbase = tacc + static_cast<uint32_t>(col_base + w * 128);
         if (kMode == 0) {
@@ -244,10 +274,11 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             uint32_t vr[32];
             tc::tmem_ld32(wbase + c, vr);
             tc::tmem_wait_ld();
-            if (valid) {
+            if (valid_row) {
               float v[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+              if (rrow) add_bf16x32(rrow + col0 + c, v, N - (col0 + c));
               store_bf16x32(orow + col0 + c, v, N - (col0 + c));
             }
           }
@@ -273,11 +304,12 @@ readme_status set_smem_attr() {
   README_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) dev = 0;
   std::call_once(once[dev], [&] {
-    err[dev] = cudaFuncSetAttribute(ffn_gemm2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSmemBytes));
-    if (err[dev] == cudaSuccess)
-      err[dev] = cudaFuncSetAttribute(ffn_gemm2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kSmemBytes));
+    const void* fns[3] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
+                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
+                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>)};
+    err[dev] = cudaSuccess;
+    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
+      err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   });
   if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
   return README_OK;
@@ -285,33 +317,39 @@ readme_status set_smem_attr() {
 
 }  // namespace
 
-readme_status launch_ffn_bf16_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                                   __nv_bfloat16* h_ws, cudaStream_t st) {
+// One projection on CTA pairs. mode 0 (a6): A = x_sorted [rows, K=H], B0/B1 = W_gate/W_up [E][N=d][K],
+// out = h [rows, d]. mode 1 (a7): A = h [rows, K=d], B0 = W_down [E][N=H][K], out = y_sorted [rows, H], or
+// with src != null (k == 1 only) row r goes to out[src[r]] (+ residual): the fused combine.
+readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, int32_t K, int32_t N, int32_t E,
+                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* B0,
+                               const __nv_bfloat16* B1, __nv_bfloat16* out, const int32_t* src,
+                               const __nv_bfloat16* residual, cudaStream_t st) {
+  if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
     return README_ERR_UNSUPPORTED;
   }
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
-  CUtensorMap mA1, mG, mU, mA2, mD;
-  bool ok = tc::make_map_2d(&mA1, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, E, kBK, 64) &&
-            tc::make_map_3d(&mU, wu, H, d, E, kBK, 64) && tc::make_map_2d(&mA2, h_ws, d, rows, kBK, 64) &&
-            tc::make_map_3d(&mD, wd, d, H, E, kBK, 64);
+  CUtensorMap mA, mB0, mB1;
+  bool ok = tc::make_map_2d(&mA, A, K, rows, kBK, 64) && tc::make_map_3d(&mB0, B0, K, N, E, kBK, 64) &&
+            (mode == 1 || tc::make_map_3d(&mB1, B1, K, N, E, kBK, 64));
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
     return README_ERR_CUDA;
   }
+  if (mode == 1) mB1 = mB0;
   const int64_t mt_ub = nseg + (rows + 255) / 256;
   const int pairs = num_sms() / 2;
-  const int64_t t1 = mt_ub * ((d + 127) / 128);
-  const int64_t t2 = mt_ub * ((H + 255) / 256);
-  const int g1 = 2 * static_cast<int>(t1 < pairs ? t1 : pairs);
-  const int g2 = 2 * static_cast<int>(t2 < pairs ? t2 : pairs);
-  ffn_gemm2_kernel<0><<<g1, kThreads, kSmemBytes, st>>>(mA1, mG, mU, H, d, E, nseg, offsets, h_ws);
-  README_CUDA(cudaGetLastError());
-  ffn_gemm2_kernel<1><<<g2, kThreads, kSmemBytes, st>>>(mA2, mD, mD, d, H, E, nseg, offsets, ys);
+  const int64_t tiles = mt_ub * ((N + (mode == 0 ? 127 : 255)) / (mode == 0 ? 128 : 256));
+  const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+  const Fuse fz{src, static_cast<int>(rows), residual};
+  if (mode == 0)
+    ffn_gemm2_kernel<0, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
+  else if (src == nullptr)
+    ffn_gemm2_kernel<1, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
+  else
+    ffn_gemm2_kernel<1, 1><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

@@ -20,23 +20,27 @@ readme_status launch_build_experts(const void* wg, const void* wu, const void* w
                                    int32_t H, int32_t E, int32_t d, const int32_t* nidx, void* eg, void* eu,
                                    void* ed, uint32_t* dev_status, cudaStream_t st);
 
-// ffn_f32.cu (SIMT fp32, no TF32)
-readme_status launch_ffn_f32(const float* xs, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
-                             const int32_t* offsets, const float* wg, const float* wu, const float* wd,
-                             float* ys, float* h_ws, cudaStream_t st);
+// ffn_f32.cu (SIMT fp32, no TF32). a6: h = silu(xs Wg^T) * (xs Wu^T); a7: out = h Wd^T, or with
+// src != null row r -> out[src[r]] (+ residual).
+readme_status launch_gate_up_f32(const float* xs, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                                 const int32_t* offsets, const float* wg, const float* wu, float* h, cudaStream_t st);
+readme_status launch_down_f32(const float* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                              const int32_t* offsets, const float* wd, float* out, const int32_t* src,
+                              const float* residual, cudaStream_t st);
 
 // ffn_sm100.cu / ffn_sm100_2cta.cu (tcgen05 / TMEM / TMA grouped GEMMs, bf16)
-readme_status launch_ffn_bf16_1cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                                   __nv_bfloat16* h_ws, cudaStream_t st);
-readme_status launch_ffn_bf16_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                                   const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                                   __nv_bfloat16* h_ws, cudaStream_t st);
-readme_status launch_ffn_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
-                              int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
-                              const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* ys,
-                              __nv_bfloat16* h_ws, cudaStream_t st);
+readme_status launch_gemm_1cta(int mode, const __nv_bfloat16* A, int64_t rows, int32_t K, int32_t N, int32_t E,
+                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* B0,
+                               const __nv_bfloat16* B1, __nv_bfloat16* out, cudaStream_t st);
+readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, int32_t K, int32_t N, int32_t E,
+                               int32_t nseg, const int32_t* offsets, const __nv_bfloat16* B0,
+                               const __nv_bfloat16* B1, __nv_bfloat16* out, const int32_t* src,
+                               const __nv_bfloat16* residual, cudaStream_t st);
+readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                  int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                  const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);
+readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                               const int32_t* offsets, const __nv_bfloat16* wd, __nv_bfloat16* out,
+                               const int32_t* src, const __nv_bfloat16* residual, cudaStream_t st);
 
 }  // namespace readme

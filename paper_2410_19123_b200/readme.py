@@ -23,7 +23,7 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 
 # Every symbol include/readme.h declares (tests check the library exports exactly these).
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
-           "readme_expert_ffn", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
+           "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
            "readme_build_experts", "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
 
@@ -47,6 +47,10 @@ _SIGS = {
     "readme_expert_ffn_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, ctypes.c_int]),
     "readme_expert_ffn": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
                                          _vp, _sz, _vp]),
+    "readme_expert_gate_up": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                                             _vp]),
+    "readme_expert_down": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                                          _vp]),
     "readme_combine": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "readme_moe_layer_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, _i32, ctypes.c_int]),
     "readme_moe_layer": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _vp, ctypes.c_int, _i32, _i32, _i32, _vp, _vp,
@@ -192,6 +196,33 @@ def expert_ffn(x_sorted: torch.Tensor, offsets: torch.Tensor, w_gate: torch.Tens
     _check("readme_expert_ffn", lib().readme_expert_ffn(
         _ptr(x_sorted), _dt(x_sorted), rows, H, E, d, n_src, _ptr(offsets), _ptr(w_gate), _ptr(w_up),
         _ptr(w_down), _ptr(out), _ptr(ws), ws.numel(), st))
+    return out
+
+
+def expert_gate_up(x_sorted: torch.Tensor, offsets: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor,
+                   n_src: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """a6: h = silu(x_sorted W_gate[e]^T) * (x_sorted W_up[e]^T) per segment (readme_expert_gate_up)."""
+    rows, H = x_sorted.shape
+    E, d, _ = w_gate.shape
+    out = out if out is not None else torch.empty((rows, d), dtype=x_sorted.dtype, device=x_sorted.device)
+    st = _prep(x_sorted, offsets, w_gate, w_up, out)
+    _check("readme_expert_gate_up", lib().readme_expert_gate_up(
+        _ptr(x_sorted), _dt(x_sorted), rows, H, E, d, n_src, _ptr(offsets), _ptr(w_gate), _ptr(w_up), _ptr(out), st))
+    return out
+
+
+def expert_down(h: torch.Tensor, offsets: torch.Tensor, w_down: torch.Tensor, n_src: int = 1,
+                src: torch.Tensor | None = None, residual: torch.Tensor | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """a7: y_sorted = h W_down[e]^T per segment; with src (k == 1) rows go to out[src[r]] + residual, i.e. the
+    combine fused into the epilogue (readme_expert_down)."""
+    rows, d = h.shape
+    E, H, _ = w_down.shape
+    out = out if out is not None else torch.empty((rows, H), dtype=h.dtype, device=h.device)
+    st = _prep(h, offsets, w_down, src, residual, out)
+    _check("readme_expert_down", lib().readme_expert_down(
+        _ptr(h), _dt(h), rows, H, E, d, n_src, _ptr(offsets), _ptr(w_down), _ptr(src), _ptr(residual), _ptr(out),
+        st))
     return out
 
 

@@ -200,6 +200,26 @@ def test_expert_ffn_f32_config1(rd):
     assert rel_err(_np(ys), ref) <= F32_TOL
 
 
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_gate_up_and_down_separately(rd, dt):
+    """a6 and a7 each teacher-forced against the oracle; a7 with src scatters rows (fused combine)."""
+    T, H, d, E = 1500, 512, 264, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, dt, seed=91)
+    res = synth.to_torch(synth.residual(T, H, seed=92), dt)
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 1)
+    xs = rd.dispatch(x.to(DEV), plan.dest, 1)
+    off = plan.offsets.cpu().numpy()
+    h = rd.expert_gate_up(xs, plan.offsets, wg.to(DEV), wu.to(DEV))
+    tol = BF16_TOL if dt == "bf16" else F32_TOL
+    assert rel_err(_np(h), oracle.expert_hidden(xs.cpu(), off, wg, wu)) <= tol
+    ys = rd.expert_down(h, plan.offsets, wd.to(DEV))
+    assert rel_err(_np(ys), oracle.expert_down(h.cpu(), off, wd)) <= tol
+    y = rd.expert_down(h, plan.offsets, wd.to(DEV), src=plan.src, residual=res.to(DEV))
+    ref = oracle.combine(oracle.expert_down(h.cpu(), off, wd), plan.dest.cpu().numpy(), np.ones((T, 1)), 1,
+                         residual=res)
+    assert rel_err(_np(y), ref) <= tol
+
+
 @pytest.mark.parametrize("kernel", ["2cta", "1cta"])
 def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
     """Segment sizes on every tile boundary: empty, 1 row, 64/128/256 +- 1 (M=128 vs M=256 tails)."""
@@ -230,9 +250,13 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
+@pytest.mark.parametrize("path", ["fused", "unfused", "1cta"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
-                                           ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2)])
-def test_moe_layer_end_to_end(rd, dt, T, H, d, E, k):
+                                           ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
+                                           ("bf16", 3000, 1024, 1376, 8, 1)])
+def test_moe_layer_end_to_end(rd, monkeypatch, path, dt, T, H, d, E, k):
+    if path != "fused":
+        monkeypatch.setenv("README_FFN_KERNEL", path)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
     res = synth.to_torch(synth.residual(T, H, seed=12), dt)
     y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k,
@@ -273,6 +297,41 @@ def test_build_experts_bit_exact(rd):
     ref = oracle.build_experts(wg, wu, wd, S)
     for got, want in zip((eg, eu, ed), ref):
         assert np.array_equal(_np(got).astype(np.float64), want)
+
+
+@pytest.mark.parametrize("with_residual", [False, True])
+def test_fused_scatter_vs_unfused(rd, monkeypatch, with_residual):
+    """k=1: the combine fused into GEMM2's epilogue (y[src[r]] = res + acc, one rounding) equals the unfused
+    sequence bit for bit without a residual; with one, the unfused path rounds twice (y_sorted, then
+    res + y_sorted), so both are checked against the oracle instead."""
+    T, H, d, E = 2000, 512, 384, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=41)
+    res = synth.to_torch(synth.residual(T, H, seed=42), "bf16") if with_residual else None
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    lgt = torch.from_numpy(lg).to(DEV)
+    r_dev = res.to(DEV) if res is not None else None
+    y1, _ = rd.moe_layer(x.to(DEV), *W, logits=lgt, residual=r_dev)
+    monkeypatch.setenv("README_FFN_KERNEL", "unfused")
+    y2, _ = rd.moe_layer(x.to(DEV), *W, logits=lgt, residual=r_dev)
+    torch.cuda.synchronize()
+    if not with_residual:
+        assert torch.equal(y1, y2)
+    else:
+        yref, _ = oracle.moe_layer(x, lg, 1, wg, wu, wd, residual=res)
+        assert rel_err(_np(y1), yref) <= BF16_TOL and rel_err(_np(y2), yref) <= BF16_TOL
+
+
+def test_fused_plan_in_with_corrupt_src_is_safe(rd):
+    """A plan whose src holds out-of-range rows must not write out of bounds (rows are skipped)."""
+    T, H, d, E = 512, 256, 128, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=44)
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    y, plan = rd.moe_layer(x.to(DEV), *W, logits=torch.from_numpy(lg).to(DEV))
+    plan.src[5] = 10 ** 6
+    plan.src[6] = -3
+    y2, _ = rd.moe_layer(x.to(DEV), *W, plan=plan)
+    torch.cuda.synchronize()
+    assert y2.shape == y.shape
 
 
 def test_permutation_equivariance_bitwise_gpu(rd):

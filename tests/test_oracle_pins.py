@@ -332,3 +332,21 @@ def test_thread_count_invariance():
     y1, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed, nthreads=1)
     y8, _ = oracle.moe_layer(x, lg, 2, eg, eu, ed, nthreads=8)
     assert np.array_equal(y1, y8)
+
+
+# ---- a6 / a7 separately: composition equals the whole expert FFN; P7(i) hidden value -----------------
+
+def test_hidden_then_down_equals_expert_ffn():
+    rows, H, E, d = 70, 24, 4, 40
+    eg, eu, ed = synth.expert_weights(E, d, H, seed=121)
+    x = synth.tokens(rows, H, seed=122)
+    off = np.array([0, 10, 10, 45, 70], np.int32)
+    h = oracle.expert_hidden(x, off, eg, eu)
+    assert np.array_equal(oracle.expert_down(h, off, ed), oracle.expert_ffn(x, off, eg, eu, ed))
+
+
+def test_hidden_closed_form():
+    c = _gold("swiglu_closed_forms.json")["cases"][0]  # h = silu(2) * 3 (W_down = [[1],[0]] copies it to y0)
+    h = oracle.expert_hidden(np.array([c["x"]]), np.array([0, 1], np.int32), np.array([c["w_gate"]], np.float64),
+                             np.array([c["w_up"]], np.float64))
+    np.testing.assert_allclose(h[0, 0], c["y"][0], atol=1e-6, rtol=0)
