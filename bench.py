@@ -203,10 +203,144 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_decode(args):
+    """Config 3: decode-style expert-aware batching. Per step the queued batch (B tokens with Zipf(1)-skewed
+    pre-gated experts) goes through one Llama-2-7B-shaped MoE layer. HBM-bound: the
+    algorithmic bytes are the weights of the experts the batch touches (U x 3*H*d*2) plus the activations.
+    Also sweeps B and the number of unique experts per batch (per-token latency vs unique experts is
+    linear, PAPER.md:234)."""
+    import torch
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = dict(synth.CONFIGS[3])
+    H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
+    inp = make_inputs(dict(synth.CONFIGS[2]), 512, 0, dev)
+    eg, eu, ed = inp["w"]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    pk, pk_src = peaks()
+
+    def measure(ids):
+        B = ids.shape[0]
+        lg = torch.from_numpy(synth.logits_for_assignments(ids, E, seed=B)).to(dev)
+        x = synth.to_torch(synth.tokens(B, H, seed=B), "bf16").to(dev)
+        plan = rd.new_plan(B, E, k, dev)
+        y = torch.empty_like(x)
+        ws = torch.empty(rd.moe_layer_workspace_bytes(B, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
+        fn = lambda: rd.moe_layer(x, eg, eu, ed, k=k, logits=lg, plan=plan, out=y, ws=ws)
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            ms.append((a, b))
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in ms]
+        U = int(len(np.unique(ids)))
+        byts = U * 3.0 * H * d * 2 + 4.0 * B * H * 2
+        t = float(np.mean(ms))
+        return {"B": B, "unique_experts": U, "ms": t, "tokens_per_s": B / (t * 1e-3),
+                "GBps": byts / (t * 1e-3) / 1e9, "hbm_frac": byts / (t * 1e-3) / 1e9 / pk["hbm_gbs"]}
+
+    sweep = [measure(synth.assignments_zipf(B, E, 1.0, seed=synth.MASTER_SEED + 3 + B)) for B in (64, 128, 256, 512)]
+    uniq = [measure(synth.assignments_unique(256, u, E, seed=synth.MASTER_SEED + 30 + u)) for u in range(1, E + 1)]
+    us = np.array([r["unique_experts"] for r in uniq], np.float64)
+    ts = np.array([r["ms"] for r in uniq]) * 1e3
+    slope, icpt = np.polyfit(us, ts, 1)
+    r2 = 1 - np.sum((ts - (slope * us + icpt)) ** 2) / np.sum((ts - ts.mean()) ** 2)
+    main_pt = sweep[2]
+    line = {"metric": METRIC, "value": main_pt["tokens_per_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main_pt["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config3_decode_batching", "B": 256, "H": H, "D": cfg["D"], "E": E, "d": d,
+                       "k": k, "assignments": "Zipf(s=1) over experts", "l2": "flushed between timed steps"},
+            "roofline": {"bound": "hbm", "achieved": main_pt["GBps"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": main_pt["hbm_frac"], "traffic": None,
+                         "algorithmic": "U*3*H*d*2 (touched experts' weights) + 4*B*H*2 per step",
+                         "peak_source": f"{pk_src} HBM copy (MEASURED_PEAKS.json)"},
+            "decode_sweep": sweep,
+            "unique_expert_sweep": {"points": uniq, "us_per_extra_expert": float(slope), "intercept_us": float(icpt),
+                                    "r2_linear": float(r2), "paper": "linear per-token latency in unique experts "
+                                                                   "(PAPER.md:234, fig:batching b)"},
+            "gpu_launches": 5 * args.steps}
+    print(json.dumps(line), flush=True)
+
+
+def run_stack(args):
+    """Config 4: the full 32-layer refactored MoE stack (MoE-only pre-norm, reading Q10), T = 16384 tokens
+    (4 requests x 4096, Markov expert locality p = 0.672), routed ONCE per request batch
+     — one readme_moe_stack call per step."""
+    import torch
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = dict(synth.CONFIGS[4])
+    T, H, d, E, k, L = args.tokens or cfg["T"], cfg["H"], cfg["d"], cfg["E"], cfg["k"], cfg["L"]
+    seed = synth.MASTER_SEED + 4
+    layers = [synth.expert_weights_device(E, d, H, dev, seed=seed, layer=l) for l in range(L)]
+    ids = synth.assignments_markov(T // 4096 if T >= 4096 else 1, min(T, 4096), E, 0.672, seed=seed)
+    lg = torch.from_numpy(synth.logits_for_assignments(ids, E, seed=seed)).to(dev)
+    x0 = synth.to_torch(synth.tokens(T, H, seed=seed), "bf16").to(dev)
+    x = torch.empty_like(x0)
+    plan = rd.new_plan(T, E, k, dev)
+    ws = torch.empty(rd.moe_stack_workspace_bytes(T, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        x.copy_(x0)
+        rd.moe_stack(x, layers, k=k, logits=lg, plan=plan, ws=ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ms = []
+    with Clocks(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step()
+            b.record()
+            ms.append((a, b))
+        torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in ms]
+    t = float(np.mean(ms))
+    pk, pk_src = peaks()
+    flops = L * 6.0 * T * k * H * d
+    ach = flops / (t * 1e-3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    line = {"metric": METRIC, "value": T / (t * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config4_stack32", "T": T, "L": L, "H": H, "E": E, "d": d, "k": k,
+                       "routing": "Markov locality p=0.672, routed once per step", "l2": "flushed between steps"},
+            "layer_tokens_per_s": T * L / (t * 1e-3),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "traffic": None, "algorithmic": f"L*6*T*k*H*d = {flops:.4g} FLOP per step",
+                         "peak_source": f"{pk_src} bf16 sustained (a ~80 ms step)"},
+            "gpu_launches": (2 + 3 * L) * args.steps + args.steps, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == 3 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        run_decode(args)
+        return
+    if args.config == 4 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        run_stack(args)
         return
     import torch
     import torch.distributed as dist

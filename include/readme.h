@@ -14,6 +14,7 @@
  *   readme_combine    a8     gather back to token order, weight, add residual
  *   readme_moe_layer  a1-a8  the whole layer; with logits == NULL it reuses a routing plan (a9: route
  *                            once, reuse across all L layers)
+ *   readme_moe_stack         L pre-norm MoE layers routed once (config 4), in place
  *   readme_build_experts     setup: slice expert stacks out of the dense FFN
  * Readings of the paper (Q1..Q14) are listed in DESIGN.md; they are cited below where they decide a
  * behaviour.
@@ -142,6 +143,24 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                                readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, const void* w_gate,
                                const void* w_up, const void* w_down, const void* residual, void* y,
                                int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
+                               int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                               readme_stream_t stream);
+
+/* The 32-layer refactored stack (BASELINE config 4; reading Q10 in DESIGN.md): a MoE-only pre-norm stack
+ *     x <- x + MoE_l(RMSNorm(x)),  l = 0..L-1,  RMSNorm(x) = x / sqrt(mean(x^2) + eps) (weight 1),
+ * routed ONCE for all layers ("expert selection can be determined at the outset";
+ * :237: "routed to Expert 1 in every layer"). x [T,H] is updated in place. w_gate/w_up/w_down are HOST
+ * arrays of L device pointers (each as in readme_expert_ffn). logits == NULL: plan-in mode as in
+ * readme_moe_layer. The attention blocks of the paper's model are outside this path.
+ * readme_dispatch_rmsnorm is its pre-norm dispatch: x_sorted[dest[t*k+j]] = RMSNorm(x[t]), fp32 statistics. */
+readme_status readme_dispatch_rmsnorm(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                      const int32_t* dest, float eps, void* x_sorted, uint32_t* dev_status,
+                                      readme_stream_t stream);
+size_t readme_moe_stack_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t d, int32_t k, readme_dtype dt);
+readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
+                               readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, int32_t L,
+                               const void* const* w_gate, const void* const* w_up, const void* const* w_down,
+                               float eps, int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
                                int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
                                readme_stream_t stream);
 

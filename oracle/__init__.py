@@ -197,6 +197,35 @@ def expert_down(h, offsets, w_down, n_src: int = 1, nthreads: int | None = None)
     return out
 
 
+def rmsnorm(x, eps: float = 1e-5):
+    """RMSNorm with weight 1 (reading Q10): x / sqrt(mean(x^2) + eps), fp64."""
+    lib = _load()
+    xa, xdt = _as_input(x)
+    T, H = xa.shape
+    out = np.empty((T, H), np.float64)
+    rc = lib.oracle_rmsnorm(_p(xa), ctypes.c_int32(xdt), ctypes.c_int64(T), ctypes.c_int32(H), ctypes.c_double(eps),
+                            _p(out))
+    _check(rc, "oracle_rmsnorm")
+    return out
+
+
+def moe_stack(x, logits, k: int, layers, eps: float = 1e-5, nthreads: int | None = None):
+    """Config 4: x <- x + MoE_l(RMSNorm(x)) for each layer, routed ONCE from the pre-gating logits
+    (PAPER.md:140-142, :237). `layers` = [(w_gate, w_up, w_down), ...]. Returns (x fp64, plan)."""
+    plan = route(logits, k)
+    xa, _ = _as_input(x)
+    xd = np.array(xa if xa.dtype != np.uint16 else _bf16_to_f64(xa), dtype=np.float64)
+    for (wg, wu, wd) in layers:
+        xs = dispatch(rmsnorm(xd, eps), plan["dest"], k)
+        ys = expert_ffn(xs, plan["offsets"], wg, wu, wd, nthreads=nthreads)
+        xd = combine(ys, plan["dest"], plan["topk_w"], k, residual=xd)
+    return xd, plan
+
+
+def _bf16_to_f64(a):
+    return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
 def combine(y_sorted, dest, topk_w, k: int, residual=None):
     """a8: y[t] = res[t] + sum_j w[t,j] * y_sorted[dest[t*k+j]] (j ascending)."""
     lib = _load()

@@ -180,6 +180,22 @@ int oracle_expert_ffn(const void* x_sorted, int32_t xdt, int64_t rows, int32_t H
     return ORACLE_OK;
 }
 
+// ---- RMSNorm for the MoE-only pre-norm stack (reading Q10 in DESIGN.md; Llama-2's RMSNorm with weight 1):
+// y[t] = x[t] / sqrt(mean_c x[t][c]^2 + eps).
+int oracle_rmsnorm(const void* x, int32_t xdt, int64_t T, int32_t H, double eps, double* y) {
+    if (T < 0 || H < 1 || eps < 0 || !dt_ok(xdt)) return ORACLE_BAD_ARG;
+    for (int64_t t = 0; t < T; ++t) {
+        double ss = 0.0;
+        for (int32_t c = 0; c < H; ++c) {
+            const double v = load(x, xdt, t * H + c);
+            ss += v * v;
+        }
+        const double r = 1.0 / std::sqrt(ss / H + eps);
+        for (int32_t c = 0; c < H; ++c) y[t * H + c] = load(x, xdt, t * H + c) * r;
+    }
+    return ORACLE_OK;
+}
+
 // ---- a6 alone: h_r = silu(W_gate,e x_r) * (W_up,e x_r) (the hidden activation of expert e's SwiGLU FFN,
 // PAPER.md:159 with sigma = SwiGLU). h [rows][d] double.
 int oracle_expert_hidden(const void* x_sorted, int32_t xdt, int64_t rows, int32_t H, int32_t E, int32_t d,

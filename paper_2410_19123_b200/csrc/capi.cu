@@ -286,6 +286,75 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   return readme_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status, stream);
 }
 
+readme_status readme_dispatch_rmsnorm(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                      const int32_t* dest, float eps, void* x_sorted, uint32_t* dev_status,
+                                      readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(T >= 0 && k >= 1 && T * static_cast<int64_t>(k) < (int64_t(1) << 31), "bad T/k");
+  README_CHECK_ARG(eps >= 0.f, "eps must be >= 0");
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(x && dest && x_sorted, "x, dest and x_sorted are required");
+  README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x and x_sorted must be 16-byte aligned");
+  return launch_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t readme_moe_stack_workspace_bytes(int64_t T, int32_t H, int32_t E, int32_t d, int32_t k, readme_dtype dt) {
+  return readme_moe_layer_workspace_bytes(T, H, E, d, k, dt);
+}
+
+readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, const void* logits,
+                               readme_dtype logits_dt, int32_t E, int32_t k, int32_t d, int32_t L,
+                               const void* const* w_gate, const void* const* w_up, const void* const* w_down,
+                               float eps, int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
+                               int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                               readme_stream_t stream) {
+  README_TRY(check_route_args(T, E, k));
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(d >= 8 && d % 8 == 0, "d must be a positive multiple of 8 (got %d)", d);
+  README_CHECK_ARG(L >= 0, "L must be >= 0");
+  README_CHECK_ARG(counts && offsets, "counts and offsets are required");
+  if (T == 0) {
+    if (logits) return readme_route(nullptr, logits_dt, 0, E, k, nullptr, nullptr, counts, offsets, nullptr, nullptr,
+                                    dev_status, ws, ws_bytes, stream);
+    return README_OK;
+  }
+  README_CHECK_ARG(x && topk_idx && topk_w && dest && ws && (L == 0 || (w_gate && w_up && w_down)),
+                   "null pointer argument");
+  const size_t need = readme_moe_stack_workspace_bytes(T, H, E, d, k, dt);
+  if (ws_bytes < need) {
+    set_error("moe_stack workspace too small: %zu < %zu", ws_bytes, need);
+    return README_ERR_WORKSPACE;
+  }
+  const int64_t rows = T * k;
+  char* w = static_cast<char*>(ws);
+  void* ws_route = w;
+  w += align_up(route_ws_bytes(T, E, k), 256);
+  void* x_sorted = w;
+  w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
+  void* y_sorted = w;
+  w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
+  void* h = w;
+  w += ffn_ws_bytes(rows, d, dt);
+  if (!src) src = reinterpret_cast<int32_t*>(w);
+  // a1-a4 once for the whole stack: the router does not depend on the layer.
+  if (logits)
+    README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                            ws_route, route_ws_bytes(T, E, k), stream));
+  for (int32_t l = 0; l < L; ++l) {
+    README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
+    README_TRY(readme_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status, stream));
+    README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], h, stream));
+    if (k == 1) {  // x <- x + MoE(RMSNorm(x)): the residual add is fused into the down epilogue, in place
+      README_TRY(readme_expert_down(h, dt, rows, H, E, d, 1, offsets, w_down[l], src, x, x, stream));
+    } else {
+      README_TRY(readme_expert_down(h, dt, rows, H, E, d, 1, offsets, w_down[l], nullptr, nullptr, y_sorted, stream));
+      README_TRY(readme_combine(y_sorted, dt, T, H, k, dest, topk_w, x, x, dev_status, stream));
+    }
+  }
+  return README_OK;
+}
+
 readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,
                                    readme_dtype dt, int32_t D, int32_t H, int32_t E, int32_t d,
                                    const int32_t* neuron_idx, void* w_gate, void* w_up, void* w_down,

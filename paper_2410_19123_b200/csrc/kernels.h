@@ -13,6 +13,9 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
 // permute.cu
 readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st);
+readme_status launch_dispatch_rmsnorm(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                      const int32_t* dest, float eps, void* x_sorted, uint32_t* dev_status,
+                                      cudaStream_t st);
 readme_status launch_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
                              uint32_t* dev_status, cudaStream_t st);

@@ -45,25 +45,6 @@ dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, con
   }
 }
 
-// k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
-__global__ void __launch_bounds__(kPermThreads)
-gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
-              uint4* __restrict__ y, uint32_t* __restrict__ dev_status) {
-  const int lane = threadIdx.x % kWarp;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; t < T;
-       t += warps) {
-    const int32_t r = __ldg(dest + t);
-    if (r < 0 || r >= T) {
-      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
-      continue;
-    }
-    copy_row(ys + static_cast<int64_t>(r) * vec, y + t * vec, vec, lane);
-  }
-}
-
-// General combine in fp32, j ascending (Q8), one rounding at the end. 8 elements per lane step.
-
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
   const uint4 v = ld_nc_v4(reinterpret_cast<const uint4*>(p));
   f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
@@ -88,6 +69,76 @@ __device__ __forceinline__ void store8(float* p, const float (&f)[8]) {
                                                     __float_as_uint(f[6]), __float_as_uint(f[7])));
 }
 
+__device__ __forceinline__ void load8_cached(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+  f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z); f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+}
+__device__ __forceinline__ void load8_cached(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// Pre-norm dispatch for the MoE-only stack (reading Q10: x <- x + MoE(RMSNorm(x)), RMSNorm weight 1):
+// x_sorted[dest[t*k+j]] = x[t] / sqrt(mean(x[t]^2) + eps), fp32 statistics, one rounding. One warp per token:
+// pass 1 sums squares (row stays in L1), pass 2 scales and writes the k destination rows.
+template <typename Elt>
+__global__ void __launch_bounds__(kPermThreads)
+dispatch_rmsnorm_kernel(const Elt* __restrict__ x, int H, int64_t T, int k, const int32_t* __restrict__ dest,
+                        float eps, Elt* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  const int groups = H / 8;
+  const int64_t nrows = T * k;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; t < T;
+       t += warps) {
+    const Elt* row = x + t * H;
+    float ss = 0.f;
+    for (int g = lane; g < groups; g += kWarp) {
+      float v[8];
+      load8_cached(row + g * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float r = rsqrtf(ss / static_cast<float>(H) + eps);
+    for (int g = lane; g < groups; g += kWarp) {
+      float v[8];
+      load8_cached(row + g * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= r;
+      for (int j = 0; j < k; ++j) {
+        const int32_t dr = __ldg(dest + t * k + j);
+        if (dr < 0 || dr >= nrows) {
+          if (dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+          continue;
+        }
+        store8(xs + static_cast<int64_t>(dr) * H + g * 8, v);
+      }
+    }
+  }
+}
+
+// k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
+__global__ void __launch_bounds__(kPermThreads)
+gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
+              uint4* __restrict__ y, uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; t < T;
+       t += warps) {
+    const int32_t r = __ldg(dest + t);
+    if (r < 0 || r >= T) {
+      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+      continue;
+    }
+    copy_row(ys + static_cast<int64_t>(r) * vec, y + t * vec, vec, lane);
+  }
+}
+
+
+// General combine in fp32, j ascending (Q8), one rounding at the end. 8 elements per lane step.
 template <typename Elt>
 __global__ void __launch_bounds__(kPermThreads)
 combine_kernel(const Elt* __restrict__ ys, int H, int64_t T, int k, const int32_t* __restrict__ dest,
@@ -168,6 +219,21 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
   dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
       static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
       static_cast<uint4*>(x_sorted), dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_dispatch_rmsnorm(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                      const int32_t* dest, float eps, void* x_sorted, uint32_t* dev_status,
+                                      cudaStream_t st) {
+  if (T == 0) return README_OK;
+  const int grid = grid_for_rows(T);
+  if (dt == README_BF16)
+    dispatch_rmsnorm_kernel<__nv_bfloat16><<<grid, kPermThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), H, T, k, dest, eps, static_cast<__nv_bfloat16*>(x_sorted), dev_status);
+  else
+    dispatch_rmsnorm_kernel<float><<<grid, kPermThreads, 0, st>>>(static_cast<const float*>(x), H, T, k, dest, eps,
+                                                                 static_cast<float*>(x_sorted), dev_status);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

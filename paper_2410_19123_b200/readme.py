@@ -24,7 +24,8 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 # Every symbol include/readme.h declares (tests check the library exports exactly these).
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
-           "readme_build_experts", "readme_set_device", "readme_status_string", "readme_last_error",
+           "readme_build_experts", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
+           "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
 
 
@@ -57,6 +58,12 @@ _SIGS = {
                                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "readme_build_experts": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
                                             _vp, _vp]),
+    "readme_dispatch_rmsnorm": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, ctypes.c_float, _vp, _vp,
+                                               _vp]),
+    "readme_moe_stack_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, _i32, ctypes.c_int]),
+    "readme_moe_stack": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _vp, ctypes.c_int, _i32, _i32, _i32, _i32,
+                                        _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                        _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -283,3 +290,49 @@ def build_experts(dense_w_gate: torch.Tensor, dense_w_up: torch.Tensor, dense_w_
         _ptr(dense_w_gate), _ptr(dense_w_up), _ptr(dense_w_down), _dt(dense_w_gate), D, H, E, d, _ptr(neuron_idx),
         _ptr(wg), _ptr(wu), _ptr(wd), _ptr(dev_status), st))
     return wg, wu, wd
+
+
+def dispatch_rmsnorm(x: torch.Tensor, dest: torch.Tensor, k: int, eps: float = 1e-5, out: torch.Tensor | None = None,
+                     dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """Pre-norm dispatch: x_sorted[dest[t*k+j]] = RMSNorm(x[t]) (readme_dispatch_rmsnorm)."""
+    T, H = x.shape
+    out = out if out is not None else torch.empty((T * k, H), dtype=x.dtype, device=x.device)
+    st = _prep(x, dest, out, dev_status)
+    _check("readme_dispatch_rmsnorm", lib().readme_dispatch_rmsnorm(_ptr(x), _dt(x), T, H, k, _ptr(dest),
+                                                                    ctypes.c_float(eps), _ptr(out), _ptr(dev_status),
+                                                                    st))
+    return out
+
+
+def moe_stack_workspace_bytes(T: int, H: int, E: int, d: int, k: int, dtype: torch.dtype) -> int:
+    return int(lib().readme_moe_stack_workspace_bytes(T, H, E, d, k,
+                                                      README_BF16 if dtype == torch.bfloat16 else README_F32))
+
+
+def moe_stack(x: torch.Tensor, layers, k: int = 1, logits: torch.Tensor | None = None, plan: Plan | None = None,
+              eps: float = 1e-5, ws: torch.Tensor | None = None) -> tuple[torch.Tensor, Plan]:
+    """L pre-norm MoE layers routed once (readme_moe_stack). `layers` = [(w_gate, w_up, w_down), ...];
+    x is updated in place and returned."""
+    T, H = x.shape
+    L = len(layers)
+    E, d, _ = layers[0][0].shape if L else (0, 8, 0)
+    if logits is None and plan is None:
+        raise ValueError("moe_stack needs logits or a plan")
+    if plan is None:
+        plan = new_plan(T, logits.shape[1], k, x.device)
+        E = logits.shape[1]
+    k = plan.k
+    need = moe_stack_workspace_bytes(T, H, E, d, k, x.dtype)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    arr = ctypes.c_void_p * max(L, 1)
+    wg = arr(*[w[0].data_ptr() for w in layers])
+    wu = arr(*[w[1].data_ptr() for w in layers])
+    wd = arr(*[w[2].data_ptr() for w in layers])
+    st = _prep(x, logits, ws, plan.dest, *[t for w in layers for t in w])
+    _check("readme_moe_stack", lib().readme_moe_stack(
+        _ptr(x), _dt(x), T, H, _ptr(logits), _dt(logits) if logits is not None else README_F32, E, k, d, L,
+        ctypes.cast(wg, ctypes.c_void_p), ctypes.cast(wu, ctypes.c_void_p), ctypes.cast(wd, ctypes.c_void_p),
+        ctypes.c_float(eps), _ptr(plan.topk_idx), _ptr(plan.topk_w), _ptr(plan.counts), _ptr(plan.offsets),
+        _ptr(plan.dest), _ptr(plan.src), _ptr(plan.dev_status), _ptr(ws), ws.numel(), st))
+    return x, plan

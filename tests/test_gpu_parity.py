@@ -413,3 +413,31 @@ def test_config2_full_size_sampled(rd):
     sample = np.concatenate([g.choice(np.nonzero(idx == e)[0], size=8, replace=False) for e in range(E)])
     yb = oracle.bruteforce(x[sample], lg[sample], 1, *dense, S)
     assert rel_err(_np(y)[sample], yb) <= BF16_TOL
+
+
+# ---- config 4: pre-norm dispatch and the route-once stack ----------------------------------------------
+
+@pytest.mark.parametrize("dt,k", [("bf16", 1), ("bf16", 2), ("f32", 1)])
+def test_dispatch_rmsnorm(rd, dt, k):
+    T, H = 700, 4096 if dt == "bf16" else 256
+    x = synth.to_torch(synth.tokens(T, H, seed=151) * 3.0, dt)
+    plan = oracle.route(synth.router_logits(T, 8, seed=152), k)
+    xs = rd.dispatch_rmsnorm(x.to(DEV), torch.from_numpy(plan["dest"]).to(DEV), k, eps=1e-5)
+    ref = oracle.dispatch(oracle.rmsnorm(x, 1e-5), plan["dest"], k)
+    assert rel_err(_np(xs), ref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+@pytest.mark.parametrize("dt,k,L", [("bf16", 1, 4), ("bf16", 2, 3), ("f32", 1, 3)])
+def test_moe_stack_end_to_end(rd, dt, k, L):
+    T, H, d, E = 600, 256, 256, 8
+    x = synth.to_torch(synth.tokens(T, H, seed=161), dt)
+    ids = synth.assignments_markov(2, T // 2, E, 0.672, seed=162)
+    lg = synth.logits_for_assignments(ids, E, seed=163) if k == 1 else synth.router_logits(T, E, seed=163)
+    layers = [tuple(synth.to_torch(w, dt) for w in synth.expert_weights(E, d, H, seed=164, layer=l))
+              for l in range(L)]
+    xg = x.to(DEV).clone()
+    yg, plan = rd.moe_stack(xg, [tuple(w.to(DEV) for w in ly) for ly in layers], k=k,
+                            logits=torch.from_numpy(lg).to(DEV))
+    yref, pref = oracle.moe_stack(x, lg, k, layers)
+    _check_plan(plan, pref, k)
+    assert rel_err(_np(yg), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)

@@ -350,3 +350,28 @@ def test_hidden_closed_form():
     h = oracle.expert_hidden(np.array([c["x"]]), np.array([0, 1], np.int32), np.array([c["w_gate"]], np.float64),
                              np.array([c["w_up"]], np.float64))
     np.testing.assert_allclose(h[0, 0], c["y"][0], atol=1e-6, rtol=0)
+
+
+# ---- RMSNorm and the route-once stack (config 4, reading Q10) ---------------------------------------
+
+def test_rmsnorm_closed_form():
+    # x = (3, 4): mean square 12.5, rms = 3.5355339 -> (0.8485281, 1.1313708); eps = 0
+    y = oracle.rmsnorm(np.array([[3.0, 4.0]]), eps=0.0)
+    np.testing.assert_allclose(y[0], [0.8485281374238571, 1.131370849898476], rtol=1e-15)
+    x = synth.tokens(5, 16, seed=131).astype(np.float64)
+    np.testing.assert_allclose(oracle.rmsnorm(7.0 * x, eps=0.0), oracle.rmsnorm(x, eps=0.0), rtol=1e-14)
+    np.testing.assert_allclose(np.mean(oracle.rmsnorm(x, eps=0.0) ** 2, axis=1), 1.0, rtol=1e-14)
+
+
+def test_stack_zero_down_is_identity_and_routes_once():
+    T, H, E, d, L = 20, 16, 4, 8, 3
+    x = synth.tokens(T, H, seed=141)
+    lg = synth.router_logits(T, E, seed=142)
+    layers = []
+    for l in range(L):
+        eg, eu, ed = synth.expert_weights(E, d, H, seed=143, layer=l)
+        layers.append((eg, eu, np.zeros_like(ed)))
+    y, plan = oracle.moe_stack(x, lg, 1, layers)
+    assert np.array_equal(y, x.astype(np.float64))  # W_down = 0 -> every layer adds exactly 0
+    ref = oracle.route(lg, 1)
+    assert np.array_equal(plan["dest"], ref["dest"])
