@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tokens", type=int, default=None, help="override T per rank")
+    ap.add_argument("--eager", action="store_true", help="time eager calls instead of CUDA-graph replays")
     return ap.parse_args()
 
 
@@ -233,6 +234,14 @@ def run_decode(args):
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
+        if not args.eager:  # one CUDA graph per decode step shape (as a serving loop would)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            fn = g.replay
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
         ms = []
         for _ in range(args.steps):
             flush.zero_()
@@ -393,11 +402,28 @@ def main():
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
+    eager_fn = step_fn
+    if world == 1 and not args.eager:
+        # The C ABI is stream-ordered and allocation-free, so the whole step captures into one CUDA graph
+        # (how a fixed-shape serving step runs); replays remove the per-call host launch cost.
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step_fn()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_fn()
+        step_fn = graph.replay
+        for _ in range(args.warmup):
+            step_fn()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         step_ms = timed(step_fn, args.steps)
+        eager_ms = timed(eager_fn, args.steps) if world == 1 else None
         if world == 1:
             # breakdown (same protocol): route alone; plan-in layer = the two fused grouped-GEMM kernels
             ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
@@ -428,6 +454,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write)"}}
     if world == 1:
         med = lambda a: float(np.median(a))
+        line["step_mode"] = "cuda_graph_replay" if not args.eager else "eager"
+        line["eager_ms_per_step"] = float(np.mean(eager_ms))
         line["stage_ms_median"] = {"step": med(step_ms), "route": med(route_ms), "dispatch": med(disp_ms),
                                    "gate_up": med(gu_ms), "down_combine": med(dn_ms)}
         f_gu, f_dn = 4.0 * T * k * H * d, 2.0 * T * k * H * d

@@ -104,22 +104,33 @@ readme_status readme_set_device(int device) {
 
 size_t readme_route_workspace_bytes(int64_t T, int32_t E, int32_t k) { return route_ws_bytes(T, E, k); }
 
+namespace readme {
+namespace {
+readme_status check_route_call(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
+                               int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
+                               void* ws, size_t ws_bytes) {
+  README_TRY(check_route_args(T, E, k));
+  README_CHECK_ARG(counts && offsets, "counts and offsets are required");
+  if (T > 0) {
+    README_CHECK_ARG(logits && topk_idx && topk_w && dest, "logits, topk_idx, topk_w, dest are required");
+    README_CHECK_ARG(logits_dt == README_F32 || logits_dt == README_BF16, "logits_dt must be F32 or BF16");
+    README_CHECK_ARG(ws != nullptr, "workspace is required");
+    if (ws_bytes < route_ws_bytes(T, E, k)) {
+      set_error("route workspace too small: %zu < %zu", ws_bytes, route_ws_bytes(T, E, k));
+      return README_ERR_WORKSPACE;
+    }
+  }
+  return README_OK;
+}
+}  // namespace
+}  // namespace readme
+
 readme_status readme_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
                            int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
                            readme_stream_t stream) {
   try {
-    README_TRY(check_route_args(T, E, k));
-    README_CHECK_ARG(counts && offsets, "counts and offsets are required");
-    if (T > 0) {
-      README_CHECK_ARG(logits && topk_idx && topk_w && dest, "logits, topk_idx, topk_w, dest are required");
-      README_CHECK_ARG(logits_dt == README_F32 || logits_dt == README_BF16, "logits_dt must be F32 or BF16");
-      README_CHECK_ARG(ws != nullptr, "workspace is required");
-      if (ws_bytes < route_ws_bytes(T, E, k)) {
-        set_error("route workspace too small: %zu < %zu", ws_bytes, route_ws_bytes(T, E, k));
-        return README_ERR_WORKSPACE;
-      }
-    }
+    README_TRY(check_route_call(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, ws, ws_bytes));
     return launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status, ws,
                         reinterpret_cast<cudaStream_t>(stream));
   } catch (const std::exception& e) {
@@ -270,10 +281,18 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   int32_t* src_ws = reinterpret_cast<int32_t*>(w);
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
-    README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
-                            ws_route, route_ws_bytes(T, E, k), stream));
+    // a1-a4 with the finalize (offsets[e] + rank, src) fused into the a5 dispatch pass
+    README_TRY(check_route_call(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, ws_route,
+                                route_ws_bytes(T, E, k)));
+    README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                            ws_route, st, /*finalize=*/false));
+    README_TRY(launch_finalize_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, E, topk_idx, offsets, dest,
+                                        src, x_sorted, st));
+  } else {
+    README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   }
-  README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   const char* kv = getenv("README_FFN_KERNEL");
   const bool fused = k == 1 && src != nullptr && !(kv && (strcmp(kv, "1cta") == 0 || strcmp(kv, "unfused") == 0));
   if (fused) {

@@ -8,11 +8,14 @@ namespace readme {
 size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
-                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st);
+                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize = true);
 
 // permute.cu
 readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st);
+readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,
+                                       const int32_t* topk_idx, const int32_t* offsets, int32_t* dest, int32_t* src,
+                                       void* x_sorted, cudaStream_t st);
 readme_status launch_dispatch_rmsnorm(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
                                       const int32_t* dest, float eps, void* x_sorted, uint32_t* dev_status,
                                       cudaStream_t st);

@@ -120,6 +120,30 @@ dispatch_rmsnorm_kernel(const Elt* __restrict__ x, int H, int64_t T, int k, cons
   }
 }
 
+// readme_moe_layer's a4-finalize + a5 in one pass: dest holds each slot's rank inside its expert (left by
+// route_tile_kernel); row = offsets[e] + rank, then dest/src are finalised and the token row copied there.
+__global__ void __launch_bounds__(kPermThreads)
+finalize_dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, int E,
+                         const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ offsets,
+                         int32_t* __restrict__ dest, int32_t* __restrict__ src, uint4* __restrict__ xs) {
+  __shared__ int s_off[README_MAX_EXPERTS + 1];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
+  __syncthreads();
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; s < nslots;
+       s += warps) {
+    int r = 0;
+    if (lane == 0) {
+      r = s_off[topk_idx[s]] + dest[s];
+      dest[s] = r;
+      if (src) src[r] = static_cast<int32_t>(s);
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    copy_row(x + (s / k) * vec, xs + static_cast<int64_t>(r) * vec, vec, lane);
+  }
+}
+
 // k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
 __global__ void __launch_bounds__(kPermThreads)
 gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
@@ -219,6 +243,18 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
   dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
       static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
       static_cast<uint4*>(x_sorted), dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,
+                                       const int32_t* topk_idx, const int32_t* offsets, int32_t* dest, int32_t* src,
+                                       void* x_sorted, cudaStream_t st) {
+  const int64_t nslots = T * k;
+  if (nslots == 0) return README_OK;
+  finalize_dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
+      static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, E, topk_idx, offsets, dest, src,
+      static_cast<uint4*>(x_sorted));
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

@@ -5,17 +5,19 @@
 // to the lower id" (Q2), softmax over the selected logits (Q1); grouping = Alg. 1's ReqQueueByExpert
 // with FIFO order inside an expert (Q7).
 //
-// Design (B200): one CTA per tile of <= 1024 slots (slot s = t*k + j), tiles claimed in launch order
-// through an atomic ticket so the lookback chain always points at running or finished CTAs.
+// Design (B200): one CTA per tile of <= 1024 slots (slot s = t*k + j); tile = blockIdx.x (blocks are
+// dispatched in index order, so a lookback only ever waits on CTAs that are running or finished).
 //   phase A  logits tile -> shared memory (all loads in flight at once), then lane-groups of
 //            LPT = min(32, pow2ceil(E)) lanes per token run a warp-shuffle arg-max k times.
 //   phase B  per warp, 32 slots at a time: __match_any_sync groups equal experts, popc of the
 //            lower-lane mask gives the stable in-warp rank; per-warp per-expert running counts in smem.
-//   phase C  per expert (one thread each): exclusive scan over warps, then decoupled lookback over tiles
+//   phase C  per expert: exclusive scan over warps and publication of the tile aggregate, then a
+//            decoupled lookback by one warp per expert that reads 32 predecessor tiles at once
 //            (64-bit status words: flag << 32 | count; 1 = tile aggregate, 2 = inclusive prefix).
 //            The last tile knows the global counts and writes counts[] and offsets[].
 //   phase D  dest[s] = (rank of s among its expert's slots); the finalize kernel adds offsets[e] and
-//            writes src. (offsets need every tile's counts, so a second launch is the cheap barrier.)
+//            writes src (offsets need every tile's counts, so a second launch is the cheap barrier).
+//            readme_moe_layer fuses that finalize into the dispatch kernel (permute.cu).
 #include <math.h>
 
 #include "kernels.h"
@@ -68,22 +70,19 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_tile_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k, int tile_tokens, int ntiles,
                   int lpt, int items, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                   int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ rank_out,
-                  uint32_t* __restrict__ dev_status, uint32_t* __restrict__ ticket, uint64_t* __restrict__ status) {
+                  uint32_t* __restrict__ dev_status, uint64_t* __restrict__ status) {
   __shared__ float s_logit[kMaxLogitFloats];
   __shared__ uint8_t s_exp[kMaxTileSlots];
   __shared__ int s_wcount[kRouteWarps][README_MAX_EXPERTS];
   __shared__ int s_prefix[README_MAX_EXPERTS];
-  __shared__ int s_tile;
+  __shared__ int s_run[README_MAX_EXPERTS];
   __shared__ int s_bad;
 
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
-  if (tid == 0) {
-    s_tile = static_cast<int>(atomicAdd(ticket, 1u));
-    s_bad = 0;
-  }
+  if (tid == 0) s_bad = 0;
   for (int i = tid; i < kRouteWarps * README_MAX_EXPERTS; i += kRouteThreads) (&s_wcount[0][0])[i] = 0;
   __syncthreads();
-  const int tile = s_tile;
+  const int tile = blockIdx.x;
   const int64_t t0 = static_cast<int64_t>(tile) * tile_tokens;
   const int64_t rem = T - t0;
   const int nt = static_cast<int>(rem < tile_tokens ? rem : tile_tokens);
@@ -178,7 +177,7 @@ route_tile_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k, in
   }
   __syncthreads();
 
-  // ---- phase C: per-expert warp scan + decoupled lookback across tiles ----
+  // ---- phase C: per-expert warp scan, publish the tile aggregate, decoupled lookback ----
   for (int e = tid; e < E; e += kRouteThreads) {
     int run = 0;
 #pragma unroll
@@ -187,27 +186,39 @@ route_tile_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k, in
       s_wcount[w][e] = run;
       run += c;
     }
-    uint64_t* my = status + static_cast<int64_t>(tile) * E + e;
+    s_run[e] = run;
+    st_relaxed_gpu_u64(status + static_cast<int64_t>(tile) * E + e,
+                       ((tile == 0 ? 2ull : 1ull) << 32) | static_cast<uint32_t>(run));
+  }
+  __syncthreads();
+  for (int e = warp; e < E; e += kRouteWarps) {
     int excl = 0;
-    if (tile == 0) {
-      st_relaxed_gpu_u64(my, (2ull << 32) | static_cast<uint32_t>(run));
-    } else {
-      st_relaxed_gpu_u64(my, (1ull << 32) | static_cast<uint32_t>(run));
-      for (int i = tile - 1; i >= 0;) {
-        const uint64_t w = ld_relaxed_gpu_u64(status + static_cast<int64_t>(i) * E + e);
-        const uint32_t flag = static_cast<uint32_t>(w >> 32);
-        if (flag == 0) {
-          __nanosleep(20);
-          continue;
-        }
-        excl += static_cast<int>(static_cast<uint32_t>(w));
-        if (flag == 2) break;
-        --i;
+    int base = tile - 1;  // the window covers tiles base, base-1, ..., base-31 (lane j -> tile base-j)
+    while (base >= 0) {
+      const int i = base - lane;
+      uint64_t w = (2ull << 32);  // lanes past tile 0 read as an empty inclusive prefix
+      if (i >= 0) w = ld_relaxed_gpu_u64(status + static_cast<int64_t>(i) * E + e);
+      const uint32_t flag = static_cast<uint32_t>(w >> 32);
+      if (__any_sync(0xffffffffu, flag == 0)) {  // a predecessor has not published yet
+        __nanosleep(32);
+        continue;
       }
-      st_relaxed_gpu_u64(my, (2ull << 32) | static_cast<uint32_t>(excl + run));
+      const uint32_t pref = __ballot_sync(0xffffffffu, flag == 2);
+      const int stop = pref ? __ffs(pref) - 1 : kWarp - 1;  // nearest predecessor with an inclusive prefix
+      int v = lane <= stop ? static_cast<int>(static_cast<uint32_t>(w)) : 0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      excl += v;
+      if (pref) break;
+      base -= kWarp;
     }
-    s_prefix[e] = excl;
-    if (tile == ntiles - 1) counts[e] = excl + run;
+    if (lane == 0) {
+      const int run = s_run[e];
+      if (tile > 0)
+        st_relaxed_gpu_u64(status + static_cast<int64_t>(tile) * E + e, (2ull << 32) | static_cast<uint32_t>(excl + run));
+      s_prefix[e] = excl;
+      if (tile == ntiles - 1) counts[e] = excl + run;
+    }
   }
   __syncthreads();
   if (tile == ntiles - 1 && tid == 0) {
@@ -249,34 +260,34 @@ __global__ void route_finalize_kernel(int64_t nslots, int E, const int32_t* __re
 size_t route_ws_bytes(int64_t T, int32_t E, int32_t k) {
   if (T <= 0 || E < 1 || k < 1) return 256;
   RouteGeom g = route_geom(T, E, k);
-  return 256 + align_up(static_cast<size_t>(g.ntiles) * E * sizeof(uint64_t), 256);
+  return align_up(static_cast<size_t>(g.ntiles) * E * sizeof(uint64_t), 256);
 }
 
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
-                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st) {
+                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize) {
   if (T == 0) {
     README_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st));
     README_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), st));
     return README_OK;
   }
   RouteGeom g = route_geom(T, E, k);
-  README_CUDA(cudaMemsetAsync(ws, 0, route_ws_bytes(T, E, k), st));
-  uint32_t* ticket = static_cast<uint32_t*>(ws);
-  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 256);
+  uint64_t* status = static_cast<uint64_t*>(ws);
+  README_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(g.ntiles) * E * sizeof(uint64_t), st));
   int lpt = 1;
   while (lpt < E && lpt < kWarp) lpt <<= 1;
   const int items = (E + lpt - 1) / lpt;
   if (logits_dt == README_F32) {
     route_tile_kernel<float><<<g.ntiles, kRouteThreads, 0, st>>>(
         static_cast<const float*>(logits), T, E, k, g.tile_tokens, g.ntiles, lpt, items, topk_idx, topk_w,
-        counts, offsets, dest, dev_status, ticket, status);
+        counts, offsets, dest, dev_status, status);
   } else {
     route_tile_kernel<__nv_bfloat16><<<g.ntiles, kRouteThreads, 0, st>>>(
         static_cast<const __nv_bfloat16*>(logits), T, E, k, g.tile_tokens, g.ntiles, lpt, items, topk_idx,
-        topk_w, counts, offsets, dest, dev_status, ticket, status);
+        topk_w, counts, offsets, dest, dev_status, status);
   }
   README_CUDA(cudaGetLastError());
+  if (!finalize) return README_OK;  // the caller fuses the finalize into its dispatch
   const int64_t nslots = T * k;
   const int64_t want = (nslots + 255) / 256, cap = 4LL * num_sms();
   const int blocks = static_cast<int>(want < cap ? want : cap);
