@@ -421,19 +421,36 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if world == 1:
+        ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
+        xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
+        hbuf = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
+        y2 = torch.empty_like(x_dev)
+        stage_fns = [lambda: rd.route(lg_dev, k, plan=plan, ws=ws_r),
+                     lambda: rd.dispatch(x_dev, plan.dest, k, out=xs),
+                     lambda: rd.expert_gate_up(xs, plan.offsets, eg, eu, out=hbuf),
+                     lambda: rd.expert_down(hbuf, plan.offsets, ed, src=plan.src, out=y2)]
     with Clocks(local) as clk:
-        step_ms = timed(step_fn, args.steps)
-        eager_ms = timed(eager_fn, args.steps) if world == 1 else None
-        if world == 1:
-            # breakdown (same protocol): route alone; plan-in layer = the two fused grouped-GEMM kernels
-            ws_r = torch.empty(rd.route_workspace_bytes(T, E, k), dtype=torch.uint8, device=dev)
-            xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
-            hbuf = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
-            y2 = torch.empty_like(x_dev)
-            route_ms = timed(lambda: rd.route(lg_dev, k, plan=plan, ws=ws_r), args.steps)
-            disp_ms = timed(lambda: rd.dispatch(x_dev, plan.dest, k, out=xs), args.steps)
-            gu_ms = timed(lambda: rd.expert_gate_up(xs, plan.offsets, eg, eu, out=hbuf), args.steps)
-            dn_ms = timed(lambda: rd.expert_down(hbuf, plan.offsets, ed, src=plan.src, out=y2), args.steps)
+        if world > 1:
+            step_ms = timed(step_fn, args.steps)
+        else:
+            # K timed steps (graph replays of readme_moe_layer); after each, in the same thermal/power
+            # window, one eager pass through the per-row C entries with events between the launches gives the
+            # live per-kernel breakdown (route | dispatch | a6 gate/up | a7 down + fused combine).
+            step_ms, eager_ms, stages = [], [], []
+            for _ in range(args.steps):
+                step_ms += timed(step_fn, 1)
+                eager_ms += timed(eager_fn, 1)
+                flush.zero_()
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(stage_fns) + 1)]
+                evs[0].record()
+                for j, f in enumerate(stage_fns):
+                    f()
+                    evs[j + 1].record()
+                torch.cuda.synchronize()
+                stages.append([evs[j].elapsed_time(evs[j + 1]) for j in range(len(stage_fns))])
+            st = np.array(stages)
+            route_ms, disp_ms, gu_ms, dn_ms = (st[:, j] for j in range(4))
     if world > 1:
         dist.barrier()
     tot_ms = sum(step_ms)
