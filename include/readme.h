@@ -174,6 +174,21 @@ readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w
                                    const int32_t* neuron_idx, void* w_gate, void* w_up, void* w_down,
                                    uint32_t* dev_status, readme_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------------- */
+/* Host runtime: expert-aware batching (Alg. 1). Pre-gated tokens wait in one FIFO per
+ * expert ("ReqQueueByExpert"); readme_scheduler_next_batch forms the next batch of at most
+ * max_tokens by repeatedly taking the largest queue (ties -> lower id) whole while it fits, then a prefix of
+ * the next largest to fill the batch, and stops (readings Q12: `k` at PAPER.md:250/:256-257 read as `E`;
+ * stop when the largest queue is empty). token_ids/experts are HOST arrays of >= max_tokens entries; the
+ * batch comes out grouped by expert in the order the queues were taken; returns its size (-1 on a bad
+ * argument). Thread-safe (one mutex per scheduler). No GPU involved. */
+typedef struct readme_scheduler readme_scheduler;
+readme_scheduler* readme_scheduler_create(int32_t E); /* NULL if E is outside [1, 256] or out of memory */
+void readme_scheduler_destroy(readme_scheduler* s);
+readme_status readme_scheduler_push(readme_scheduler* s, const int64_t* token_ids, const int32_t* experts, int64_t n);
+int64_t readme_scheduler_queued(readme_scheduler* s, int32_t e); /* e = -1: all queues */
+int64_t readme_scheduler_next_batch(readme_scheduler* s, int64_t max_tokens, int64_t* token_ids, int32_t* experts);
+
 /* Helpers. */
 /* The library links its own (static) CUDA runtime: bind the calling host thread to `device` before
  * calling the entry points above from that thread (the Python binding does this per call). */

@@ -25,7 +25,8 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
            "readme_build_experts", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
-           "readme_set_device", "readme_status_string", "readme_last_error",
+           "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
+           "readme_scheduler_next_batch", "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
 
 
@@ -64,6 +65,11 @@ _SIGS = {
     "readme_moe_stack": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _vp, ctypes.c_int, _i32, _i32, _i32, _i32,
                                         _vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                                         _vp]),
+    "readme_scheduler_create": (_vp, [_i32]),
+    "readme_scheduler_destroy": (None, [_vp]),
+    "readme_scheduler_push": (ctypes.c_int, [_vp, _vp, _vp, _i64]),
+    "readme_scheduler_queued": (_i64, [_vp, _i32]),
+    "readme_scheduler_next_batch": (_i64, [_vp, _i64, _vp, _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -336,3 +342,45 @@ def moe_stack(x: torch.Tensor, layers, k: int = 1, logits: torch.Tensor | None =
         ctypes.c_float(eps), _ptr(plan.topk_idx), _ptr(plan.topk_w), _ptr(plan.counts), _ptr(plan.offsets),
         _ptr(plan.dest), _ptr(plan.src), _ptr(plan.dev_status), _ptr(ws), ws.numel(), st))
     return x, plan
+
+
+class ExpertScheduler:
+    """Expert-aware batching (Alg. 1) over per-expert FIFO queues, in the native host
+    runtime (readme_scheduler_*)."""
+
+    def __init__(self, E: int):
+        import numpy as np
+        self._np = np
+        self.E = E
+        self._h = lib().readme_scheduler_create(E)
+        if not self._h:
+            raise ValueError(f"readme_scheduler_create({E}) failed")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().readme_scheduler_destroy(h)
+            self._h = None
+
+    def push(self, token_ids, experts):
+        np = self._np
+        t = np.ascontiguousarray(token_ids, dtype=np.int64)
+        e = np.ascontiguousarray(experts, dtype=np.int32)
+        if t.shape != e.shape:
+            raise ValueError("token_ids and experts must have the same length")
+        _check("readme_scheduler_push", lib().readme_scheduler_push(
+            self._h, t.ctypes.data_as(ctypes.c_void_p), e.ctypes.data_as(ctypes.c_void_p), t.size))
+
+    def queued(self, e: int = -1) -> int:
+        return int(lib().readme_scheduler_queued(self._h, e))
+
+    def next_batch(self, max_tokens: int):
+        """Returns (token_ids int64 [n], experts int32 [n]) of the next batch (grouped by expert)."""
+        np = self._np
+        t = np.empty(max(max_tokens, 1), np.int64)
+        e = np.empty(max(max_tokens, 1), np.int32)
+        n = lib().readme_scheduler_next_batch(self._h, max_tokens, t.ctypes.data_as(ctypes.c_void_p),
+                                              e.ctypes.data_as(ctypes.c_void_p))
+        if n < 0:
+            raise ValueError("readme_scheduler_next_batch: bad argument")
+        return t[:n].copy(), e[:n].copy()

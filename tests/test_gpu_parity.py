@@ -441,3 +441,15 @@ def test_moe_stack_end_to_end(rd, dt, k, L):
     yref, pref = oracle.moe_stack(x, lg, k, layers)
     _check_plan(plan, pref, k)
     assert rel_err(_np(yg), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+# ---- NEXT-2: expert-aware batching on the GPU serving loop ---------------------------------------------
+
+def test_serving_expert_aware_touches_fewer_experts(rd):
+    from paper_2410_19123_b200 import serving
+    E, d, H = 8, 256, 512
+    W = [synth.to_torch(w, "bf16").to(DEV) for w in synth.expert_weights(E, d, H, seed=171)]
+    a = serving.simulate("expert_aware", *W, n_requests=256, max_tokens=64, steps=20, device=DEV)
+    b = serving.simulate("fifo", *W, n_requests=256, max_tokens=64, steps=20, device=DEV)
+    assert a["tokens"] == b["tokens"] == 20 * 64
+    assert a["mean_unique_experts"] < b["mean_unique_experts"]
