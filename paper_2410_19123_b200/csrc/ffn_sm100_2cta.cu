@@ -15,6 +15,8 @@
 // rows), so padding waste stays at the 128-row granularity of v1.
 // GEMM1 B operand per CTA r: 64 rows of W_gate then the same 64 rows of W_up (neurons n0+64r ..), so in
 // accumulator column space gate column c pairs with up column c+64 inside every 128-column window.
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "kernels.h"
@@ -41,6 +43,7 @@ struct __align__(8) Smem {
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
+  alignas(16) uint8_t stg[4][32 * 128];  // epilogue staging, one 4 KB tile per epilogue warp
   int seg_off[kMaxSeg + 1];
   int tile_start[kMaxSeg + 1];
 };
@@ -51,13 +54,14 @@ struct Tile {
   bool m256;
 };
 
-__device__ __forceinline__ Tile decode_tile(const Smem& s, int t, int nseg, int bn_out, int& gcur) {
+__device__ __forceinline__ Tile decode_tile(const Smem& s, int t, int nseg, int bn_out, int& gcur, int NT,
+                                           bool n_fastest) {
   while (gcur + 1 < nseg && s.tile_start[gcur + 1] <= t) ++gcur;
   const int g = gcur;
   const int cnt = s.seg_off[g + 1] - s.seg_off[g];
   const int mt_g = (cnt + 255) / 256;
   const int local = t - s.tile_start[g];
-  const int nt = local / mt_g, mt = local % mt_g;
+  const int nt = n_fastest ? local % NT : local / mt_g, mt = n_fastest ? local / NT : local % mt_g;
   Tile tl;
   tl.g = g;
   tl.m0 = s.seg_off[g] + mt * 256;
@@ -65,20 +69,6 @@ __device__ __forceinline__ Tile decode_tile(const Smem& s, int t, int nseg, int 
   tl.m256 = tl.rows > 128;
   tl.n0 = nt * bn_out;
   return tl;
-}
-
-__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int ncols_left) {
-#pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    if (j < ncols_left) {
-      uint4 w;
-      w.x = pack_bf16x2(v[j + 0], v[j + 1]);
-      w.y = pack_bf16x2(v[j + 2], v[j + 3]);
-      w.z = pack_bf16x2(v[j + 4], v[j + 5]);
-      w.w = pack_bf16x2(v[j + 6], v[j + 7]);
-      st_v4(reinterpret_cast<uint4*>(dst + j), w);
-    }
-  }
 }
 
 // Fusion of the combine into GEMM2 (readme_moe_layer's path, k == 1): kFuse == 1 makes the epilogue
@@ -90,7 +80,46 @@ struct Fuse {
   const int32_t* src;                 // [rows] expert-contiguous row -> token (= dest^-1, k == 1)
   int rows;                           // T
   const __nv_bfloat16* residual;      // [T, N] or null (GEMM2 scatter only)
+  int lab;                            // experiment knobs (README_LAB): bit0 skip output stores, bit1 N-fastest order
 };
+
+// Epilogue staging (per epilogue warp: 32 rows x 128 B; 16-byte chunks XOR-swizzled by row & 7 so the
+// row-per-thread writes and the row-cooperative reads are both bank-conflict-light).
+__device__ __forceinline__ void stage_row_bf16x32(uint8_t* stg, int row, int chunk0, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 w;
+    w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+    w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+    w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+    w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+    const int c = chunk0 + j;
+    *reinterpret_cast<uint4*>(stg + row * 128 + ((c ^ (row & 7)) << 4)) = w;
+  }
+}
+// Write the warp's 32 staged rows: lane l moves 16 B chunk (l & 7) of row 4i + (l >> 3); row r goes to the
+// global address held by lane r (0 = skip the row); chunks at or past `bytes_left` are not written.
+__device__ __forceinline__ void stage_flush(const uint8_t* stg, int lane, uint64_t my_row, int bytes_left,
+                                            bool evict_first) {
+  __syncwarp();
+  uint64_t pol = 0;
+  if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = i * 4 + (lane >> 3), c = lane & 7;
+    const uint64_t dst = __shfl_sync(0xffffffffu, my_row, r);
+    if (dst && c * 16 < bytes_left) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
+      if (evict_first)
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(reinterpret_cast<uint4*>(dst) + c),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                     : "memory");
+      else
+        st_v4(reinterpret_cast<uint4*>(dst) + c, v);
+    }
+  }
+  __syncwarp();
+}
 
 __device__ __forceinline__ void add_bf16x32(const __nv_bfloat16* src, float (&v)[32], int ncols_left) {
 #pragma unroll
@@ -157,7 +186,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t phase = 0;
     int gcur = 0;
     for (int t = pair; t < ntiles; t += npairs) {
-      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
       const int e = tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
@@ -193,7 +222,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       uint32_t phase = 0;
       int gcur = 0, i = 0;
       for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -222,7 +251,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int q = warp & 3;
     int gcur = 0, i = 0;
     for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur);
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -240,7 +269,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         n_windows = 1;
         out_off = (q >> 1) * (kBnOut / 2);
       }
-      const bool valid = row_in_tile < tl.rows;
+      const bool valid = row_in_tile < tl.rows && !(fz.lab & 1);
       int64_t orow_idx = tl.m0 + row_in_tile;
       bool valid_row = valid;
       if constexpr (kMode == 1 && kFuse == 1) {  // k == 1: expert row r holds token src[r]
@@ -249,6 +278,9 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       __nv_bfloat16* orow = out + orow_idx * N;
       const __nv_bfloat16* rrow = (kMode == 1 && kFuse == 1 && fz.residual) ? fz.residual + orow_idx * N : nullptr;
+      uint8_t* stg = s.stg[q];
+      // Each 64-column output chunk: every thread puts its row's 128 B into the warp's staging tile, then
+      // the warp writes 4 full rows (4 x 128 B) per store instruction (coalesced, whole L2 lines).
       for (int w = 0; w < n_windows; ++w) {
         const uint32_t wbase = tacc + static_cast<uint32_t>(col_base + w * 128);
         if (kMode == 0) {
@@ -260,33 +292,41 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc::tmem_ld32(wbase + c, gr);
             tc::tmem_ld32(wbase + 64 + c, ur);
             tc::tmem_wait_ld();
-            if (valid) {
-              float v[32];
+            float v[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
-              store_bf16x32(orow + hcol0 + c, v, N - (hcol0 + c));
-            }
+            for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+            stage_row_bf16x32(stg, lane, c / 8, v);
           }
+          stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, (N - hcol0) * 2,
+                      (fz.lab & 8) != 0);
         } else {
-          const int col0 = tl.n0 + out_off + w * 128;
 #pragma unroll 1
-          for (int c = 0; c < 128; c += 32) {
-            uint32_t vr[32];
-            tc::tmem_ld32(wbase + c, vr);
-            tc::tmem_wait_ld();
-            if (valid_row) {
+          for (int c0 = 0; c0 < 128; c0 += 64) {
+            const int col0 = tl.n0 + out_off + w * 128 + c0;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 32) {
+              uint32_t vr[32];
+              tc::tmem_ld32(wbase + c0 + c, vr);
+              tc::tmem_wait_ld();
               float v[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-              if (rrow) add_bf16x32(rrow + col0 + c, v, N - (col0 + c));
-              store_bf16x32(orow + col0 + c, v, N - (col0 + c));
+              if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, N - (col0 + c));
+              stage_row_bf16x32(stg, lane, c / 8, v);
             }
+            stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (N - col0) * 2,
+                        (fz.lab & 8) != 0);
           }
         }
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(&s.tempty[acc], 0);
+      // The MMA only needs this warp's TMEM reads finished (tcgen05.wait::ld + fence above), not its global
+      // stores, so the arrive is relaxed (lab bit 2 restores release semantics for A/B measurement).
+      if (lane == 0) {
+        if (fz.lab & 4) tc::mbar_arrive_cluster(&s.tempty[acc], 0);
+        else tc::mbar_arrive_cluster_relaxed(&s.tempty[acc], 0);
+      }
     }
   }
 
@@ -343,7 +383,8 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   const int pairs = num_sms() / 2;
   const int64_t tiles = mt_ub * ((N + (mode == 0 ? 127 : 255)) / (mode == 0 ? 128 : 256));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  const Fuse fz{src, static_cast<int>(rows), residual};
+  const char* lab = getenv("README_LAB");
+  const Fuse fz{src, static_cast<int>(rows), residual, lab ? atoi(lab) : 0};
   if (mode == 0)
     ffn_gemm2_kernel<0, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   else if (src == nullptr)

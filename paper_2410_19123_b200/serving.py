@@ -47,10 +47,12 @@ def simulate(policy: str, w_gate, w_up, w_down, n_requests: int = 512, max_token
         if B == 0:
             break
         lg = torch.from_numpy(synth.logits_for_assignments(ex.astype(np.int32), E, seed=int(clock * 1000) % 100003))
+        lg = lg.to(device)
         x = x_pool[torch.from_numpy(req.astype(np.int64)).to(device)]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)  # let the host enqueue the whole step first: the events then time the GPU only
         a.record()
-        y, plan = rd.moe_layer(x, w_gate, w_up, w_down, k=1, logits=lg.to(device))
+        y, plan = rd.moe_layer(x, w_gate, w_up, w_down, k=1, logits=lg)
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)
