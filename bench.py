@@ -285,7 +285,7 @@ def run_decode(args):
                                                    "(decode- / prefill-prioritized), PAPER.md:426; A100 trace replay",
                             "workload": "512 concurrent requests, MaxTokenLen 256, locality p=0.672, 48 steps, "
                                         "one Llama-2-7B-shape MoE layer per step on the GPU"},
-            "gpu_launches": 5 * args.steps}
+            "gpu_launches": 3 * args.steps}  # route, finalize+dispatch, expert FFN
     print(json.dumps(line), flush=True)
 
 
@@ -343,7 +343,7 @@ def run_stack(args):
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                          "traffic": None, "algorithmic": f"L*6*T*k*H*d = {flops:.4g} FLOP per step",
                          "peak_source": f"{pk_src} bf16 sustained (a ~80 ms step)"},
-            "gpu_launches": (2 + 3 * L) * args.steps + args.steps, "clocks": clk.summary()}
+            "gpu_launches": (2 + 2 * L) * args.steps, "clocks": clk.summary()}  # route+finalize, L x (norm-dispatch, FFN)
     print(json.dumps(line), flush=True)
 
 
@@ -433,10 +433,11 @@ def main():
         xs = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
         hbuf = torch.empty((T * k, d), dtype=torch.bfloat16, device=dev)
         y2 = torch.empty_like(x_dev)
+        ws_f = torch.empty(rd.expert_ffn_workspace_bytes(T * k, H, E, d, torch.bfloat16), dtype=torch.uint8,
+                           device=dev)
         stage_fns = [lambda: rd.route(lg_dev, k, plan=plan, ws=ws_r),
                      lambda: rd.dispatch(x_dev, plan.dest, k, out=xs),
-                     lambda: rd.expert_gate_up(xs, plan.offsets, eg, eu, out=hbuf),
-                     lambda: rd.expert_down(hbuf, plan.offsets, ed, src=plan.src, out=y2)]
+                     lambda: rd.expert_ffn(xs, plan.offsets, eg, eu, ed, out=y2, ws=ws_f)]
     with Clocks(local) as clk:
         if world > 1:
             step_ms = timed(step_fn, args.steps)
@@ -457,7 +458,10 @@ def main():
                 torch.cuda.synchronize()
                 stages.append([evs[j].elapsed_time(evs[j + 1]) for j in range(len(stage_fns))])
             st = np.array(stages)
-            route_ms, disp_ms, gu_ms, dn_ms = (st[:, j] for j in range(4))
+            route_ms, disp_ms, ffn_ms = (st[:, j] for j in range(3))
+            # the two projections as separate launches (readme_expert_gate_up / _down), for reference
+            gu_ms = timed(lambda: rd.expert_gate_up(xs, plan.offsets, eg, eu, out=hbuf), max(3, args.steps // 3))
+            dn_ms = timed(lambda: rd.expert_down(hbuf, plan.offsets, ed, src=plan.src, out=y2), max(3, args.steps // 3))
     if world > 1:
         dist.barrier()
     tot_ms = sum(step_ms)
@@ -481,26 +485,25 @@ def main():
         line["step_mode"] = "cuda_graph_replay" if not args.eager else "eager"
         line["eager_ms_per_step"] = float(np.mean(eager_ms))
         line["stage_ms_median"] = {"step": med(step_ms), "route": med(route_ms), "dispatch": med(disp_ms),
-                                   "gate_up": med(gu_ms), "down_combine": med(dn_ms)}
-        f_gu, f_dn = 4.0 * T * k * H * d, 2.0 * T * k * H * d
+                                   "expert_ffn": med(ffn_ms)}
+        f_all, f_gu, f_dn = 6.0 * T * k * H * d, 4.0 * T * k * H * d, 2.0 * T * k * H * d
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("gate_up_bytes_per_launch")
-        ach = f_gu / (float(np.mean(gu_ms)) * 1e-3) / 1e12
-        ach_dn = f_dn / (float(np.mean(dn_ms)) * 1e-3) / 1e12
+                traffic = json.load(f).get("expert_ffn_bytes_per_launch")
+        ach = f_all / (float(np.mean(ffn_ms)) * 1e-3) / 1e12
+        a_gu = f_gu / (float(np.mean(gu_ms)) * 1e-3) / 1e12
+        a_dn = f_dn / (float(np.mean(dn_ms)) * 1e-3) / 1e12
         line["roofline"] = {"bound": "tensor",
-                            "kernel": "a6 grouped gate/up GEMM + SiLU*up (ffn_gemm2_kernel<0>, tcgen05 cta_group::2), "
-                                      "one launch = readme_expert_gate_up",
+                            "kernel": "grouped expert FFN: a6 gate/up GEMM + SiLU*up and a7 down GEMM in ONE persistent "
+                                      "tcgen05 cta_group::2 launch (ffn_layer2_kernel) = readme_expert_ffn",
                             "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                             "frac": ach / pk["bf16_tflops"], "traffic": traffic,
                             "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)",
-                            "algorithmic": f"4*T*k*H*d = {f_gu:.4g} FLOP per launch",
-                            "down_combine": {"achieved": ach_dn, "frac": ach_dn / pk["bf16_tflops"],
-                                             "algorithmic": f"2*T*k*H*d = {f_dn:.4g} FLOP per launch"},
-                            "both_gemms_frac": (f_gu + f_dn) / ((float(np.mean(gu_ms)) + float(np.mean(dn_ms))) * 1e-3)
-                                               / 1e12 / pk["bf16_tflops"]}
+                            "algorithmic": f"6*T*k*H*d = {f_all:.4g} FLOP per launch",
+                            "split_launches": {"gate_up_tflops": a_gu, "gate_up_frac": a_gu / pk["bf16_tflops"],
+                                               "down_combine_tflops": a_dn, "down_combine_frac": a_dn / pk["bf16_tflops"]}}
         # the standalone permutation entries (readme_dispatch / readme_combine), HBM-bound
         ys = torch.empty_like(xs)
         comb_ms = timed(lambda: rd.combine(ys, plan.dest, plan.topk_w, k, out=y2), args.steps)
@@ -512,7 +515,7 @@ def main():
         line["hbm"] = {"dispatch_GBps": dg, "combine_GBps": cg, "peak_GBps": hbm, "dispatch_frac": dg / hbm,
                        "combine_frac": cg / hbm, "note": "readme_dispatch is on the step; readme_combine is the "
                        "standalone entry (inside readme_moe_layer, k=1, it is fused into the down GEMM epilogue)"}
-        line["gpu_launches"] = (5 if k == 1 else 6) * args.steps  # route(2)+dispatch+gate_up+down(+combine if k>1)
+        line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + finalize/dispatch + expert FFN (+combine)
     else:
         line["gpu_launches"] = None
     line["clocks"] = clk.summary()

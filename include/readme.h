@@ -59,6 +59,7 @@ typedef enum { README_F32 = 0, README_BF16 = 1 } readme_dtype;
 
 #define README_DEV_NONFINITE_LOGIT 0x1u /* some logit was NaN/Inf (Q3: NaN ranks as -inf) */
 #define README_DEV_BAD_INDEX 0x2u       /* a caller-supplied plan held an id/row out of range */
+#define README_DEV_SCHED_TIMEOUT 0x4u   /* the single-launch expert FFN could not co-schedule its CTA pairs */
 
 #define README_MAX_EXPERTS 256
 

@@ -68,9 +68,45 @@ readme_status check_rows(readme_dtype dt, int32_t H) {
     if (s_ != README_OK) return s_;     \
   } while (0)
 
-size_t ffn_ws_bytes(int64_t rows, int32_t d, readme_dtype dt) {
-  return align_up(static_cast<size_t>(rows) * d * dt_size(dt), 256) + 256;
+// expert-FFN workspace: h [rows, d] then the merged kernel's readiness counters (sized for 512 segments)
+size_t ffn_h_bytes(int64_t rows, int32_t d, readme_dtype dt) {
+  return align_up(static_cast<size_t>(rows) * d * dt_size(dt), 256);
 }
+size_t ffn_ws_bytes(int64_t rows, int32_t d, readme_dtype dt) {
+  return ffn_h_bytes(rows, d, dt) + ffn_layer_ready_bytes(rows, 512) + 256;
+}
+
+// Which bf16 kernel family runs the expert FFN: the single-launch CTA-pair kernel by default;
+// README_FFN_KERNEL=split (two CTA-pair launches), =1cta (two single-CTA launches) or =unfused
+// (split, and no fused combine in readme_moe_layer) for A/B measurement.
+enum class FfnPath { kMerged, kSplit, k1cta, kUnfused };
+FfnPath ffn_path() {
+  const char* v = getenv("README_FFN_KERNEL");
+  if (!v) return FfnPath::kMerged;
+  if (strcmp(v, "split") == 0) return FfnPath::kSplit;
+  if (strcmp(v, "1cta") == 0) return FfnPath::k1cta;
+  if (strcmp(v, "unfused") == 0) return FfnPath::kUnfused;
+  return FfnPath::kMerged;
+}
+
+// a6 + a7 (+ fused a8 when src != null) over the workspace `ws` (ffn_ws_bytes).
+readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
+                      int32_t n_src, const int32_t* offsets, const void* w_gate, const void* w_up,
+                      const void* w_down, const int32_t* src, const void* residual, void* out, void* ws,
+                      uint32_t* dev_status, cudaStream_t st) {
+  readme_stream_t stream = reinterpret_cast<readme_stream_t>(st);
+  if (dt == README_BF16 && ffn_path() == FfnPath::kMerged) {
+    uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt));
+    return launch_ffn_layer_2cta(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, n_src * E, offsets,
+                                 static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
+                                 static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(ws),
+                                 static_cast<__nv_bfloat16*>(out), src,
+                                 static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st);
+  }
+  README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
+  return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, src, residual, out, stream);
+}
+
 
 }  // namespace
 }  // namespace readme
@@ -220,9 +256,15 @@ readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t r
     set_error("expert_ffn workspace too small: %zu < %zu", ws_bytes, ffn_ws_bytes(rows, d, dt));
     return README_ERR_WORKSPACE;
   }
-  README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
-  return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, nullptr, nullptr, y_sorted, stream);
+  README_CHECK_ARG(x_sorted && w_gate && w_up && w_down && y_sorted, "null pointer argument");
+  README_CHECK_ARG(aligned16(x_sorted) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) &&
+                       aligned16(y_sorted),
+                   "all tensors must be 16-byte aligned");
+  return run_ffn(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted, ws,
+                 nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
+
+
 
 readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
@@ -293,12 +335,15 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   } else {
     README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   }
-  const char* kv = getenv("README_FFN_KERNEL");
-  const bool fused = k == 1 && src != nullptr && !(kv && (strcmp(kv, "1cta") == 0 || strcmp(kv, "unfused") == 0));
+  const FfnPath path = ffn_path();
+  const bool fused = k == 1 && src != nullptr && path != FfnPath::k1cta && path != FfnPath::kUnfused;
   if (fused) {
     // a6, then a7 with a8 fused into its epilogue: y[src[r]] = residual + h_r W_down^T (k == 1, weight 1).
-    README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, ws_ffn, stream));
-    return readme_expert_down(ws_ffn, dt, rows, H, E, d, 1, offsets, w_down, src, residual, y, stream);
+    README_CHECK_ARG(aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y) &&
+                         (!residual || aligned16(residual)),
+                     "tensors must be 16-byte aligned");
+    return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
+                   dev_status, reinterpret_cast<cudaStream_t>(stream));
   }
   README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
                                ffn_ws_bytes(rows, d, dt), stream));
@@ -363,11 +408,12 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
   for (int32_t l = 0; l < L; ++l) {
     README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
     README_TRY(readme_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status, stream));
-    README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], h, stream));
     if (k == 1) {  // x <- x + MoE(RMSNorm(x)): the residual add is fused into the down epilogue, in place
-      README_TRY(readme_expert_down(h, dt, rows, H, E, d, 1, offsets, w_down[l], src, x, x, stream));
+      README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,
+                         dev_status, reinterpret_cast<cudaStream_t>(stream)));
     } else {
-      README_TRY(readme_expert_down(h, dt, rows, H, E, d, 1, offsets, w_down[l], nullptr, nullptr, y_sorted, stream));
+      README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], nullptr, nullptr,
+                         y_sorted, h, dev_status, reinterpret_cast<cudaStream_t>(stream)));
       README_TRY(readme_combine(y_sorted, dt, T, H, k, dest, topk_w, x, x, dev_status, stream));
     }
   }

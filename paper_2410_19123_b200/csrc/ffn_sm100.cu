@@ -363,7 +363,7 @@ readme_status launch_gemm_1cta(int mode, const __nv_bfloat16* A, int64_t rows, i
 bool force_1cta() {
   const char* v = getenv("README_FFN_KERNEL");
   return v && strcmp(v, "1cta") == 0;
-}
+}  // (=split / =unfused keep the CTA-pair kernels; see capi.cu ffn_path())
 
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,

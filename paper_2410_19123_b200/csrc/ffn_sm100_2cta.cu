@@ -46,6 +46,8 @@ struct __align__(8) Smem {
   alignas(16) uint8_t stg[4][32 * 128];  // epilogue staging, one 4 KB tile per epilogue warp
   int seg_off[kMaxSeg + 1];
   int tile_start[kMaxSeg + 1];
+  int tile_start2[kMaxSeg + 1];  // merged a6+a7 kernel: the down tiles' prefix
+  int mt_start[kMaxSeg + 1];     // merged kernel: first m-tile id of each segment (readiness counters)
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 
@@ -337,6 +339,306 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
 }
 
+
+// ===================================================================================================
+// The whole expert FFN (a6 then a7, a8 fused for k == 1) in ONE persistent CTA-pair launch. The tile list
+// is [every gate/up tile][every down tile], statically strided over the pairs; a down tile (g, m) starts
+// once all NT1 gate/up tiles of (g, m) have stored their h rows: each epilogue warp publishes its part of
+// a gate/up tile with a release add on ready[m-tile] (after a generic->async proxy fence, since the down
+// tile reads h with TMA), and the down producer acquires ready[m-tile] == NT1 * 8 before loading. Down
+// tiles come after every gate/up tile in every pair's sequence, so a wait only ever depends on tiles that
+// are earlier in some pair's sequence (all pairs are co-resident: one CTA per SM, grid <= #SMs; a bounded
+// poll flags README_DEV_SCHED_TIMEOUT instead of hanging if that ever fails). This removes the gate/up
+// kernel's tail, the down kernel's prologue and the down kernel's last-round imbalance.
+struct LayerArgs {
+  int H, d, E, nseg;
+  const int32_t* offsets;
+  __nv_bfloat16* h;          // [rows, d]
+  __nv_bfloat16* y;          // [rows, H] (y_sorted) or [T, H] (scatter)
+  uint32_t* ready;           // [#m-tiles] zeroed before the launch
+  uint32_t* dev_status;
+  Fuse fz;
+};
+
+struct LTile {
+  int mode, g, mt, m0, rows, n0;
+  bool m256;
+};
+
+__device__ __forceinline__ LTile decode_ltile(const Smem& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
+                                             int& gcur2) {
+  LTile tl;
+  int local, g, NT;
+  if (t < T1) {
+    while (gcur1 + 1 < nseg && s.tile_start[gcur1 + 1] <= t) ++gcur1;
+    g = gcur1;
+    local = t - s.tile_start[g];
+    tl.mode = 0;
+    NT = NT1;
+  } else {
+    const int t2 = t - T1;
+    while (gcur2 + 1 < nseg && s.tile_start2[gcur2 + 1] <= t2) ++gcur2;
+    g = gcur2;
+    local = t2 - s.tile_start2[g];
+    tl.mode = 1;
+    NT = NT2;
+  }
+  (void)NT;
+  const int cnt = s.seg_off[g + 1] - s.seg_off[g];
+  const int mt_g = (cnt + 255) / 256;
+  const int nt = local / mt_g, mt = local % mt_g;
+  tl.g = g;
+  tl.mt = mt;
+  tl.m0 = s.seg_off[g] + mt * 256;
+  tl.rows = min(256, cnt - mt * 256);
+  tl.m256 = tl.rows > 128;
+  tl.n0 = nt * (tl.mode == 0 ? 128 : 256);
+  return tl;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int kFuse>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
+                  const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
+                  const __grid_constant__ CUtensorMap tmD, LayerArgs la) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
+  const uint32_t cta = tc::cluster_ctarank();
+  const bool leader = cta == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
+  const int NT1 = (d + 127) / 128, NT2 = (H + 255) / 256;
+  const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
+  const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
+
+  for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = la.offsets[i];
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmX);
+    tc::prefetch_tmap(&tmG);
+    tc::prefetch_tmap(&tmU);
+    tc::prefetch_tmap(&tmH);
+    tc::prefetch_tmap(&tmD);
+  }
+  if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
+  __syncthreads();
+  if (tid == 0) {
+    int a1 = 0, a2 = 0, am = 0;
+    for (int g = 0; g < nseg; ++g) {
+      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + 255) / 256;
+      s.tile_start[g] = a1;
+      s.tile_start2[g] = a2;
+      s.mt_start[g] = am;
+      a1 += mt_g * NT1;
+      a2 += mt_g * NT2;
+      am += mt_g;
+    }
+    s.tile_start[nseg] = a1;
+    s.tile_start2[nseg] = a2;
+    s.mt_start[nseg] = am;
+    for (int i = 0; i < kStages; ++i) {
+      tc::mbar_init(&s.full[i], 1);
+      tc::mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s.tfull[i], 1);
+      tc::mbar_init(&s.tempty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  const int T1 = s.tile_start[nseg];
+  const int ntiles = T1 + s.tile_start2[nseg];
+  const uint32_t tmem_base = s.tmem_base;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
+    int stage = 0;
+    uint32_t phase = 0;
+    int g1 = 0, g2 = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+      const int e = tl.g % E;
+      const int a_rows = tl.m256 ? 128 : 64;
+      const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
+      if (tl.mode == 1) {
+        // wait until every gate/up tile of this m-tile has published its h rows
+        if (lane == 0) {
+          const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
+          uint32_t spins = 0;
+          while (ld_acquire_u32(rp) < ready_target) {
+            __nanosleep(128);
+            if (++spins == (1u << 25)) {
+              if (la.dev_status) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+              break;
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+      }
+      const int KB = tl.mode == 0 ? KB1 : KB2;
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::mbar_wait(&s.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          const uint32_t fb = tc::mapa(&s.full[stage], 0);
+          const int k0 = kb * kBK;
+          if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
+          const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
+          tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
+          if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
+          if (tl.mode == 0) {
+            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
+            tc::tma_load_3d_2sm(&tmU, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
+          } else {
+            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, tl.n0 + 128 * static_cast<int>(cta), e);
+            tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 128 * static_cast<int>(cta) + 64, e);
+          }
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer (leader CTA, one thread) =====
+      constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
+      constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
+      int stage = 0;
+      uint32_t phase = 0;
+      int g1 = 0, g2 = 0, i = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++i) {
+        const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+        const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
+        const int acc = i & 1;
+        const uint32_t use = static_cast<uint32_t>(i >> 1);
+        tc::mbar_wait_cluster(&s.tempty[acc], (use & 1u) ^ 1u);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+        const int KB = tl.mode == 0 ? KB1 : KB2;
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait_cluster(&s.full[stage], phase);
+          tc::fence_after();
+          const uint32_t a0 = tc::smem_u32(s.a[stage]), b0 = tc::smem_u32(s.b[stage]);
+#pragma unroll
+          for (int kk = 0; kk < kBK / kUK; ++kk)
+            tc::mma_f16<2>(d_tmem, tc::sdesc_sw128(a0 + kk * kUK * 2), tc::sdesc_sw128(b0 + kk * kUK * 2), idesc,
+                           (kb | kk) != 0 ? 1u : 0u);
+          tc::commit_2sm_mc(&s.empty[stage], 0x3);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 of both CTAs =====
+    const int q = warp & 3;
+    uint8_t* stg = s.stg[q];
+    int g1 = 0, g2 = 0, i = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++i) {
+      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+      const int acc = i & 1;
+      const uint32_t use = static_cast<uint32_t>(i >> 1);
+      tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
+      tc::fence_after();
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256);
+      int row_in_tile, n_windows, out_off;
+      const int bn_out = tl.mode == 0 ? 128 : 256;
+      if (tl.m256) {
+        row_in_tile = static_cast<int>(cta) * 128 + q * 32 + lane;
+        n_windows = 2;
+        out_off = 0;
+      } else {
+        row_in_tile = static_cast<int>(cta) * 64 + (q & 1) * 32 + lane;
+        n_windows = 1;
+        out_off = (q >> 1) * (bn_out / 2);
+      }
+      const bool valid = row_in_tile < tl.rows;
+      const int64_t r = tl.m0 + row_in_tile;
+      if (tl.mode == 0) {
+        __nv_bfloat16* orow = la.h + r * d;
+        for (int w = 0; w < n_windows; ++w) {
+          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
+          const int hcol0 = tl.n0 + out_off + w * 64;
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 32) {
+            uint32_t gr[32], ur[32];
+            tc::tmem_ld32(wbase + c, gr);
+            tc::tmem_ld32(wbase + 64 + c, ur);
+            tc::tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+            stage_row_bf16x32(stg, lane, c / 8, v);
+          }
+          stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, (d - hcol0) * 2, false);
+        }
+      } else {
+        int64_t orow_idx = r;
+        bool valid_row = valid;
+        if constexpr (kFuse == 1) {
+          orow_idx = valid ? __ldg(la.fz.src + r) : 0;
+          valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
+        }
+        __nv_bfloat16* orow = la.y + orow_idx * H;
+        const __nv_bfloat16* rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
+        for (int w = 0; w < n_windows; ++w) {
+          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 64) {
+            const int col0 = tl.n0 + out_off + w * 128 + c0;
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 32) {
+              uint32_t vr[32];
+              tc::tmem_ld32(wbase + c0 + c, vr);
+              tc::tmem_wait_ld();
+              float v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+              if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
+              stage_row_bf16x32(stg, lane, c / 8, v);
+            }
+            stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2,
+                        false);
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive_cluster_relaxed(&s.tempty[acc], 0);
+        if (tl.mode == 0) {
+          // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release)
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + s.mt_start[tl.g] + tl.mt)
+                       : "memory");
+        }
+      }
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
+}
+
 readme_status set_smem_attr() {
   static std::once_flag once[64];
   static cudaError_t err[64];
@@ -344,11 +646,13 @@ readme_status set_smem_attr() {
   README_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) dev = 0;
   std::call_once(once[dev], [&] {
-    const void* fns[3] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
+    const void* fns[5] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
-                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>)};
+                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<0>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1>)};
     err[dev] = cudaSuccess;
-    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
+    for (int i = 0; i < 5 && err[dev] == cudaSuccess; ++i)
       err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   });
   if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
@@ -391,6 +695,44 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
     ffn_gemm2_kernel<1, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   else
     ffn_gemm2_kernel<1, 1><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
+  return align_up(static_cast<size_t>(nseg + (rows + 255) / 256 + 1) * sizeof(uint32_t), 256);
+}
+
+readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                    int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                    const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
+                                    __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
+                                    uint32_t* ready, uint32_t* dev_status, cudaStream_t st) {
+  if (rows == 0) return README_OK;
+  if (nseg > kMaxSeg) {
+    set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
+    return README_ERR_UNSUPPORTED;
+  }
+  readme_status rs = set_smem_attr();
+  if (rs != README_OK) return rs;
+  CUtensorMap mX, mG, mU, mH, mD;
+  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, E, kBK, 64) &&
+            tc::make_map_3d(&mU, wu, H, d, E, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
+            tc::make_map_3d(&mD, wd, d, H, E, kBK, 64);
+  if (!ok) {
+    set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
+    return README_ERR_CUDA;
+  }
+  README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
+  const int64_t mt_ub = nseg + (rows + 255) / 256;
+  const int pairs = num_sms() / 2;
+  const int64_t tiles = mt_ub * ((d + 127) / 128 + (H + 255) / 256);
+  const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+  LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0}};
+  if (src)
+    ffn_layer2_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
+  else
+    ffn_layer2_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

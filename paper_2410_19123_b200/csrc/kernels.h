@@ -42,6 +42,14 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
                                int32_t nseg, const int32_t* offsets, const __nv_bfloat16* B0,
                                const __nv_bfloat16* B1, __nv_bfloat16* out, const int32_t* src,
                                const __nv_bfloat16* residual, cudaStream_t st);
+// a6 + a7 (+ a8 when src != null, k == 1) in one persistent CTA-pair launch; `ready` is a device scratch of
+// ffn_layer_ready_bytes() bytes (zeroed by the launcher).
+size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg);
+readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                    int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                    const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
+                                    __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
+                                    uint32_t* ready, uint32_t* dev_status, cudaStream_t st);
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                   const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);

@@ -47,6 +47,8 @@ for name, off in offs.items():
     o = torch.from_numpy(off).to(dev)
     gu = timeit(lambda: rd.expert_gate_up(xs, o, wg, wu, out=h))
     dn = timeit(lambda: rd.expert_down(h, o, wd, out=ys))
-    print(json.dumps({"variant": variant, "routing": name, "gate_up_ms": gu, "down_ms": dn,
-                      "gate_up_tflops": 4 * T * H * d / gu / 1e9, "down_tflops": 2 * T * H * d / dn / 1e9}),
-          flush=True)
+    ws = torch.empty(rd.expert_ffn_workspace_bytes(T, H, E, d, torch.bfloat16), dtype=torch.uint8, device=dev)
+    ffn = timeit(lambda: rd.expert_ffn(xs, o, wg, wu, wd, out=ys, ws=ws))
+    print(json.dumps({"variant": variant, "routing": name, "gate_up_ms": gu, "down_ms": dn, "expert_ffn_ms": ffn,
+                      "gate_up_tflops": 4 * T * H * d / gu / 1e9, "down_tflops": 2 * T * H * d / dn / 1e9,
+                      "expert_ffn_tflops": 6 * T * H * d / ffn / 1e9}), flush=True)

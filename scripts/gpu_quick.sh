@@ -15,5 +15,5 @@ if [ "${PROF:-1}" = "1" ]; then
 B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 run launches 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B
 EXTRA=sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum
-run ncu_gemm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:ffn_gemm -s 2 -c 2 -o gpurun_out/prof_gemm $B
+run ncu_gemm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"ffn_layer2|route_tile|finalize_dispatch" -s 3 -c 3 -o gpurun_out/prof_gemm $B
 fi

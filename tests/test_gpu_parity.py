@@ -177,7 +177,7 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
     (4000, 512, 256, 8, 1, "zipf"),    # many 256-row tiles, 128-row and 256-row tails
     (1024, 256, 128, 4, 1, None),      # counts ~256 -> exact and near-exact tiles
 ])
-@pytest.mark.parametrize("kernel", ["2cta", "1cta"])
+@pytest.mark.parametrize("kernel", ["merged", "split", "1cta"])
 def test_expert_ffn_bf16_teacher_forced(rd, monkeypatch, kernel, T, H, d, E, k, skew):
     monkeypatch.setenv("README_FFN_KERNEL", kernel)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + H, skew=skew)
@@ -220,7 +220,7 @@ def test_gate_up_and_down_separately(rd, dt):
     assert rel_err(_np(y), ref) <= tol
 
 
-@pytest.mark.parametrize("kernel", ["2cta", "1cta"])
+@pytest.mark.parametrize("kernel", ["merged", "split", "1cta"])
 def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
     """Segment sizes on every tile boundary: empty, 1 row, 64/128/256 +- 1 (M=128 vs M=256 tails)."""
     monkeypatch.setenv("README_FFN_KERNEL", kernel)
@@ -250,7 +250,7 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("path", ["fused", "unfused", "1cta"])
+@pytest.mark.parametrize("path", ["fused", "split", "unfused", "1cta"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
                                            ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
                                            ("bf16", 3000, 1024, 1376, 8, 1)])
