@@ -289,6 +289,49 @@ def run_decode(args):
     print(json.dumps(line), flush=True)
 
 
+def run_tiny(args):
+    """Config 1: the tiny fp32 layer (E=8, top-1, H=64, expert width 128, T=256) — latency only (SURVEY
+    §8(d)); the CUDA-core fp32 path (no TF32)."""
+    import torch
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    c = synth.CONFIGS[1]
+    T, H, d, E, k = c["T"], c["H"], c["d"], c["E"], c["k"]
+    seed = synth.MASTER_SEED + 1
+    x = synth.to_torch(synth.tokens(T, H, seed=seed), "f32").to(dev)
+    lg = torch.from_numpy(synth.router_logits(T, E, seed=seed)).to(dev)
+    W = [synth.to_torch(w, "f32").to(dev) for w in synth.expert_weights(E, d, H, seed=seed)]
+    plan = rd.new_plan(T, E, k, dev)
+    y = torch.empty_like(x)
+    ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, k, torch.float32), dtype=torch.uint8, device=dev)
+    fn = lambda: rd.moe_layer(x, *W, k=k, logits=lg, plan=plan, out=y, ws=ws)
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    ms = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        ms.append((a, b))
+    torch.cuda.synchronize()
+    t = float(np.mean([a.elapsed_time(b) for a, b in ms]))
+    line = {"metric": METRIC, "value": T / (t * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config1_tiny", "T": T, "H": H, "E": E, "d": d, "k": k,
+                       "note": "latency-bound (12.6 MFLOP); graph replay, warm L2"},
+            "latency_us": t * 1e3, "gpu_launches": 3 * args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def run_stack(args):
     """Config 4: the full 32-layer refactored MoE stack (MoE-only pre-norm, reading Q10), T = 16384 tokens
     (4 requests x 4096, Markov expert locality p = 0.672), routed ONCE per request batch
@@ -354,6 +397,9 @@ def main():
         return
     if args.config == 3 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         run_decode(args)
+        return
+    if args.config == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        run_tiny(args)
         return
     if args.config == 4 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         run_stack(args)

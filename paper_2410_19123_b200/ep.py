@@ -41,6 +41,11 @@ class EPPlan:
         return int(self.seg_offsets[-1])
 
 
+def _host_staged(group) -> bool:
+    """gloo has no device all-to-all: stage CUDA tensors through host memory (CPU tests, one-GPU tests)."""
+    return dist.get_backend(group) == "gloo"
+
+
 def plan_from_counts(counts_local, group=None) -> EPPlan:
     """C1: exchange per-expert counts once per batch. `counts_local` is this rank's [E] int32 histogram
     (any device the process group's backend accepts). Returns host-side split lists and segment table."""
@@ -51,6 +56,8 @@ def plan_from_counts(counts_local, group=None) -> EPPlan:
         raise ValueError(f"E={E} experts cannot be sharded over {G} ranks")
     El = E // G
     send = counts_local.reshape(G, El).contiguous()
+    if _host_staged(group):
+        send = send.cpu()
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)  # recv[p, e] = rows source p has for my expert e
     send_h = send.cpu().numpy().astype(np.int64)
@@ -69,6 +76,11 @@ def exchange(rows: torch.Tensor, plan: EPPlan, reverse: bool = False, out: torch
     n_out = int(sum(out_s))
     if out is None:
         out = torch.empty((n_out,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    if _host_staged(group) and rows.is_cuda:
+        tmp = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(tmp, rows.cpu(), output_split_sizes=out_s, input_split_sizes=in_s, group=group)
+        out.copy_(tmp)
+        return out
     dist.all_to_all_single(out, rows, output_split_sizes=out_s, input_split_sizes=in_s, group=group)
     return out
 

@@ -1,0 +1,67 @@
+"""Expert parallelism with the real CUDA kernels on ONE GPU (-m gpu): G ranks run as G processes sharing
+cuda:0 over the gloo backend (NCCL refuses two ranks on one device). Each rank routes its own tokens,
+exchanges rows with the all-to-alls of paper_2410_19123_b200.ep, runs readme_expert_ffn over the
+(source rank, local expert) segments of its expert shard and combines. The result must equal the
+single-GPU layer bit for bit (P12: rows reach their expert in global token order and no kernel splits K)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, H, E, d, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_2410_19123_b200 import ep
+        from paper_2410_19123_b200 import readme as rd
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        El = E // world
+        x = synth.to_torch(synth.tokens(T * world, H, seed=1), "bf16").to(dev)
+        lg = torch.from_numpy(synth.router_logits(T * world, E, seed=2)).to(dev)
+        W = [synth.to_torch(w, "bf16").to(dev) for w in synth.expert_weights(E, d, H, seed=3)]
+        y_full, _ = rd.moe_layer(x, *W, logits=lg)
+        sl = slice(rank * El, (rank + 1) * El)
+        layer = ep.EPMoELayer(x[rank * T:(rank + 1) * T].contiguous(), lg[rank * T:(rank + 1) * T].contiguous(),
+                              W[0][sl].contiguous(), W[1][sl].contiguous(), W[2][sl].contiguous(), E, 1)
+        y = layer.step()
+        torch.cuda.synchronize()
+        ok = torch.equal(y, y_full[rank * T:(rank + 1) * T])
+        q.put((rank, bool(ok), layer.ep.recv_splits))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_on_one_gpu_equals_single_layer(world):
+    T, H, E, d = 512, 256, 8, 256
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, H, E, d, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, splits in res:
+        assert ok is True, f"rank {rank}: {ok}"
