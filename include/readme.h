@@ -120,7 +120,7 @@ readme_status readme_expert_gate_up(const void* x_sorted, readme_dtype dt, int64
 /* a7 alone: y_sorted_r = h_r W_down[e]^T per segment, out [rows,H]. With src != NULL (a layer with k == 1, whose
  * combine weight is exactly 1) row r is instead written to out[src[r]] + residual[src[r]] (residual nullable;
  * out is then y [T = rows, H]): the combine a8 fused into the epilogue, fp32 add, one rounding. Rows whose
- * src is out of range are skipped. residual without src is an argument error. */
+ * src is out of range are skipped. With src == NULL and residual != NULL: out[r] = residual[r] + y_r. */
 readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
                                  int32_t n_src, const int32_t* offsets, const void* w_down, const int32_t* src,
                                  const void* residual, void* out, readme_stream_t stream);
@@ -164,6 +164,16 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
                                float eps, int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets,
                                int32_t* dest, int32_t* src, uint32_t* dev_status, void* ws, size_t ws_bytes,
                                readme_stream_t stream);
+
+/* The permanent expert (§3: neurons "activated for all tokens", NEXT-3 of SURVEY §8(f)):
+ *     y[t] <- y[t] + F_perm(x[t]),   F_perm(x) = W_down,p (silu(W_gate,p x) * (W_up,p x))   for EVERY token,
+ * added in place to y (call it after readme_moe_layer). w_gate/w_up [d_perm,H], w_down [H,d_perm] of dtype
+ * dt; runs the same grouped-GEMM kernels over one segment of T rows (no dispatch: token order), with the
+ * add fused into the down projection's epilogue. ws: readme_permanent_expert_workspace_bytes(...). */
+size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_perm, readme_dtype dt);
+readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t d_perm,
+                                      const void* w_gate, const void* w_up, const void* w_down, void* y, void* ws,
+                                      size_t ws_bytes, readme_stream_t stream);
 
 /* Setup (once per model load, not on the timed path): expert slicing, PAPER.md:159-163 (M_i is a
  * selection matrix without replacement).  dense_w_gate/up [D,H], dense_w_down [H,D] of dtype dt;

@@ -232,7 +232,6 @@ readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, i
   README_TRY(check_ffn_args(dt, rows, H, E, d, n_src, offsets));
   if (rows == 0) return README_OK;
   README_CHECK_ARG(h && w_down && out, "null pointer argument");
-  README_CHECK_ARG(src || !residual, "residual requires src (the fused-combine form)");
   README_CHECK_ARG(aligned16(h) && aligned16(w_down) && aligned16(out) && (!residual || aligned16(residual)),
                    "all tensors must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -418,6 +417,36 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
     }
   }
   return README_OK;
+}
+
+readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t d_perm,
+                                      const void* w_gate, const void* w_up, const void* w_down, void* y, void* ws,
+                                      size_t ws_bytes, readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
+  README_CHECK_ARG(d_perm >= 8 && d_perm % 8 == 0, "d_perm must be a positive multiple of 8 (got %d)", d_perm);
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(x && w_gate && w_up && w_down && y && ws, "null pointer argument");
+  README_CHECK_ARG(aligned16(x) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y) &&
+                       aligned16(ws),
+                   "all tensors must be 16-byte aligned");
+  const size_t need = readme_permanent_expert_workspace_bytes(T, H, d_perm, dt);
+  if (ws_bytes < need) {
+    set_error("permanent_expert workspace too small: %zu < %zu", ws_bytes, need);
+    return README_ERR_WORKSPACE;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // one segment covering every token in token order: offsets = {0, T} (kept at the front of ws)
+  int32_t* offs = static_cast<int32_t*>(ws);
+  README_TRY(launch_set_offsets(offs, static_cast<int32_t>(T), st));
+  void* ws_ffn = static_cast<char*>(ws) + 256;
+  // y <- y + F_perm(x): the down projection adds the residual y in its epilogue, in place (identity rows)
+  return run_ffn(x, dt, T, H, 1, d_perm, 1, offs, w_gate, w_up, w_down, nullptr, y, y, ws_ffn, nullptr, st);
+}
+
+size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_perm, readme_dtype dt) {
+  (void)H;
+  return 256 + ffn_ws_bytes(T < 0 ? 0 : T, d_perm < 0 ? 0 : d_perm, dt);
 }
 
 readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,

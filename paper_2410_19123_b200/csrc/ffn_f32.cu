@@ -85,8 +85,8 @@ ffn_f32_kernel(const float* __restrict__ A, int64_t rows, int K, int N, int E, i
     if (src) {  // fused combine (k == 1): row r holds token src[r]
       orow = src[r];
       if (orow < 0 || orow >= rows) continue;
-      if (residual) v += residual[orow * N + n];
     }
+    if (residual) v += residual[orow * N + n];
     C[orow * N + n] = v;
   }
 }

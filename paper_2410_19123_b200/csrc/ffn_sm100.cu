@@ -375,7 +375,8 @@ readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t
 readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
                                const int32_t* offsets, const __nv_bfloat16* wd, __nv_bfloat16* out,
                                const int32_t* src, const __nv_bfloat16* residual, cudaStream_t st) {
-  if (force_1cta() && src == nullptr) return launch_gemm_1cta(1, h, rows, d, H, E, nseg, offsets, wd, wd, out, st);
+  if (force_1cta() && src == nullptr && residual == nullptr)
+    return launch_gemm_1cta(1, h, rows, d, H, E, nseg, offsets, wd, wd, out, st);
   return launch_gemm_2cta(1, h, rows, d, H, E, nseg, offsets, wd, nullptr, out, src, residual, st);
 }
 

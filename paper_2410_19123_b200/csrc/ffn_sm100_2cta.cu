@@ -274,8 +274,8 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const bool valid = row_in_tile < tl.rows && !(fz.lab & 1);
       int64_t orow_idx = tl.m0 + row_in_tile;
       bool valid_row = valid;
-      if constexpr (kMode == 1 && kFuse == 1) {  // k == 1: expert row r holds token src[r]
-        orow_idx = valid ? __ldg(fz.src + orow_idx) : 0;
+      if constexpr (kMode == 1 && kFuse == 1) {  // k == 1: expert row r holds token src[r] (identity if null)
+        orow_idx = valid ? (fz.src ? __ldg(fz.src + orow_idx) : orow_idx) : 0;
         valid_row = valid && orow_idx >= 0 && orow_idx < fz.rows;  // a corrupt plan never writes out of bounds
       }
       __nv_bfloat16* orow = out + orow_idx * N;
@@ -592,7 +592,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         int64_t orow_idx = r;
         bool valid_row = valid;
         if constexpr (kFuse == 1) {
-          orow_idx = valid ? __ldg(la.fz.src + r) : 0;
+          orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
           valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
         }
         __nv_bfloat16* orow = la.y + orow_idx * H;
@@ -691,7 +691,7 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   const Fuse fz{src, static_cast<int>(rows), residual, lab ? atoi(lab) : 0};
   if (mode == 0)
     ffn_gemm2_kernel<0, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
-  else if (src == nullptr)
+  else if (src == nullptr && residual == nullptr)
     ffn_gemm2_kernel<1, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   else
     ffn_gemm2_kernel<1, 1><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
@@ -729,7 +729,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   const int64_t tiles = mt_ub * ((d + 127) / 128 + (H + 255) / 256);
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0}};
-  if (src)
+  if (src || residual)
     ffn_layer2_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
   else
     ffn_layer2_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);

@@ -13,6 +13,7 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
 // permute.cu
 readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st);
+readme_status launch_set_offsets(int32_t* offs, int32_t T, cudaStream_t st);  // {0, T}
 readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,
                                        const int32_t* topk_idx, const int32_t* offsets, int32_t* dest, int32_t* src,
                                        void* x_sorted, cudaStream_t st);

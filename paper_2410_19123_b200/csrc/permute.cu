@@ -14,6 +14,11 @@ namespace readme {
 namespace {
 
 constexpr int kPermThreads = 256;
+
+__global__ void set_offsets_kernel(int32_t* offs, int32_t T) {
+  offs[0] = 0;
+  offs[1] = T;
+}
 constexpr int kUnroll = 4;
 
 // One warp moves one row of `vec` uint4 from src_row to dst_row.
@@ -243,6 +248,12 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
   dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
       static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
       static_cast<uint4*>(x_sorted), dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_set_offsets(int32_t* offs, int32_t T, cudaStream_t st) {
+  set_offsets_kernel<<<1, 1, 0, st>>>(offs, T);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

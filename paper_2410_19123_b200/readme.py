@@ -24,7 +24,8 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 # Every symbol include/readme.h declares (tests check the library exports exactly these).
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
-           "readme_build_experts", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
+           "readme_build_experts", "readme_permanent_expert_workspace_bytes", "readme_permanent_expert",
+           "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
            "readme_scheduler_next_batch", "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
@@ -70,6 +71,9 @@ _SIGS = {
     "readme_scheduler_push": (ctypes.c_int, [_vp, _vp, _vp, _i64]),
     "readme_scheduler_queued": (_i64, [_vp, _i32]),
     "readme_scheduler_next_batch": (_i64, [_vp, _i64, _vp, _vp]),
+    "readme_permanent_expert_workspace_bytes": (_sz, [_i64, _i32, _i32, ctypes.c_int]),
+    "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
+                                               _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -384,3 +388,17 @@ class ExpertScheduler:
         if n < 0:
             raise ValueError("readme_scheduler_next_batch: bad argument")
         return t[:n].copy(), e[:n].copy()
+
+
+def permanent_expert(x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor,
+                     y: torch.Tensor, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """y += F_perm(x) for every token (the permanent expert; readme_permanent_expert)."""
+    T, H = x.shape
+    dp = w_gate.shape[0]
+    need = int(lib().readme_permanent_expert_workspace_bytes(T, H, dp, _dt(x)))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    st = _prep(x, w_gate, w_up, w_down, y, ws)
+    _check("readme_permanent_expert", lib().readme_permanent_expert(
+        _ptr(x), _dt(x), T, H, dp, _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(y), _ptr(ws), ws.numel(), st))
+    return y

@@ -453,3 +453,17 @@ def test_serving_expert_aware_touches_fewer_experts(rd):
     b = serving.simulate("fifo", *W, n_requests=256, max_tokens=64, steps=20, device=DEV)
     assert a["tokens"] == b["tokens"] == 20 * 64
     assert a["mean_unique_experts"] < b["mean_unique_experts"]
+
+
+# ---- NEXT-3: permanent expert ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_permanent_expert(rd, dt):
+    T, H, d, E, dp = 900, 256, 256, 8, 136
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, dt, seed=181)
+    pg, pu, pd = (synth.to_torch(w, dt) for w in synth.expert_weights(1, dp, H, seed=182))
+    y, _ = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), logits=torch.from_numpy(lg).to(DEV))
+    rd.permanent_expert(x.to(DEV), pg[0].to(DEV), pu[0].to(DEV), pd[0].to(DEV), y)
+    yref, _ = oracle.moe_layer(x, lg, 1, wg, wu, wd)
+    yref = yref + oracle.expert_ffn(x, np.array([0, T], np.int32), pg, pu, pd)
+    assert rel_err(_np(y), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)

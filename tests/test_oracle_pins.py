@@ -375,3 +375,25 @@ def test_stack_zero_down_is_identity_and_routes_once():
     assert np.array_equal(y, x.astype(np.float64))  # W_down = 0 -> every layer adds exactly 0
     ref = oracle.route(lg, 1)
     assert np.array_equal(plan["dest"], ref["dest"])
+
+
+# ---- NEXT-3: permanent expert ----------------------------------------------------------
+
+def test_permanent_expert_folds_into_every_expert_Q6():
+    """k=1: an expert whose neuron set is S_e plus the permanent set P (disjoint) equals expert S_e plus the
+    always-on expert P — outputs sum over neurons (linearity of W_2 M^T in PAPER.md:159)."""
+    T, H, D, E, d, p = 24, 16, 64, 4, 10, 6
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=151)
+    g = synth.rng(152, 0)
+    perm = g.permutation(D)
+    P = np.sort(perm[:p]).astype(np.int32)
+    rest = perm[p:]
+    S = np.stack([np.sort(g.choice(rest, size=d, replace=False)) for _ in range(E)]).astype(np.int32)
+    SP = np.sort(np.concatenate([S, np.tile(P, (E, 1))], axis=1), axis=1).astype(np.int32)
+    x = synth.tokens(T, H, seed=153)
+    lg = synth.router_logits(T, E, seed=154)
+    folded, _ = oracle.moe_layer(x, lg, 1, *oracle.build_experts(wg, wu, wd, SP))
+    base, _ = oracle.moe_layer(x, lg, 1, *oracle.build_experts(wg, wu, wd, S))
+    pg, pu, pd = oracle.build_experts(wg, wu, wd, P[None, :])
+    perm_y = oracle.expert_ffn(x, np.array([0, T], np.int32), pg, pu, pd)
+    assert rel_err(base + perm_y, folded) < 1e-12
