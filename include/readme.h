@@ -15,6 +15,7 @@
  *   readme_moe_layer  a1-a8  the whole layer; with logits == NULL it reuses a routing plan (a9: route
  *                            once, reuse across all L layers)
  *   readme_moe_stack         L pre-norm MoE layers routed once (config 4), in place
+ *   readme_router_forward    the pre-gating router G itself (one causal transformer block + gating head)
  *   readme_build_experts     setup: slice expert stacks out of the dense FFN
  * Readings of the paper (Q1..Q14) are listed in DESIGN.md; they are cited below where they decide a
  * behaviour.
@@ -174,6 +175,38 @@ size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_p
 readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t d_perm,
                                       const void* w_gate, const void* w_up, const void* w_down, void* y, void* ws,
                                       size_t ws_bytes, readme_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* The pre-gating router G (NEXT-1 of SURVEY §8(f)): PAPER.md:130-133 (§2.3, "one transformer block with
+ * causal attention"), table:router_details (1 layer, 4 heads, vocab 32000, embedding and
+ * feature dim 512, MLP intermediate dim 512, SwiGLU, RoPE, RMSNorm, 18.0 M parameters) and a linear gating
+ * head to the N expert logits G(x_<=t) that readme_route consumes. Readings (Q15): Llama-style
+ * pre-norm block h1 = h0 + Attn(RMSNorm_1(h0)), h2 = h1 + MLP(RMSNorm_2(h1)),
+ * logits = RMSNorm_f(h2) W_head^T; RoPE theta 10000 on the (i, i+64) halves of each 128-dim head; no biases.
+ * Run once per token, never per layer. All weights bf16 DEVICE pointers, nn.Linear
+ * [out, in] layout; the struct itself is a host object read during the call. */
+typedef struct {
+  int32_t vocab;       /* rows of emb (32000 in the paper) */
+  int32_t n_experts;   /* N, rows of w_head (1..16) */
+  const void* emb;     /* [vocab, 512] */
+  const void* norm1;   /* [512] RMSNorm weight before attention */
+  const void* w_qkv;   /* [1536, 512]: rows 0..511 W_q, 512..1023 W_k, 1024..1535 W_v */
+  const void* w_o;     /* [512, 512] */
+  const void* norm2;   /* [512] RMSNorm weight before the MLP */
+  const void* w_gate;  /* [512, 512] SwiGLU MLP */
+  const void* w_up;    /* [512, 512] */
+  const void* w_down;  /* [512, 512] */
+  const void* norm_f;  /* [512] final RMSNorm weight */
+  const void* w_head;  /* [n_experts, 512] gating head */
+} readme_router_weights;
+
+/* token_ids [T] int32 (device), sequences concatenated: seq_starts [nseq+1] int32 (DEVICE), seq_starts[0] = 0,
+ * non-decreasing, seq_starts[nseq] = T; attention is causal inside each sequence and positions restart at 0
+ * for each one. logits [T, n_experts] f32 out. Out-of-vocabulary ids set README_DEV_BAD_INDEX (id 0 used). */
+size_t readme_router_workspace_bytes(int64_t T, int32_t nseq);
+readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
+                                    const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
+                                    void* ws, size_t ws_bytes, readme_stream_t stream);
 
 /* Setup (once per model load, not on the timed path): expert slicing, PAPER.md:159-163 (M_i is a
  * selection matrix without replacement).  dense_w_gate/up [D,H], dense_w_down [H,D] of dtype dt;

@@ -62,11 +62,6 @@ readme_status check_rows(readme_dtype dt, int32_t H) {
   return README_OK;
 }
 
-#define README_TRY(expr)                \
-  do {                                  \
-    readme_status s_ = (expr);          \
-    if (s_ != README_OK) return s_;     \
-  } while (0)
 
 // expert-FFN workspace: h [rows, d] then the merged kernel's readiness counters (sized for 512 segments)
 size_t ffn_h_bytes(int64_t rows, int32_t d, readme_dtype dt) {
@@ -447,6 +442,51 @@ readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T,
 size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_perm, readme_dtype dt) {
   (void)H;
   return 256 + ffn_ws_bytes(T < 0 ? 0 : T, d_perm < 0 ? 0 : d_perm, dt);
+}
+
+size_t readme_router_workspace_bytes(int64_t T, int32_t nseq) {
+  return router_ws_bytes(T < 0 ? 0 : T, nseq < 1 ? 1 : nseq);
+}
+
+readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
+                                    const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
+                                    void* ws, size_t ws_bytes, readme_stream_t stream) {
+  README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
+  README_CHECK_ARG(nseq >= 1, "nseq must be >= 1");
+  README_CHECK_ARG(w != nullptr, "weights are required");
+  README_CHECK_ARG(w->vocab >= 1, "vocab must be >= 1");
+  if (w->n_experts < 1 || w->n_experts > 16) {
+    set_error("router gating head supports 1..16 experts (got %d)", w->n_experts);
+    return README_ERR_UNSUPPORTED;
+  }
+  README_CHECK_ARG(eps >= 0.f, "eps must be >= 0");
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(token_ids && seq_starts && logits && ws, "null pointer argument");
+  README_CHECK_ARG(w->emb && w->norm1 && w->w_qkv && w->w_o && w->norm2 && w->w_gate && w->w_up && w->w_down &&
+                       w->norm_f && w->w_head,
+                   "null weight pointer");
+  README_CHECK_ARG(aligned16(w->w_qkv) && aligned16(w->w_o) && aligned16(w->w_gate) && aligned16(w->w_up) &&
+                       aligned16(w->w_down) && aligned16(ws),
+                   "projection weights and workspace must be 16-byte aligned");
+  if (ws_bytes < router_ws_bytes(T, nseq)) {
+    set_error("router workspace too small: %zu < %zu", ws_bytes, router_ws_bytes(T, nseq));
+    return README_ERR_WORKSPACE;
+  }
+  RouterWeights rw;
+  rw.vocab = w->vocab;
+  rw.n_experts = w->n_experts;
+  rw.emb = static_cast<const __nv_bfloat16*>(w->emb);
+  rw.g1 = static_cast<const __nv_bfloat16*>(w->norm1);
+  rw.wqkv = static_cast<const __nv_bfloat16*>(w->w_qkv);
+  rw.wo = static_cast<const __nv_bfloat16*>(w->w_o);
+  rw.g2 = static_cast<const __nv_bfloat16*>(w->norm2);
+  rw.wg = static_cast<const __nv_bfloat16*>(w->w_gate);
+  rw.wu = static_cast<const __nv_bfloat16*>(w->w_up);
+  rw.wd = static_cast<const __nv_bfloat16*>(w->w_down);
+  rw.gf = static_cast<const __nv_bfloat16*>(w->norm_f);
+  rw.whead = static_cast<const __nv_bfloat16*>(w->w_head);
+  return launch_router_forward(token_ids, T, seq_starts, nseq, rw, eps, logits, ws, dev_status,
+                               reinterpret_cast<cudaStream_t>(stream));
 }
 
 readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,

@@ -32,6 +32,12 @@ readme_status cuda_fail(cudaError_t e, const char* where);
     if (e_ != cudaSuccess) return ::readme::cuda_fail(e_, #call);      \
   } while (0)
 
+#define README_TRY(expr)            \
+  do {                              \
+    readme_status s_ = (expr);      \
+    if (s_ != README_OK) return s_; \
+  } while (0)
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline size_t dt_size(readme_dtype dt) { return dt == README_BF16 ? 2 : 4; }

@@ -58,4 +58,14 @@ readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, 
                                const int32_t* offsets, const __nv_bfloat16* wd, __nv_bfloat16* out,
                                const int32_t* src, const __nv_bfloat16* residual, cudaStream_t st);
 
+// router.cu: the pre-gating router G (one causal transformer block + gating head), NEXT-1.
+struct RouterWeights {
+  int vocab, n_experts;
+  const __nv_bfloat16 *emb, *g1, *wqkv, *wo, *g2, *wg, *wu, *wd, *gf, *whead;
+};
+size_t router_ws_bytes(int64_t T, int32_t nseq);
+readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
+                                    const RouterWeights& w, float eps, float* logits, void* ws,
+                                    uint32_t* dev_status, cudaStream_t st);
+
 }  // namespace readme

@@ -25,7 +25,7 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
            "readme_build_experts", "readme_permanent_expert_workspace_bytes", "readme_permanent_expert",
-           "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
+           "readme_router_workspace_bytes", "readme_router_forward", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
            "readme_scheduler_next_batch", "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
@@ -74,6 +74,8 @@ _SIGS = {
     "readme_permanent_expert_workspace_bytes": (_sz, [_i64, _i32, _i32, ctypes.c_int]),
     "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
                                                _vp]),
+    "readme_router_workspace_bytes": (_sz, [_i64, _i32]),
+    "readme_router_forward": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -402,3 +404,32 @@ def permanent_expert(x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor, 
     _check("readme_permanent_expert", lib().readme_permanent_expert(
         _ptr(x), _dt(x), T, H, dp, _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(y), _ptr(ws), ws.numel(), st))
     return y
+
+
+class _RouterWeights(ctypes.Structure):
+    _fields_ = [("vocab", ctypes.c_int32), ("n_experts", ctypes.c_int32)] + \
+               [(n, ctypes.c_void_p) for n in ("emb", "norm1", "w_qkv", "w_o", "norm2", "w_gate", "w_up", "w_down",
+                                               "norm_f", "w_head")]
+
+
+ROUTER_KEYS = ("emb", "norm1", "w_qkv", "w_o", "norm2", "w_gate", "w_up", "w_down", "norm_f", "w_head")
+
+
+def router_forward(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: dict, eps: float = 1e-5,
+                   out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                   dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """The pre-gating router G: token ids -> expert logits [T, N] f32 (readme_router_forward). `weights` maps
+    ROUTER_KEYS to bf16 CUDA tensors (nn.Linear [out, in] layouts)."""
+    T = token_ids.numel()
+    nseq = seq_starts.numel() - 1
+    N = weights["w_head"].shape[0]
+    out = out if out is not None else torch.empty((T, N), dtype=torch.float32, device=token_ids.device)
+    need = int(lib().readme_router_workspace_bytes(T, nseq))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=token_ids.device)
+    st = _prep(token_ids, seq_starts, out, ws, dev_status, *[weights[k] for k in ROUTER_KEYS])
+    w = _RouterWeights(weights["emb"].shape[0], N, *[weights[k].data_ptr() for k in ROUTER_KEYS])
+    _check("readme_router_forward", lib().readme_router_forward(
+        _ptr(token_ids), T, _ptr(seq_starts), nseq, ctypes.cast(ctypes.pointer(w), ctypes.c_void_p),
+        ctypes.c_float(eps), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
+    return out

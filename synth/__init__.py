@@ -104,6 +104,34 @@ def neuron_sets(E: int, D: int, d: int, seed: int = MASTER_SEED, mode: str = "ov
     return out
 
 
+def router_weights(vocab: int = 32000, n_experts: int = 8, seed: int = MASTER_SEED, dim: int = 512,
+                   ffn: int = 512) -> dict:
+    """Random-init pre-gating router (table:router_details): embeddings N(0,1), projections
+    N(0, 1/fan_in) in nn.Linear [out, in] layout, RMSNorm weights 1 + 0.1 N(0,1), gating head N(0, 1/dim).
+    float32 numpy arrays (callers round to bf16)."""
+    tid = 200
+    w = {
+        "emb": normal((vocab, dim), seed, tid + 1),
+        "norm1": 1.0 + normal((dim,), seed, tid + 2, std=0.1),
+        "w_qkv": normal((3 * dim, dim), seed, tid + 3, std=1.0 / np.sqrt(dim)),
+        "w_o": normal((dim, dim), seed, tid + 4, std=1.0 / np.sqrt(dim)),
+        "norm2": 1.0 + normal((dim,), seed, tid + 5, std=0.1),
+        "w_gate": normal((ffn, dim), seed, tid + 6, std=1.0 / np.sqrt(dim)),
+        "w_up": normal((ffn, dim), seed, tid + 7, std=1.0 / np.sqrt(dim)),
+        "w_down": normal((dim, ffn), seed, tid + 8, std=1.0 / np.sqrt(ffn)),
+        "norm_f": 1.0 + normal((dim,), seed, tid + 9, std=0.1),
+        "w_head": normal((n_experts, dim), seed, tid + 10, std=1.0 / np.sqrt(dim)),
+    }
+    return {k: v.astype(np.float32) for k, v in w.items()}
+
+
+def token_ids(T: int, vocab: int = 32000, seed: int = MASTER_SEED) -> np.ndarray:
+    """Synthetic token ids, Zipf-like over the vocabulary (a natural-text-like frequency profile)."""
+    g = rng(seed, TID_ASSIGN + 40)
+    r = g.zipf(1.2, size=T)
+    return ((r - 1) % vocab).astype(np.int32)
+
+
 # ---- routing-assignment recipes (the draws; turned into logits below) -------------------------------
 
 def assignments_markov(n_req: int, req_len: int, E: int, p_follow: float = 0.672,

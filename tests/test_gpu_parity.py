@@ -467,3 +467,46 @@ def test_permanent_expert(rd, dt):
     yref, _ = oracle.moe_layer(x, lg, 1, wg, wu, wd)
     yref = yref + oracle.expert_ffn(x, np.array([0, T], np.int32), pg, pu, pd)
     assert rel_err(_np(y), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+# ---- NEXT-1: the pre-gating router G ---------------------------------------------------------------------
+
+def test_router_forward_parity(rd):
+    """readme_router_forward vs the fp64 oracle on ragged sequences (1 token, exact 32-multiples, several
+    query tiles). Logits: bf16 rule. Decisions: identical where the oracle's top-two margin exceeds the
+    measured logit error band; inside the band any expert within the band of the oracle's max is accepted
+    (the north star's near-tie consistency rule, widened to the bf16 error of a router computed on the GPU,
+    reading Q16). The routing plan built from the GPU's own logits is then bit-exact (as in every route test)."""
+    from oracle import router
+    vocab, N = 32000, 8
+    W = {k: synth.to_torch(v, "bf16") for k, v in synth.router_weights(vocab=vocab, n_experts=N, seed=191).items()}
+    lens = [1, 64, 100, 37, 300]
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(starts[-1])
+    ids = synth.token_ids(T, vocab=vocab, seed=192)
+    lg = rd.router_forward(torch.from_numpy(ids).to(DEV), torch.from_numpy(starts).to(DEV),
+                           {k: v.to(DEV) for k, v in W.items()})
+    torch.cuda.synchronize()
+    ref = router.forward(ids, starts, W)
+    got = _np(lg).astype(np.float64)
+    assert rel_err(got, ref) <= BF16_TOL
+    band = 4.0 * np.max(np.abs(got - ref))
+    top = np.sort(ref, axis=1)
+    gpu_ids = got.argmax(axis=1)
+    clear = (top[:, -1] - top[:, -2]) > band
+    assert np.array_equal(gpu_ids[clear], ref.argmax(axis=1)[clear])
+    assert np.all(ref[np.arange(T), gpu_ids] >= top[:, -1] - band)
+    plan = rd.route(lg, 1)
+    _check_plan(plan, oracle.route(lg.cpu(), 1), 1)
+
+
+def test_router_causal_on_gpu(rd):
+    """Appending tokens to a sequence never changes the GPU logits of its prefix (bitwise: the kernels
+    process each query row against keys <= it in a fixed order)."""
+    vocab, N = 32000, 8
+    W = {k: synth.to_torch(v, "bf16").to(DEV) for k, v in synth.router_weights(vocab=vocab, n_experts=N, seed=193).items()}
+    ids = torch.from_numpy(synth.token_ids(200, vocab=vocab, seed=194)).to(DEV)
+    full = rd.router_forward(ids, torch.tensor([0, 200], dtype=torch.int32, device=DEV), W)
+    pre = rd.router_forward(ids[:70].contiguous(), torch.tensor([0, 70], dtype=torch.int32, device=DEV), W)
+    torch.cuda.synchronize()
+    assert rel_err(_np(pre), _np(full[:70])) <= 1e-6

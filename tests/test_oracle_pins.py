@@ -397,3 +397,63 @@ def test_permanent_expert_folds_into_every_expert_Q6():
     pg, pu, pd = oracle.build_experts(wg, wu, wd, P[None, :])
     perm_y = oracle.expert_ffn(x, np.array([0, T], np.int32), pg, pu, pd)
     assert rel_err(base + perm_y, folded) < 1e-12
+
+
+# ---- NEXT-1: the pre-gating router G (oracle.router) ----------------------------------------------------
+
+def _small_router(vocab=300, N=8, seed=161):
+    import torch
+    W = synth.router_weights(vocab=vocab, n_experts=N, seed=seed)
+    return {k: torch.from_numpy(v).to(torch.bfloat16) for k, v in W.items()}
+
+
+def test_router_param_count_matches_paper():
+    """table:router_details: 18.0 M parameters at vocab 32000, dim 512, MLP 512."""
+    from oracle import router
+    W = synth.router_weights(vocab=32000, n_experts=8)
+    n = router.param_count(W)
+    assert abs(n - 18.0e6) / 18.0e6 < 0.02, n
+
+
+def test_router_masked_equals_incremental():
+    """The masked full-sequence evaluation equals a token-by-token evaluation with a growing KV cache
+    (no mask): pins the causal mask, RoPE positions (restart per sequence) and the block wiring."""
+    from oracle import router
+    W = _small_router()
+    ids = synth.token_ids(23, vocab=300, seed=162)
+    starts = np.array([0, 9, 9, 23])  # includes an empty sequence
+    a = router.forward(ids, starts, W)
+    b = router.forward_incremental(ids, starts, W)
+    assert np.max(np.abs(a - b)) < 1e-10
+
+
+def test_router_causal_prefix_invariance():
+    """Appending tokens never changes earlier decisions (causality)."""
+    from oracle import router
+    W = _small_router()
+    ids = synth.token_ids(40, vocab=300, seed=163)
+    full = router.forward(ids, np.array([0, 40]), W)
+    pre = router.forward(ids[:17], np.array([0, 17]), W)
+    assert np.max(np.abs(full[:17] - pre)) < 1e-10
+
+
+def test_rope_invariants():
+    """RoPE: identity at position 0, norm-preserving, and <R(p)q, R(p')k> depends only on p - p'."""
+    from oracle import router
+    g = np.random.default_rng(5)
+    q, k = g.standard_normal((1, 128)), g.standard_normal((1, 128))
+    assert np.array_equal(router.rope(q, np.array([0])), q)
+    r = router.rope(q, np.array([37]))
+    assert abs(np.linalg.norm(r) - np.linalg.norm(q)) < 1e-12
+    d1 = router.rope(q, np.array([10])) @ router.rope(k, np.array([3])).T
+    d2 = router.rope(q, np.array([107])) @ router.rope(k, np.array([100])).T
+    assert abs(d1 - d2).max() < 1e-10
+
+
+def test_router_zero_head_gives_zero_logits():
+    from oracle import router
+    import torch
+    W = _small_router()
+    W["w_head"] = torch.zeros_like(W["w_head"])
+    out = router.forward(synth.token_ids(12, vocab=300, seed=164), np.array([0, 12]), W)
+    assert np.all(out == 0.0)
