@@ -373,6 +373,26 @@ def run_stack(args):
         torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in ms]
     t = float(np.mean(ms))
+    # the pre-gating router G (one causal block + gating head) over the same requests, once per step
+    RW = {kk: synth.to_torch(v, "bf16").to(dev) for kk, v in synth.router_weights(n_experts=E, seed=seed).items()}
+    ids = torch.from_numpy(synth.token_ids(T, seed=seed)).to(dev)
+    starts = torch.arange(0, T + 1, min(T, 4096), dtype=torch.int32, device=dev)
+    r_ws = torch.empty(rd.router_workspace_bytes(T, starts.numel() - 1), dtype=torch.uint8, device=dev)
+    r_out = torch.empty((T, E), dtype=torch.float32, device=dev)
+    rfn = lambda: rd.router_forward(ids, starts, RW, out=r_out, ws=r_ws)
+    for _ in range(args.warmup):
+        rfn()
+    torch.cuda.synchronize()
+    rms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rfn()
+        b.record()
+        rms.append((a, b))
+    torch.cuda.synchronize()
+    router_ms = float(np.mean([a.elapsed_time(b) for a, b in rms]))
     pk, pk_src = peaks()
     flops = L * 6.0 * T * k * H * d
     ach = flops / (t * 1e-3) / 1e12
@@ -383,6 +403,9 @@ def run_stack(args):
             "config": {"workload": "config4_stack32", "T": T, "L": L, "H": H, "E": E, "d": d, "k": k,
                        "routing": "Markov locality p=0.672, routed once per step", "l2": "flushed between steps"},
             "layer_tokens_per_s": T * L / (t * 1e-3),
+            "router": {"ms": router_ms, "share_of_step_with_router": router_ms / (router_ms + t),
+                       "note": "readme_router_forward over the same T tokens (4096-token sequences), run once per "
+                               "request, not per layer; paper: AR router 1.26-1.50 % of step latency (PAPER.md:647)"},
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                          "traffic": None, "algorithmic": f"L*6*T*k*H*d = {flops:.4g} FLOP per step",
                          "peak_source": f"{pk_src} bf16 sustained (a ~80 ms step)"},
