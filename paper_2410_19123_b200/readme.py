@@ -415,6 +415,10 @@ class _RouterWeights(ctypes.Structure):
 ROUTER_KEYS = ("emb", "norm1", "w_qkv", "w_o", "norm2", "w_gate", "w_up", "w_down", "norm_f", "w_head")
 
 
+def router_workspace_bytes(T: int, nseq: int) -> int:
+    return int(lib().readme_router_workspace_bytes(T, nseq))
+
+
 def router_forward(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: dict, eps: float = 1e-5,
                    out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
                    dev_status: torch.Tensor | None = None) -> torch.Tensor:
