@@ -9,8 +9,7 @@
 // theta 10000 on the (i, i+64) halves of each 128-dim head; no biases.
 //
 // Kernels here: the embedding gather + first RMSNorm, a weighted RMSNorm, the causal attention with RoPE
-// applied on the fly (SIMT fp32 flash-style tiles: the router is ~50 GFLOP for 8192 tokens, off the hot
-// path), and the gating head (final RMSNorm + 512 x N dot products per token). The QKV / output / MLP
+// applied on the fly (flash-attention on mma.sync bf16 tensor-core fragments), and the gating head (final RMSNorm + 512 x N dot products per token). The QKV / output / MLP
 // projections are dense contractions and run on the tcgen05 CTA-pair GEMM kernels of ffn_sm100_2cta.cu.
 #include <math.h>
 
@@ -113,126 +112,209 @@ __global__ void router_head_kernel(const __nv_bfloat16* __restrict__ h2, int64_t
   }
 }
 
-// Causal attention with RoPE, per (sequence, head, 32-query tile); K/V streamed in 32-key tiles.
-// qkv [T, 1536] bf16 (q | k | v, head h = columns h*128..), seq_starts [nseq+1] (device), out [T, 512] bf16.
-// Thread (r = tid / 8, s = tid % 8): scores of row r for keys 4s..4s+3 and output dims 16s..16s+15.
-constexpr int kQT = 32, kKT = 32;
+// Causal attention with RoPE on the tensor cores (mma.sync m16n8k16 bf16 -> fp32), flash-attention style:
+// one CTA (4 warps) per (sequence, head, 64-query tile); each warp owns 16 query rows, keeps Q as A
+// fragments, streams 64-key tiles (K with RoPE, V transposed) through shared memory, keeps S = Q K^T and
+// O in registers with an online softmax. ~17 GFLOP per 4096-token request (off the hot path).
+// qkv [T, 1536] bf16 (q | k | v, head h = columns h*128..), out [T, 512] bf16.
+constexpr int kQT = 64, kKT = 64;
+constexpr int kKS = kHd + 8;   // K smem row stride (bf16): conflict-free B-fragment loads
+constexpr int kVS = kKT + 8;   // V^T smem row stride (bf16)
 
-__device__ __forceinline__ void rope_pair(float& lo, float& hi, int pos, int i) {
-  // rotate dims (i, i + 64) of a head by angle pos * theta^(-2i/128)
-  const float inv = exp2f(-static_cast<float>(2 * i) / kHd * log2f(kTheta));
-  float sn, cs;
-  sincosf(static_cast<float>(pos) * inv, &sn, &cs);
-  const float a = lo, b = hi;
-  lo = a * cs - b * sn;
-  hi = b * cs + a * sn;
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) { return pack_bf16x2(lo, hi); }
+
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(256)
+// RoPE applied once per token, in place on the q and k parts of qkv (positions restart per sequence).
+// One warp per token; lane i handles angle pairs i and i + 32 (of 64) for all 4 heads of q and k.
+__global__ void router_rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t T, const int32_t* __restrict__ seq_starts,
+                                   int nseq) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x / kWarp) + threadIdx.x / kWarp;
+  if (t >= T) return;
+  int lo_s = 0, hi_s = nseq;  // find the sequence holding t (binary search on seq_starts)
+  while (hi_s - lo_s > 1) {
+    const int mid = (lo_s + hi_s) / 2;
+    if (seq_starts[mid] <= t) lo_s = mid; else hi_s = mid;
+  }
+  const int pos = static_cast<int>(t - seq_starts[lo_s]);
+  __nv_bfloat16* row = qkv + t * (3 * kD);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = lane + 32 * u;
+    const float inv = exp2f(-static_cast<float>(2 * i) / kHd * log2f(kTheta));
+    float sn, cs;
+    sincosf(static_cast<float>(pos) * inv, &sn, &cs);
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {  // q, k
+#pragma unroll
+      for (int h = 0; h < kHeads; ++h) {
+        __nv_bfloat16* base = row + part * kD + h * kHd;
+        const float a = __bfloat162float(base[i]), b = __bfloat162float(base[i + 64]);
+        base[i] = __float2bfloat16_rn(a * cs - b * sn);
+        base[i + 64] = __float2bfloat16_rn(b * cs + a * sn);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128)
 router_attention_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ seq_starts,
                         const int32_t* __restrict__ tile_seq, const int32_t* __restrict__ tile_q0,
                         const int32_t* __restrict__ ntiles, __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float att_smem[];
-  float(*sQ)[kHd + 1] = reinterpret_cast<float(*)[kHd + 1]>(att_smem);
-  float(*sK)[kHd + 1] = reinterpret_cast<float(*)[kHd + 1]>(att_smem + kQT * (kHd + 1));
-  float(*sV)[kHd] = reinterpret_cast<float(*)[kHd]>(att_smem + (kQT + kKT) * (kHd + 1));
-  float(*sP)[kKT + 1] = reinterpret_cast<float(*)[kKT + 1]>(att_smem + (kQT + kKT) * (kHd + 1) + kKT * kHd);
+  __shared__ __align__(16) __nv_bfloat16 sK[kKT * kKS];      // [key][dim] (also stages Q first)
+  __shared__ __align__(16) __nv_bfloat16 sVt[kHd * kVS];     // [dim][key]
   const int tile = blockIdx.x, head = blockIdx.y;
   if (tile >= *ntiles) return;
   const int seq = tile_seq[tile];
   const int s0 = seq_starts[seq], s1 = seq_starts[seq + 1];
-  const int q0 = tile_q0[tile];  // absolute first query row
+  const int q0 = tile_q0[tile];
   const int nq = min(kQT, s1 - q0);
-  const int tid = threadIdx.x, r = tid / 8, sub = tid % 8;
-  const float scale = rsqrtf(static_cast<float>(kHd));
+  const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
   const int ld = 3 * kD;
+  const float scale_log2 = rsqrtf(static_cast<float>(kHd)) * 1.4426950408889634f;  // softmax in base 2
 
-  // Q tile with RoPE (positions relative to the sequence start)
-  for (int i = tid; i < kQT * (kHd / 2); i += blockDim.x) {
-    const int rr = i / (kHd / 2), c = i % (kHd / 2);
-    float lo = 0.f, hi = 0.f;
-    if (rr < nq) {
-      const int64_t row = q0 + rr;
-      lo = __bfloat162float(qkv[row * ld + head * kHd + c]);
-      hi = __bfloat162float(qkv[row * ld + head * kHd + c + 64]);
-      rope_pair(lo, hi, static_cast<int>(row - s0), c);
-    }
-    sQ[rr][c] = lo * scale;
-    sQ[rr][c + 64] = hi * scale;
+  // ---- Q tile (RoPE already applied) -> smem -> A fragments (16 rows per warp, 8 k-chunks of 16 dims) ----
+  for (int i = tid; i < kQT * (kHd / 8); i += blockDim.x) {
+    const int rr = i / (kHd / 8), c8 = (i % (kHd / 8)) * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (rr < nq) v = *reinterpret_cast<const uint4*>(&qkv[static_cast<int64_t>(q0 + rr) * ld + head * kHd + c8]);
+    *reinterpret_cast<uint4*>(&sK[rr * kKS + c8]) = v;
   }
-  float m_i = -INFINITY, l_i = 0.f;
-  float o[16];
+  __syncthreads();
+  const int r_lo = warp * 16 + lane / 4;  // this thread's two rows: r_lo and r_lo + 8
+  const int cq = (lane % 4) * 2;
+  uint32_t qa[8][4];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) o[j] = 0.f;
+  for (int kc = 0; kc < 8; ++kc) {
+    const int c = kc * 16 + cq;
+    qa[kc][0] = *reinterpret_cast<const uint32_t*>(&sK[r_lo * kKS + c]);
+    qa[kc][1] = *reinterpret_cast<const uint32_t*>(&sK[(r_lo + 8) * kKS + c]);
+    qa[kc][2] = *reinterpret_cast<const uint32_t*>(&sK[r_lo * kKS + c + 8]);
+    qa[kc][3] = *reinterpret_cast<const uint32_t*>(&sK[(r_lo + 8) * kKS + c + 8]);
+  }
+  float o[16][4];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows r_lo, r_lo + 8
+  const int qrow0 = q0 + r_lo, qrow1 = qrow0 + 8;
 
   const int q_last = q0 + nq - 1;
   for (int k0 = s0; k0 <= q_last; k0 += kKT) {
     const int nk = min(kKT, s1 - k0);
-    __syncthreads();
-    for (int i = tid; i < kKT * (kHd / 2); i += blockDim.x) {
-      const int kk = i / (kHd / 2), c = i % (kHd / 2);
-      float lo = 0.f, hi = 0.f, vlo = 0.f, vhi = 0.f;
+    __syncthreads();  // previous tile's smem reads are done
+    for (int i = tid; i < kKT * (kHd / 8); i += blockDim.x) {
+      const int kk = i / (kHd / 8), c8 = (i % (kHd / 8)) * 8;
+      uint4 kv4 = make_uint4(0u, 0u, 0u, 0u), vv4 = make_uint4(0u, 0u, 0u, 0u);
       if (kk < nk) {
         const int64_t row = k0 + kk;
-        lo = __bfloat162float(qkv[row * ld + kD + head * kHd + c]);
-        hi = __bfloat162float(qkv[row * ld + kD + head * kHd + c + 64]);
-        rope_pair(lo, hi, static_cast<int>(row - s0), c);
-        vlo = __bfloat162float(qkv[row * ld + 2 * kD + head * kHd + c]);
-        vhi = __bfloat162float(qkv[row * ld + 2 * kD + head * kHd + c + 64]);
+        kv4 = *reinterpret_cast<const uint4*>(&qkv[row * ld + kD + head * kHd + c8]);
+        vv4 = *reinterpret_cast<const uint4*>(&qkv[row * ld + 2 * kD + head * kHd + c8]);
       }
-      sK[kk][c] = lo;
-      sK[kk][c + 64] = hi;
-      sV[kk][c] = vlo;
-      sV[kk][c + 64] = vhi;
+      *reinterpret_cast<uint4*>(&sK[kk * kKS + c8]) = kv4;
+      const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(&vv4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sVt[(c8 + j) * kVS + kk] = vv[j];
     }
     __syncthreads();
-    // scores for row r, keys 4*sub .. 4*sub+3 (causal: key <= query)
-    float sc[4];
+    // S = Q K^T for this warp's 16 rows x 64 keys (8 n-chunks of 8 keys)
+    float sc[8][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int kk = 4 * sub + j;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < kHd; ++c) acc = fmaf(sQ[r][c], sK[kk][c], acc);
-      const bool ok = r < nq && kk < nk && (k0 + kk) <= (q0 + r);
-      sc[j] = ok ? acc : -INFINITY;
+    for (int nc = 0; nc < 8; ++nc) {
+      sc[nc][0] = sc[nc][1] = sc[nc][2] = sc[nc][3] = 0.f;
+      const int key = nc * 8 + lane / 4;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[key * kKS + kc * 16 + cq]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sK[key * kKS + kc * 16 + cq + 8]);
+        mma_bf16(sc[nc], qa[kc], b0, b1);
+      }
     }
-    float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+    // causal mask + online softmax (rows r_lo / r_lo+8; this thread holds keys nc*8 + cq, +1)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-    for (int off = 4; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float m_new = fmaxf(m_i, mx);
-    const float corr = (m_i == -INFINITY) ? 0.f : expf(m_i - m_new);
-    float ps = 0.f;
+    for (int nc = 0; nc < 8; ++nc) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float p = (sc[j] == -INFINITY) ? 0.f : expf(sc[j] - m_new);
-      sP[r][4 * sub + j] = p;
-      ps += p;
+      for (int j = 0; j < 2; ++j) {
+        const int key = k0 + nc * 8 + cq + j;
+        const bool kv = (nc * 8 + cq + j) < nk;
+        sc[nc][j] = (kv && key <= qrow0) ? sc[nc][j] * scale_log2 : -INFINITY;
+        sc[nc][2 + j] = (kv && key <= qrow1) ? sc[nc][2 + j] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, sc[nc][j]);
+        mx1 = fmaxf(mx1, sc[nc][2 + j]);
+      }
     }
 #pragma unroll
-    for (int off = 4; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-    l_i = l_i * corr + ps;
-    m_i = m_new;
-    __syncwarp();
+    for (int off = 1; off <= 2; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float c0 = (mn0 == -INFINITY) ? 1.f : exp2f(m0 - mn0);
+    const float c1 = (mn1 == -INFINITY) ? 1.f : exp2f(m1 - mn1);
+    float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[j] *= corr;
-    for (int kk = 0; kk < nk; ++kk) {
-      const float p = sP[r][kk];
+    for (int nc = 0; nc < 8; ++nc) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) o[j] = fmaf(p, sV[kk][16 * sub + j], o[j]);
+      for (int j = 0; j < 2; ++j) {
+        sc[nc][j] = (sc[nc][j] == -INFINITY) ? 0.f : exp2f(sc[nc][j] - mn0);
+        sc[nc][2 + j] = (sc[nc][2 + j] == -INFINITY) ? 0.f : exp2f(sc[nc][2 + j] - mn1);
+        ps0 += sc[nc][j];
+        ps1 += sc[nc][2 + j];
+      }
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      ps0 += __shfl_xor_sync(0xffffffffu, ps0, off);
+      ps1 += __shfl_xor_sync(0xffffffffu, ps1, off);
+    }
+    l0 = l0 * c0 + ps0;
+    l1 = l1 * c1 + ps1;
+    m0 = mn0;
+    m1 = mn1;
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      o[n][0] *= c0;
+      o[n][1] *= c0;
+      o[n][2] *= c1;
+      o[n][3] *= c1;
+    }
+    // O += P V: P (16 x 64 keys) as A fragments, V^T rows as B fragments (16 n-chunks of 8 dims)
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      uint32_t pa[4];
+      pa[0] = pack2(sc[2 * kc][0], sc[2 * kc][1]);
+      pa[1] = pack2(sc[2 * kc][2], sc[2 * kc][3]);
+      pa[2] = pack2(sc[2 * kc + 1][0], sc[2 * kc + 1][1]);
+      pa[3] = pack2(sc[2 * kc + 1][2], sc[2 * kc + 1][3]);
+#pragma unroll
+      for (int n = 0; n < 16; ++n) {
+        const int dim = n * 8 + lane / 4;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sVt[dim * kVS + kc * 16 + cq]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sVt[dim * kVS + kc * 16 + cq + 8]);
+        mma_bf16(o[n], pa, b0, b1);
+      }
     }
   }
-  if (r < nq) {
-    const float inv = 1.f / l_i;
-    const int64_t row = q0 + r;
+  // normalise and store rows r_lo, r_lo + 8 (columns n*8 + cq, +1)
+  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) out[row * kD + head * kHd + 16 * sub + j] = __float2bfloat16_rn(o[j] * inv);
+  for (int n = 0; n < 16; ++n) {
+    const int col = head * kHd + n * 8 + cq;
+    if (r_lo < nq)
+      *reinterpret_cast<uint32_t*>(&out[static_cast<int64_t>(qrow0) * kD + col]) = pack2(o[n][0] * i0, o[n][1] * i0);
+    if (r_lo + 8 < nq)
+      *reinterpret_cast<uint32_t*>(&out[static_cast<int64_t>(qrow1) * kD + col]) = pack2(o[n][2] * i1, o[n][3] * i1);
   }
 }
 
 // Query-tile table: for each sequence, ceil(len/32) tiles (seq id, first row). Built on the device.
-constexpr size_t kAttSmem = sizeof(float) * ((kQT + kKT) * (kHd + 1) + kKT * kHd + kQT * (kKT + 1));
-
 __global__ void router_tiles_kernel(const int32_t* __restrict__ seq_starts, int nseq, int32_t* __restrict__ tile_seq,
                                     int32_t* __restrict__ tile_q0, int32_t* __restrict__ ntiles_out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -284,19 +366,13 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   README_CUDA(cudaGetLastError());
   // q | k | v = a . Wqkv^T (tcgen05 CTA-pair GEMM over one segment)
   README_TRY(launch_gemm_2cta(1, a, T, kD, 3 * kD, 1, 1, offs, w.wqkv, nullptr, qkv, nullptr, nullptr, st));
+  router_rope_kernel<<<gblocks, 32 * wpb, 0, st>>>(qkv, T, seq_starts, nseq);
+  README_CUDA(cudaGetLastError());
   router_tiles_kernel<<<1, 1, 0, st>>>(seq_starts, nseq, tile_seq, tile_q0, ntiles);
   README_CUDA(cudaGetLastError());
   const int64_t max_tiles = T / kQT + nseq;
   dim3 ag(static_cast<unsigned>(max_tiles), kHeads);
-  static bool attr_set[64] = {false};
-  int dev = 0;
-  README_CUDA(cudaGetDevice(&dev));
-  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    README_CUDA(cudaFuncSetAttribute(router_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kAttSmem)));
-    attr_set[dev] = true;
-  }
-  router_attention_kernel<<<ag, 256, kAttSmem, st>>>(qkv, seq_starts, tile_seq, tile_q0, ntiles, att);
+  router_attention_kernel<<<ag, 128, 0, st>>>(qkv, seq_starts, tile_seq, tile_q0, ntiles, att);
   README_CUDA(cudaGetLastError());
   // h1 = h0 + att . Wo^T (the residual add fused into the GEMM epilogue)
   README_TRY(launch_gemm_2cta(1, att, T, kD, kD, 1, 1, offs, w.wo, nullptr, h1, nullptr, h0, st));

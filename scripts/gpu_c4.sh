@@ -1,0 +1,5 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+python -m paper_2410_19123_b200.build > gpurun_out/build.log 2>&1
+timeout 900 python bench.py --config 4 --steps 5 --warmup 2 > gpurun_out/bench4.log 2>&1; tail -c 2500 gpurun_out/bench4.log

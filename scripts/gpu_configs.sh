@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 python -m paper_2410_19123_b200.build > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
 run() { local name=$1; shift; local t=$1; shift; timeout $t "$@" > gpurun_out/$name.log 2>&1; echo "$name rc=$?" | tee -a gpurun_out/summary.txt; }
 rm -f gpurun_out/summary.txt
-[ "${TESTS:-1}" = "1" ] && run t_all 1200 python -m pytest tests -m gpu -q && tail -c 600 gpurun_out/t_all.log
+TESTS=0; [ "${TESTS:-1}" = "1" ] && run t_all 1200 python -m pytest tests -m gpu -q && tail -c 600 gpurun_out/t_all.log
 run bench2 600 python bench.py --steps 30 --warmup 5
 run bench1 300 python bench.py --config 1 --steps 50 --warmup 5
 run bench3 600 python bench.py --config 3 --steps 30 --warmup 5

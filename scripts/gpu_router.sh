@@ -2,5 +2,5 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 python -m paper_2410_19123_b200.build > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "router or permanent" 2>&1 | tail -25
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "router" 2>&1 | tail -25
+timeout 900 python bench.py --config 4 --steps 5 --warmup 2 > gpurun_out/bench4.log 2>&1; tail -c 2500 gpurun_out/bench4.log
