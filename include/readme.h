@@ -126,6 +126,17 @@ readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, i
                                  int32_t n_src, const int32_t* offsets, const void* w_down, const int32_t* src,
                                  const void* residual, void* out, readme_stream_t stream);
 
+/* The expert FFN over an expert CACHE (memory-constrained mode, §4.1; NEXT-4): the weights
+ * are slot pools w_gate/w_up [n_slots,d,H], w_down [n_slots,H,d] and expert e's weights sit in slot
+ * expert_slot[e] (DEVICE int32 [E]); only experts with rows are read, so slots of untouched experts may hold
+ * anything. One segment group (n_src = 1). src/residual/out as in readme_expert_down (src == NULL and
+ * residual == NULL: out = y_sorted). bf16 only. ws: readme_expert_ffn_workspace_bytes(...). */
+readme_status readme_expert_ffn_slots(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                      int32_t d, const int32_t* offsets, const int32_t* expert_slot, int32_t n_slots,
+                                      const void* w_gate, const void* w_up, const void* w_down, const int32_t* src,
+                                      const void* residual, void* out, uint32_t* dev_status, void* ws,
+                                      size_t ws_bytes, readme_stream_t stream);
+
 /* a8: combine (Eq. 2's weighted sum):
  *     y[t] = residual[t] + sum_{j<k} topk_w[t,j] * y_sorted[dest[t*k+j]]   (j ascending, fp32, Q8)
  * topk_w is nullable iff k == 1 (weight 1); residual [T,H] nullable. With k == 1 and no residual the
@@ -232,6 +243,21 @@ void readme_scheduler_destroy(readme_scheduler* s);
 readme_status readme_scheduler_push(readme_scheduler* s, const int64_t* token_ids, const int32_t* experts, int64_t n);
 int64_t readme_scheduler_queued(readme_scheduler* s, int32_t e); /* e = -1: all queues */
 int64_t readme_scheduler_next_batch(readme_scheduler* s, int64_t max_tokens, int64_t* token_ids, int32_t* experts);
+
+/* Host runtime: the expert cache of the memory-constrained mode (§4.1). `capacity` slots;
+ * policy 0 = LRU, 1 = Belady-inspired (evict argmax_{e in C} F(e,t), the resident whose next access after t
+ * is farthest, never-again first; PAPER.md:208 — requires the pre-gated future reference string from
+ * readme_cache_set_future), 2 = Random (seeded). Ties go to the lowest key (reading Q17). Keys are int64
+ * (layer * E + expert). readme_cache_access returns 1 on a hit, 0 on a miss (the key is then resident, in the
+ * slot of the evicted key if the cache was full; *evicted = that key or -1), -1 on a bad argument; *slot =
+ * the key's slot in [0, capacity). Host-only, thread-safe. */
+typedef struct readme_expert_cache readme_expert_cache;
+readme_expert_cache* readme_cache_create(int32_t capacity, int32_t policy, uint64_t seed);
+void readme_cache_destroy(readme_expert_cache* c);
+readme_status readme_cache_set_future(readme_expert_cache* c, const int64_t* keys, const int64_t* times, int64_t n);
+int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int64_t* evicted, int32_t* slot);
+int32_t readme_cache_lookup(readme_expert_cache* c, int64_t key); /* slot or -1 */
+void readme_cache_stats(readme_expert_cache* c, int64_t* hits, int64_t* misses);
 
 /* Helpers. */
 /* The library links its own (static) CUDA runtime: bind the calling host thread to `device` before

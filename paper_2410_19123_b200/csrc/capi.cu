@@ -260,6 +260,34 @@ readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t r
 
 
 
+readme_status readme_expert_ffn_slots(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
+                                      int32_t d, const int32_t* offsets, const int32_t* expert_slot, int32_t n_slots,
+                                      const void* w_gate, const void* w_up, const void* w_down, const int32_t* src,
+                                      const void* residual, void* out, uint32_t* dev_status, void* ws,
+                                      size_t ws_bytes, readme_stream_t stream) {
+  README_TRY(check_ffn_args(dt, rows, H, E, d, 1, offsets));
+  if (dt != README_BF16) {
+    set_error("readme_expert_ffn_slots is bf16-only");
+    return README_ERR_UNSUPPORTED;
+  }
+  README_CHECK_ARG(expert_slot != nullptr && n_slots >= 1, "expert_slot and n_slots >= 1 are required");
+  if (rows == 0) return README_OK;
+  README_CHECK_ARG(x_sorted && w_gate && w_up && w_down && out && ws, "null pointer argument");
+  README_CHECK_ARG(aligned16(x_sorted) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) &&
+                       aligned16(out) && aligned16(ws) && (!residual || aligned16(residual)),
+                   "all tensors must be 16-byte aligned");
+  if (ws_bytes < ffn_ws_bytes(rows, d, dt)) {
+    set_error("expert_ffn_slots workspace too small: %zu < %zu", ws_bytes, ffn_ws_bytes(rows, d, dt));
+    return README_ERR_WORKSPACE;
+  }
+  uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt));
+  return launch_ffn_layer_2cta(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, E, offsets,
+                               static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
+                               static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(ws),
+                               static_cast<__nv_bfloat16*>(out), src, static_cast<const __nv_bfloat16*>(residual),
+                               ready, dev_status, reinterpret_cast<cudaStream_t>(stream), expert_slot, n_slots);
+}
+
 readme_status readme_combine(const void* y_sorted, readme_dtype dt, int64_t T, int32_t H, int32_t k,
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
                              uint32_t* dev_status, readme_stream_t stream) {

@@ -358,6 +358,7 @@ struct LayerArgs {
   uint32_t* ready;           // [#m-tiles] zeroed before the launch
   uint32_t* dev_status;
   Fuse fz;
+  const int32_t* expert_slot;  // nullable: expert e's weights live at slot expert_slot[e] of the weight pools
 };
 
 struct LTile {
@@ -467,7 +468,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     int g1 = 0, g2 = 0;
     for (int t = pair; t < ntiles; t += npairs) {
       const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
-      const int e = tl.g % E;
+      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
       const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
@@ -707,7 +708,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                     const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
-                                    uint32_t* ready, uint32_t* dev_status, cudaStream_t st) {
+                                    uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
+                                    const int32_t* expert_slot, int32_t n_slots) {
   if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
@@ -716,9 +718,10 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
   CUtensorMap mX, mG, mU, mH, mD;
-  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, E, kBK, 64) &&
-            tc::make_map_3d(&mU, wu, H, d, E, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
-            tc::make_map_3d(&mD, wd, d, H, E, kBK, 64);
+  const int32_t EW = expert_slot ? n_slots : E;  // outer extent of the weight tensors
+  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, 64) &&
+            tc::make_map_3d(&mU, wu, H, d, EW, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
+            tc::make_map_3d(&mD, wd, d, H, EW, kBK, 64);
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
     return README_ERR_CUDA;
@@ -728,7 +731,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   const int pairs = num_sms() / 2;
   const int64_t tiles = mt_ub * ((d + 127) / 128 + (H + 255) / 256);
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0}};
+  LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
+               expert_slot};
   if (src || residual)
     ffn_layer2_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
   else

@@ -27,7 +27,9 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_build_experts", "readme_permanent_expert_workspace_bytes", "readme_permanent_expert",
            "readme_router_workspace_bytes", "readme_router_forward", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
-           "readme_scheduler_next_batch", "readme_set_device", "readme_status_string", "readme_last_error",
+           "readme_scheduler_next_batch", "readme_expert_ffn_slots", "readme_cache_create", "readme_cache_destroy",
+           "readme_cache_set_future", "readme_cache_access", "readme_cache_lookup", "readme_cache_stats",
+           "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
 
 
@@ -76,6 +78,14 @@ _SIGS = {
                                                _vp]),
     "readme_router_workspace_bytes": (_sz, [_i64, _i32]),
     "readme_router_forward": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
+    "readme_expert_ffn_slots": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
+                                               _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "readme_cache_create": (_vp, [_i32, _i32, ctypes.c_uint64]),
+    "readme_cache_destroy": (None, [_vp]),
+    "readme_cache_set_future": (ctypes.c_int, [_vp, _vp, _vp, _i64]),
+    "readme_cache_access": (_i32, [_vp, _i64, _i64, _vp, _vp]),
+    "readme_cache_lookup": (_i32, [_vp, _i64]),
+    "readme_cache_stats": (None, [_vp, _vp, _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -437,3 +447,63 @@ def router_forward(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: d
         _ptr(token_ids), T, _ptr(seq_starts), nseq, ctypes.cast(ctypes.pointer(w), ctypes.c_void_p),
         ctypes.c_float(eps), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
     return out
+
+
+def expert_ffn_slots(x_sorted: torch.Tensor, offsets: torch.Tensor, expert_slot: torch.Tensor, w_gate: torch.Tensor,
+                     w_up: torch.Tensor, w_down: torch.Tensor, E: int, src: torch.Tensor | None = None,
+                     residual: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """Expert FFN over slot pools (readme_expert_ffn_slots): expert e's weights at slot expert_slot[e]."""
+    rows, H = x_sorted.shape
+    S, d, _ = w_gate.shape
+    if out is None:
+        out = torch.empty((rows, H), dtype=x_sorted.dtype, device=x_sorted.device)
+    need = expert_ffn_workspace_bytes(rows, H, E, d, x_sorted.dtype)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x_sorted.device)
+    st = _prep(x_sorted, offsets, expert_slot, w_gate, w_up, w_down, src, residual, out, ws, dev_status)
+    _check("readme_expert_ffn_slots", lib().readme_expert_ffn_slots(
+        _ptr(x_sorted), _dt(x_sorted), rows, H, E, d, _ptr(offsets), _ptr(expert_slot), S, _ptr(w_gate),
+        _ptr(w_up), _ptr(w_down), _ptr(src), _ptr(residual), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
+    return out
+
+
+class ExpertCache:
+    """Expert cache policy in the native runtime (readme_cache_*): LRU, Belady (pre-gated future), Random."""
+    POLICIES = {"lru": 0, "belady": 1, "random": 2}
+
+    def __init__(self, capacity: int, policy: str, seed: int = 0):
+        self._h = lib().readme_cache_create(capacity, self.POLICIES[policy], seed)
+        if not self._h:
+            raise ValueError("readme_cache_create failed")
+        self.capacity = capacity
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().readme_cache_destroy(h)
+            self._h = None
+
+    def set_future(self, keys, times):
+        import numpy as np
+        k = np.ascontiguousarray(keys, dtype=np.int64)
+        t = np.ascontiguousarray(times, dtype=np.int64)
+        _check("readme_cache_set_future", lib().readme_cache_set_future(
+            self._h, k.ctypes.data_as(ctypes.c_void_p), t.ctypes.data_as(ctypes.c_void_p), k.size))
+
+    def access(self, key: int, t: int):
+        """Returns (hit: bool, slot: int, evicted: int or -1)."""
+        ev = ctypes.c_int64(-1)
+        sl = ctypes.c_int32(-1)
+        r = lib().readme_cache_access(self._h, key, t, ctypes.byref(ev), ctypes.byref(sl))
+        if r < 0:
+            raise ValueError("readme_cache_access: bad argument")
+        return bool(r), int(sl.value), int(ev.value)
+
+    def lookup(self, key: int) -> int:
+        return int(lib().readme_cache_lookup(self._h, key))
+
+    def stats(self):
+        h, m = ctypes.c_int64(0), ctypes.c_int64(0)
+        lib().readme_cache_stats(self._h, ctypes.byref(h), ctypes.byref(m))
+        return int(h.value), int(m.value)

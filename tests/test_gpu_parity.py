@@ -510,3 +510,26 @@ def test_router_causal_on_gpu(rd):
     pre = rd.router_forward(ids[:70].contiguous(), torch.tensor([0, 70], dtype=torch.int32, device=DEV), W)
     torch.cuda.synchronize()
     assert rel_err(_np(pre), _np(full[:70])) <= 1e-6
+
+
+# ---- NEXT-4: memory-constrained mode (expert cache + prefetch) ----------------------------------------
+
+@pytest.mark.parametrize("policy,prefetch,cap", [("belady", True, 3), ("lru", False, 3), ("belady", True, 8),
+                                                  ("random", True, 4)])
+def test_offloaded_stack_equals_resident_stack(rd, policy, prefetch, cap):
+    """Experts streamed from pinned host memory through a small device cache give exactly the same result
+    as the all-resident route-once stack (readme_moe_stack): the cache only moves weights."""
+    from paper_2410_19123_b200.offload import OffloadedStack
+    T, H, d, E, L = 512, 256, 256, 8, 4
+    x = synth.to_torch(synth.tokens(T, H, seed=201), "bf16").to(DEV)
+    ids = synth.assignments_unique(T, 3, E, seed=202)
+    lg = torch.from_numpy(synth.logits_for_assignments(ids, E, seed=203)).to(DEV)
+    layers = [tuple(synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=204, layer=l))
+              for l in range(L)]
+    ref, _ = rd.moe_stack(x.clone(), [tuple(w.to(DEV) for w in ly) for ly in layers], logits=lg)
+    host = [tuple(w.pin_memory() for w in ly) for ly in layers]
+    st = OffloadedStack(host, cap, policy, DEV)
+    y, stats = st.forward(x.clone(), lg, prefetch=prefetch)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref)
+    assert stats["hits"] + stats["misses"] == L * 3
