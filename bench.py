@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tokens", type=int, default=None, help="override T per rank")
     ap.add_argument("--eager", action="store_true", help="time eager calls instead of CUDA-graph replays")
+    ap.add_argument("--offload", action="store_true",
+                    help="config 4 in the memory-constrained mode (NEXT-4): experts in pinned host memory")
     return ap.parse_args()
 
 
@@ -413,6 +415,131 @@ def run_stack(args):
     print(json.dumps(line), flush=True)
 
 
+def run_offload(args):
+    """Config 4, memory-constrained mode (NEXT-4 of SURVEY §8(f)): the experts of
+    L layers live in pinned host memory and only `cap` expert slots fit on the device. A queue of Q pre-gated
+    batches (T tokens each, u experts per batch as expert-aware batching yields them) runs through the L
+    layers; the makespan of the queue is timed with CUDA events for fine-grained prefetching (next step's
+    experts load on a separate stream while this step computes) vs on-demand loading, under the
+    Belady-inspired and LRU caches. Plus the paper's cache-hit table setup (Table tab:cache-hit): n_req
+    concurrent decode requests sharing one expert cache of k = 2..5 slots (per layer), Markov locality p=0.672."""
+    import torch
+
+    import synth
+    from paper_2410_19123_b200 import readme as rd
+    from paper_2410_19123_b200.offload import OffloadedStack
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = dict(synth.CONFIGS[4])
+    H, d, E = cfg["H"], cfg["d"], cfg["E"]
+    L, Q, u = 8, 8, 2
+    T = args.tokens or 8192
+    seed = synth.MASTER_SEED + 40
+    host = []
+    for l in range(L):
+        ws = synth.expert_weights_device(E, d, H, dev, seed=seed, layer=l)
+        host.append(tuple(w.cpu().pin_memory() for w in ws))
+        del ws
+    torch.cuda.empty_cache()
+    x0s, lgs, touched = [], [], []
+    for b in range(Q):
+        ids = synth.assignments_unique(T, u, E, seed=seed + 100 + b)
+        lgs.append(torch.from_numpy(synth.logits_for_assignments(ids, E, seed=seed + 200 + b)).to(dev))
+        x0s.append(synth.to_torch(synth.tokens(T, H, seed=seed + 300 + b), "bf16").to(dev))
+        touched.append(sorted(set(ids.tolist())))
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    expert_bytes = 3 * d * H * 2
+    runs = []
+    with Clocks(0) as clk:
+        for cap in (4, 8, 16):
+            for policy in ("belady", "lru"):
+                st = OffloadedStack(host, cap, policy, dev)
+                for prefetch in (True, False):
+                    ms = []
+                    for it in range(args.warmup + args.steps):
+                        batches = [(x.clone(), lg) for x, lg in zip(x0s, lgs)]
+                        flush.zero_()
+                        torch.cuda.synchronize()
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record()
+                        _, stats = st.run(batches, prefetch=prefetch)
+                        b.record()
+                        torch.cuda.synchronize()
+                        if it >= args.warmup:
+                            ms.append(a.elapsed_time(b))
+                    t = float(np.mean(ms))
+                    runs.append({"cap_slots": cap, "policy": policy, "prefetch": prefetch, "ms": t,
+                                 "tokens_per_s": Q * T / (t * 1e-3), "hit_ratio": stats["hit_ratio"],
+                                 "misses": stats["misses"], "h2d_GBps": stats["bytes_loaded"] / (t * 1e-3) / 1e9})
+                del st
+                torch.cuda.empty_cache()
+    for r in runs:
+        if r["prefetch"]:
+            od = next(q for q in runs if q["cap_slots"] == r["cap_slots"] and q["policy"] == r["policy"]
+                      and not q["prefetch"])
+            r["latency_reduction_vs_on_demand"] = 1.0 - r["ms"] / od["ms"]
+    # the same Q batches with all L*E experts resident (readme_moe_stack per batch): the floor
+    dev_layers = [tuple(w.to(dev) for w in ly) for ly in host]
+    res_ms = []
+    for it in range(args.warmup + args.steps):
+        xs = [x.clone() for x in x0s]
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for xb, lg in zip(xs, lgs):
+            rd.moe_stack(xb, dev_layers, logits=lg)
+        b.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            res_ms.append(a.elapsed_time(b))
+    resident_ms = float(np.mean(res_ms))
+    del dev_layers
+    # H2D copy bandwidth of one expert from pinned memory (the load stream's roofline)
+    src = torch.cat([w[0].reshape(-1) for w in host[0]]).pin_memory()
+    slot = torch.empty_like(src, device=dev)
+    h2d = []
+    for it in range(8):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        slot.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            h2d.append(a.elapsed_time(b))
+    h2d_GBps = expert_bytes / (float(np.median(h2d)) * 1e-3) / 1e9
+    # Table tab:cache-hit setup: n_req concurrent decode requests share one (per-layer) expert cache
+    n_req, n_tok = 8, 512
+    chains = synth.assignments_markov(n_req, n_tok, E, 0.672, seed=seed + 500).reshape(n_req, n_tok)
+    trace = chains.T.reshape(-1).astype(np.int64)  # decode step by step, request by request
+    table = {}
+    for k in (2, 3, 4, 5):
+        row = {}
+        for policy in ("random", "lru", "belady"):
+            c = rd.ExpertCache(k, policy, seed=1)
+            c.set_future(trace, np.arange(trace.size))
+            for t, key in enumerate(trace.tolist()):
+                c.access(key, t)
+            h, m = c.stats()
+            row[policy] = h / (h + m)
+        table[str(k)] = row
+    best = max((r for r in runs if r["prefetch"]), key=lambda r: r["tokens_per_s"])
+    line = {"metric": "memory-constrained MoE stack tokens/s (experts in host memory, NEXT-4)",
+            "value": best["tokens_per_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": best["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config4_offload", "Q_batches": Q, "T": T, "L": L, "H": H, "E": E, "d": d,
+                       "experts_per_batch": u, "host_expert_bytes": L * E * expert_bytes,
+                       "routing": "expert-aware batches (u experts each), routed once per batch",
+                       "l2": "flushed between steps"},
+            "runs": runs, "resident_ms": resident_ms, "h2d_expert_GBps": h2d_GBps,
+            "cache_hit_table": {"setup": f"{n_req} concurrent decode requests x {n_tok} tokens, Markov p=0.672, "
+                                         f"E={E}, one layer's cache of k slots (PAPER.md Table tab:cache-hit)",
+                                "hit_ratio": table},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -423,6 +550,9 @@ def main():
         return
     if args.config == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         run_tiny(args)
+        return
+    if args.config == 4 and args.offload and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        run_offload(args)
         return
     if args.config == 4 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
         run_stack(args)

@@ -249,13 +249,16 @@ int64_t readme_scheduler_next_batch(readme_scheduler* s, int64_t max_tokens, int
  * is farthest, never-again first; PAPER.md:208 — requires the pre-gated future reference string from
  * readme_cache_set_future), 2 = Random (seeded). Ties go to the lowest key (reading Q17). Keys are int64
  * (layer * E + expert). readme_cache_access returns 1 on a hit, 0 on a miss (the key is then resident, in the
- * slot of the evicted key if the cache was full; *evicted = that key or -1), -1 on a bad argument; *slot =
- * the key's slot in [0, capacity). Host-only, thread-safe. */
+ * slot of the evicted key if the cache was full; *evicted = that key or -1), -1 on a bad argument, -2 if the
+ * cache is full of protected keys; *slot = the key's slot in [0, capacity). Residents last accessed at or
+ * after `protect_since` are never evicted (the experts of the layer being assembled; pass INT64_MAX for none).
+ * Host-only, thread-safe. */
 typedef struct readme_expert_cache readme_expert_cache;
 readme_expert_cache* readme_cache_create(int32_t capacity, int32_t policy, uint64_t seed);
 void readme_cache_destroy(readme_expert_cache* c);
 readme_status readme_cache_set_future(readme_expert_cache* c, const int64_t* keys, const int64_t* times, int64_t n);
-int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int64_t* evicted, int32_t* slot);
+int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int64_t protect_since, int64_t* evicted,
+                            int32_t* slot);
 int32_t readme_cache_lookup(readme_expert_cache* c, int64_t key); /* slot or -1 */
 void readme_cache_stats(readme_expert_cache* c, int64_t* hits, int64_t* misses);
 

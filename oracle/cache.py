@@ -16,8 +16,12 @@ def _splitmix64(state):
     return state, z ^ (z >> 31)
 
 
-def simulate(trace, capacity, policy, seed=0):
-    """trace: list of keys accessed at times 0..n-1. Returns (hits, misses, [(t, hit, evicted)])."""
+def simulate(trace, capacity, policy, seed=0, protect_since=None):
+    """trace: list of keys accessed at times 0..n-1. Returns (hits, misses, [(t, hit, evicted)]).
+    protect_since (optional, one int per access): a resident last accessed at or after protect_since[t] is not
+    a candidate for eviction at time t — the experts of the layer being assembled must all be resident when it
+    runs (reading Q18). If no resident is a candidate, the access raises (the caller sized the
+    cache below one layer's experts)."""
     resident, last, log = [], {}, []
     rng = seed
     hits = misses = 0
@@ -31,6 +35,10 @@ def simulate(trace, capacity, policy, seed=0):
         ev = -1
         if len(resident) >= capacity:
             res = sorted(resident)
+            if protect_since is not None:
+                res = [k for k in res if last[k] < protect_since[t]]
+                if not res:
+                    raise ValueError("every resident expert is protected")
             if policy == "lru":
                 ev = min(res, key=lambda k: (last[k], k))
             elif policy == "belady":

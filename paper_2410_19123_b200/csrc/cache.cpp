@@ -73,7 +73,8 @@ readme_status readme_cache_set_future(readme_expert_cache* c, const int64_t* key
   return README_OK;
 }
 
-int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int64_t* evicted, int32_t* slot) {
+int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int64_t protect_since, int64_t* evicted,
+                            int32_t* slot) {
   if (!c) return -1;
   std::lock_guard<std::mutex> g(c->mu);
   if (evicted) *evicted = -1;
@@ -93,7 +94,12 @@ int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int6
     // choose the victim among the residents, deterministically (ties -> lowest key)
     std::vector<int64_t> res;
     res.reserve(c->slot_of.size());
-    for (const auto& kv : c->slot_of) res.push_back(kv.first);
+    for (const auto& kv : c->slot_of)
+      if (c->last_use[kv.first] < protect_since) res.push_back(kv.first);  // keys in use are not evictable
+    if (res.empty()) {
+      --c->misses;
+      return -2;
+    }
     std::sort(res.begin(), res.end());
     int64_t victim = res[0];
     if (c->policy == 0) {  // LRU: least recently accessed

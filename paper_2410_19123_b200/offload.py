@@ -55,56 +55,83 @@ class OffloadedStack:
         self.bytes_loaded += 3 * self.d * self.H * 2
 
     def forward(self, x: torch.Tensor, logits: torch.Tensor, prefetch: bool = True):
-        """x [T,H] bf16 (updated in place through all L layers), logits [T,E]. Returns (x, stats)."""
-        T, H = x.shape
-        E = self.E
-        cache = rd.ExpertCache(self.cap, self.policy, seed=7)
-        plan = rd.route(logits, 1)
-        counts = plan.counts.cpu().numpy()  # the one host sync per batch: pre-gating fixes every layer
-        touched = [e for e in range(E) if counts[e] > 0]
-        refs = [l * E + e for l in range(self.L) for e in touched]
-        cache.set_future(refs, np.arange(len(refs)))
-        xs = torch.empty_like(x)
-        ws = torch.empty(rd.expert_ffn_workspace_bytes(T, H, E, self.d, x.dtype), dtype=torch.uint8, device=self.dev)
-        slot_tables = []
-        t = 0
-        comp = torch.cuda.current_stream(self.dev)
+        """One batch: x [T,H] bf16 (updated in place through all L layers), logits [T,E]. Returns (x, stats)."""
+        out, stats = self.run([(x, logits)], prefetch=prefetch)
+        return out[0], stats
 
-        def ensure(l):
-            nonlocal t
+    def run(self, batches, prefetch: bool = True, policy: str | None = None):
+        """Serve a queue of batches [(x, logits), ...] through the L layers. All batches are pre-gated first
+        (route once each; one host read of the counts for the whole queue), so the cache knows the exact future
+        reference string of (layer, expert) accesses across batches. Every layer waits only
+        for its own experts; with `prefetch`, the loads of the next (batch, layer) step are issued while the
+        current one computes; without it, a step's loads start after the previous step ends."""
+        E = self.E
+        cache = rd.ExpertCache(self.cap, policy or self.policy, seed=7)
+        plans = [rd.route(lg, 1) for (_x, lg) in batches]
+        counts = torch.stack([p.counts for p in plans]).cpu().numpy()
+        touched = [[e for e in range(E) if c[e] > 0] for c in counts]
+        steps = [(b, l) for b in range(len(batches)) for l in range(self.L)]
+        refs = [l * E + e for (b, l) in steps for e in touched[b]]
+        cache.set_future(refs, np.arange(len(refs)))
+        comp = torch.cuda.current_stream(self.dev)
+        self.slot_ready = [None] * self.cap
+        self.slot_free = [None] * self.cap
+        self.bytes_loaded = 0
+        state = {"t": 0, "prev_first": 0}
+
+        def ensure(step):
+            """Cache decisions for one (batch, layer) step, in order. Its own experts are protected once placed;
+            with prefetch the step still computing (the previous one) is protected too, so a prefetch copy never
+            has to wait for that step to release a slot — unless the cache cannot hold both steps' experts, in
+            which case that access falls back to protecting this step only (the copy then waits, slot_free)."""
+            b, l = step
             table = np.zeros(E, np.int32)
-            for e in touched:
-                hit, slot, _ev = cache.access(l * E + e, t)
-                t += 1
+            first = state["t"]
+            guard = state["prev_first"] if prefetch else first
+            for e in touched[b]:
+                try:
+                    hit, slot, _ev = cache.access(l * E + e, state["t"], protect_since=guard)
+                except RuntimeError:
+                    hit, slot, _ev = cache.access(l * E + e, state["t"], protect_since=first)
+                state["t"] += 1
                 if not hit:
                     self._load(l * E + e, slot)
                 table[e] = slot
+            state["prev_first"] = first
             return table
 
+        work = []
+        for (x, _lg), plan in zip(batches, plans):
+            T, H = x.shape
+            work.append((torch.empty_like(x), torch.empty(rd.expert_ffn_workspace_bytes(T, H, E, self.d, x.dtype),
+                                                          dtype=torch.uint8, device=self.dev)))
         tables = {}
         prev_done = None
-        for l in range(self.L):
-            if l == 0 or not prefetch:
-                if prev_done is not None:  # on demand: a layer's loads start only after the previous layer
+        for i, (b, l) in enumerate(steps):
+            if i == 0 or not prefetch:
+                if prev_done is not None:  # on demand: this step's loads start only after the previous step
                     self.load_stream.wait_event(prev_done)
-                tables[l] = ensure(l)
-            table = tables.pop(l)
-            for e in touched:
+                tables[i] = ensure((b, l))
+            table = tables.pop(i)
+            for e in touched[b]:
                 comp.wait_event(self.slot_ready[int(table[e])])
             slot_of = torch.from_numpy(table).pin_memory().to(self.dev, non_blocking=True)
-            slot_tables.append(slot_of)
+            x = batches[b][0]
+            xs, ws = work[b]
+            plan = plans[b]
             rd.dispatch_rmsnorm(x, plan.dest, 1, eps=self.eps, out=xs)
             rd.expert_ffn_slots(xs, plan.offsets, slot_of, self.pool_g, self.pool_u, self.pool_d, E, src=plan.src,
                                 residual=x, out=x, ws=ws)
             done = torch.cuda.Event()
             done.record(comp)
             prev_done = done
-            for e in touched:
+            for e in touched[b]:
                 self.slot_free[int(table[e])] = done
-            if prefetch and l + 1 < self.L:
-                # issued right after layer l is enqueued: copies into free slots overlap layer l's compute;
-                # a copy that evicts one of layer l's slots waits for layer l (slot_free) first.
-                tables[l + 1] = ensure(l + 1)
+            if prefetch and i + 1 < len(steps):
+                # issued right after step i is enqueued: copies into free slots overlap its compute; a copy that
+                # evicts one of step i's slots waits for step i (slot_free) first.
+                tables[i + 1] = ensure(steps[i + 1])
         hits, misses = cache.stats()
-        return x, {"hits": hits, "misses": misses, "hit_ratio": hits / max(1, hits + misses),
-                   "touched_experts": len(touched), "bytes_loaded": self.bytes_loaded}
+        return [b[0] for b in batches], {"hits": hits, "misses": misses, "hit_ratio": hits / max(1, hits + misses),
+                                         "touched_experts": [len(t) for t in touched],
+                                         "bytes_loaded": self.bytes_loaded}

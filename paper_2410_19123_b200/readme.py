@@ -83,7 +83,7 @@ _SIGS = {
     "readme_cache_create": (_vp, [_i32, _i32, ctypes.c_uint64]),
     "readme_cache_destroy": (None, [_vp]),
     "readme_cache_set_future": (ctypes.c_int, [_vp, _vp, _vp, _i64]),
-    "readme_cache_access": (_i32, [_vp, _i64, _i64, _vp, _vp]),
+    "readme_cache_access": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "readme_cache_lookup": (_i32, [_vp, _i64]),
     "readme_cache_stats": (None, [_vp, _vp, _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
@@ -491,11 +491,14 @@ class ExpertCache:
         _check("readme_cache_set_future", lib().readme_cache_set_future(
             self._h, k.ctypes.data_as(ctypes.c_void_p), t.ctypes.data_as(ctypes.c_void_p), k.size))
 
-    def access(self, key: int, t: int):
-        """Returns (hit: bool, slot: int, evicted: int or -1)."""
+    def access(self, key: int, t: int, protect_since: int = 2 ** 63 - 1):
+        """Returns (hit: bool, slot: int, evicted: int or -1). Residents accessed at or after protect_since are
+        not evictable."""
         ev = ctypes.c_int64(-1)
         sl = ctypes.c_int32(-1)
-        r = lib().readme_cache_access(self._h, key, t, ctypes.byref(ev), ctypes.byref(sl))
+        r = lib().readme_cache_access(self._h, key, t, protect_since, ctypes.byref(ev), ctypes.byref(sl))
+        if r == -2:
+            raise RuntimeError("expert cache full of protected experts: capacity below one layer's working set")
         if r < 0:
             raise ValueError("readme_cache_access: bad argument")
         return bool(r), int(sl.value), int(ev.value)

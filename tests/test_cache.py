@@ -75,3 +75,86 @@ def test_native_cache_matches_oracle(rd, policy):
             slots[key] = slot
         hits, misses = c.stats()
         assert hits + misses == n
+
+
+# ---- protect_since: the experts of the step being assembled are never evicted (reading Q18) -------------
+
+def _step_trace(g, E, L, B, u):
+    """Accesses of B batches x L layers; each batch touches u experts (same in every layer); the protect
+    boundary of an access is the first access of its (batch, layer) step."""
+    trace, prot = [], []
+    for _b in range(B):
+        ex = sorted(g.choice(E, u, replace=False).tolist())
+        for l in range(L):
+            start = len(trace)
+            for e in ex:
+                trace.append(l * E + e)
+                prot.append(start)
+    return trace, prot
+
+
+def _optimal_protected(trace, cap, prot):
+    """Max hits over every eviction sequence that never evicts a protected resident (exhaustive)."""
+    from functools import lru_cache
+    trace = tuple(trace)
+
+    @lru_cache(maxsize=None)
+    def best(t, res):  # res: sorted tuple of (key, last access)
+        if t == len(trace):
+            return 0
+        key = trace[t]
+        if key in [r[0] for r in res]:
+            return 1 + best(t + 1, tuple(sorted([r for r in res if r[0] != key] + [(key, t)])))
+        if len(res) < cap:
+            return best(t + 1, tuple(sorted(res + ((key, t),))))
+        return max(best(t + 1, tuple(sorted([r for r in res if r != v] + [(key, t)])))
+                   for v in res if v[1] < prot[t])
+
+    return best(0, ())
+
+
+def test_protected_belady_is_optimal_on_step_traces():
+    g = np.random.default_rng(11)
+    for _ in range(150):
+        u = int(g.integers(1, 3))
+        tr, prot = _step_trace(g, int(g.integers(3, 6)), int(g.integers(1, 3)), int(g.integers(1, 4)), u)
+        cap = int(g.integers(u, u + 3))
+        assert cache.simulate(tr, cap, "belady", protect_since=prot)[0] == _optimal_protected(tr, cap, prot)
+
+
+@pytest.mark.parametrize("policy", ["lru", "belady", "random"])
+def test_protect_keeps_the_step_resident(policy):
+    g = np.random.default_rng(12)
+    for trial in range(60):
+        u = int(g.integers(1, 4))
+        tr, prot = _step_trace(g, 8, int(g.integers(1, 4)), int(g.integers(1, 5)), u)
+        _, _, log = cache.simulate(tr, u, policy, seed=trial, protect_since=prot)  # capacity = one step
+        for t, (_t, _hit, ev) in enumerate(log):
+            assert ev not in tr[prot[t]:t]  # never evicts an expert this step already placed
+        # with no protection boundary in force (protect_since = t + 1 protects nothing) the rule is unchanged
+        free = [t + 1 for t in range(len(tr))]
+        assert cache.simulate(tr, u + 1, policy, seed=trial, protect_since=free) == \
+            cache.simulate(tr, u + 1, policy, seed=trial)
+
+
+@pytest.mark.parametrize("policy", ["lru", "belady", "random"])
+def test_native_cache_protect_matches_oracle(rd, policy):
+    g = np.random.default_rng(13)
+    for trial in range(40):
+        u = int(g.integers(1, 4))
+        tr, prot = _step_trace(g, 8, int(g.integers(1, 5)), int(g.integers(1, 6)), u)
+        cap = int(g.integers(u, u + 4))
+        _, _, log = cache.simulate(tr, cap, policy, seed=trial, protect_since=prot)
+        c = rd.ExpertCache(cap, policy, seed=trial)
+        c.set_future(np.array(tr, np.int64), np.arange(len(tr)))
+        for t, key in enumerate(tr):
+            hit, _slot, ev = c.access(key, t, protect_since=prot[t])
+            assert (hit, ev) == (log[t][1], log[t][2])
+
+
+def test_native_cache_all_protected_raises(rd):
+    c = rd.ExpertCache(2, "lru")
+    c.access(1, 0, protect_since=0)
+    c.access(2, 1, protect_since=0)
+    with pytest.raises(RuntimeError):
+        c.access(3, 2, protect_since=0)

@@ -533,3 +533,38 @@ def test_offloaded_stack_equals_resident_stack(rd, policy, prefetch, cap):
     torch.cuda.synchronize()
     assert torch.equal(y, ref)
     assert stats["hits"] + stats["misses"] == L * 3
+
+
+@pytest.mark.parametrize("policy,prefetch", [("belady", True), ("lru", True), ("belady", False)])
+def test_offloaded_queue_matches_resident_and_cache_oracle(rd, policy, prefetch):
+    """A queue of pre-gated batches through the offloaded stack: every batch's output equals the resident
+    stack's, and the hit/miss count equals the oracle cache simulation of the same reference string with the
+    protection boundary (oracle/cache.py, reading Q18): the current step, plus the previous one with prefetch."""
+    from oracle import cache as ocache
+    from paper_2410_19123_b200.offload import OffloadedStack
+    T, H, d, E, L, B, cap = 384, 256, 256, 8, 3, 4, 6
+    layers = [tuple(synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=214, layer=l))
+              for l in range(L)]
+    dev_layers = [tuple(w.to(DEV) for w in ly) for ly in layers]
+    batches, refs, trace, prot = [], [], [], []
+    prev = 0
+    for b in range(B):
+        x = synth.to_torch(synth.tokens(T, H, seed=220 + b), "bf16").to(DEV)
+        ids = synth.assignments_unique(T, 2 + b % 2, E, seed=230 + b)
+        lg = torch.from_numpy(synth.logits_for_assignments(ids, E, seed=240 + b)).to(DEV)
+        refs.append(rd.moe_stack(x.clone(), dev_layers, logits=lg)[0])
+        batches.append((x.clone(), lg))
+        ex = sorted(set(ids.reshape(-1).tolist()))
+        for l in range(L):
+            start = len(trace)
+            for e in ex:  # prefetch also protects the step still computing (cap 6 >= two steps of <= 3 experts)
+                trace.append(l * E + e)
+                prot.append(prev if prefetch else start)
+            prev = start
+    st = OffloadedStack([tuple(w.pin_memory() for w in ly) for ly in layers], cap, policy, DEV)
+    outs, stats = st.run(batches, prefetch=prefetch)
+    torch.cuda.synchronize()
+    for y, r in zip(outs, refs):
+        assert torch.equal(y, r)
+    hits, misses, _ = ocache.simulate(trace, cap, policy, protect_since=prot)
+    assert (stats["hits"], stats["misses"]) == (hits, misses)
