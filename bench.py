@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tokens", type=int, default=None, help="override T per rank")
     ap.add_argument("--eager", action="store_true", help="time eager calls instead of CUDA-graph replays")
+    ap.add_argument("--ep", default="peer", choices=["peer", "nccl"],
+                    help="N>1 expert parallelism: all-to-alls fused into the kernels over peer memory (default) "
+                         "or NCCL all_to_all_single between the library's kernels")
     ap.add_argument("--offload", action="store_true",
                     help="config 4 in the memory-constrained mode (NEXT-4): experts in pinned host memory")
     return ap.parse_args()
@@ -567,7 +570,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # README_BENCH_BACKEND=gloo lets several ranks share one GPU (a functional check of the N>1 path only:
+        # their kernels time-slice, so the numbers mean nothing)
+        backend = os.environ.get("README_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            local = local % torch.cuda.device_count()
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)} if backend == "nccl" else {}))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = dict(synth.CONFIGS[args.config if world == 1 else 5])
@@ -591,8 +599,15 @@ def main():
 
     if world > 1:
         from paper_2410_19123_b200 import ep
-        layer = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
-        step_fn = layer.step
+        if args.ep == "peer":
+            layer, lg_ep = ep.PeerEPLayer.from_config(cfg, T, dist.group.WORLD, dev)
+
+            def step_fn():  # route once (+ count exchange on the device), then the fused layer
+                layer.route(lg_ep)
+                layer.layer(residual=True)
+        else:
+            layer = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
+            step_fn = layer.step
     else:
         inp = make_inputs(cfg, T, rank, dev)
         eg, eu, ed = inp["w"]
@@ -678,6 +693,9 @@ def main():
             "config": {"workload": (f"config{args.config}_{cfg['name']}" if world == 1 else "config5_expert_parallel"),
                        "T_per_gpu": T, "H": H, "D": cfg["D"], "E": E, "d": d, "k": k,
                        "parallelism": "single" if world == 1 else f"ep{world}",
+                       **({} if world == 1 else {"ep_exchange": "peer-memory stores fused into the dispatch kernel "
+                                                 "and the down-GEMM epilogue" if args.ep == "peer" else
+                                                 "NCCL all_to_all_single"}),
                        "l2": "flushed between timed steps (256 MiB write)"}}
     if world == 1:
         med = lambda a: float(np.median(a))
@@ -716,7 +734,9 @@ def main():
                        "standalone entry (inside readme_moe_layer, k=1, it is fused into the down GEMM epilogue)"}
         line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + finalize/dispatch + expert FFN (+combine)
     else:
-        line["gpu_launches"] = None
+        # peer: route, finalize, publish, (signal, wait) x3, plan, dispatch, FFN = 12; nccl: route, finalize,
+        # dispatch, FFN, combine (+ NCCL's own kernels)
+        line["gpu_launches"] = (12 if args.ep == "peer" else 5) * args.steps
     line["clocks"] = clk.summary()
 
     if world == 1 and not args.no_e2e:
@@ -747,6 +767,8 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        if args.ep == "peer":
+            layer.close()
         dist.destroy_process_group()
 
 

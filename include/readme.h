@@ -61,6 +61,7 @@ typedef enum { README_F32 = 0, README_BF16 = 1 } readme_dtype;
 #define README_DEV_NONFINITE_LOGIT 0x1u /* some logit was NaN/Inf (Q3: NaN ranks as -inf) */
 #define README_DEV_BAD_INDEX 0x2u       /* a caller-supplied plan held an id/row out of range */
 #define README_DEV_SCHED_TIMEOUT 0x4u   /* the single-launch expert FFN could not co-schedule its CTA pairs */
+#define README_DEV_EP_TIMEOUT 0x8u      /* readme_ep_wait gave up on a peer (~10 s) instead of hanging */
 
 #define README_MAX_EXPERTS 256
 
@@ -261,6 +262,67 @@ int32_t readme_cache_access(readme_expert_cache* c, int64_t key, int64_t t, int6
                             int32_t* slot);
 int32_t readme_cache_lookup(readme_expert_cache* c, int64_t key); /* slot or -1 */
 void readme_cache_stats(readme_expert_cache* c, int64_t* hits, int64_t* misses);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Expert parallelism over peer memory (stretch C4). G <= README_EP_MAX_RANKS ranks, one
+ * process per GPU, experts contiguous per rank (rank q owns [q*E/G, (q+1)*E/G)), tokens data-parallel.
+ * Instead of NCCL all-to-alls, rows move by stores into the peer's memory: the dispatch kernel writes each
+ * token row into the owning rank's receive buffer, and the down projection's epilogue writes each result
+ * row back into its source rank's output (+ the source's residual) — the combine all-to-all fused into
+ * the GEMM. Ranks order the phases with flag words (release/acquire at system scope). Because pre-gating
+ * fixes every token's expert for all layers, counts are exchanged once per batch
+ * (readme_ep_publish_counts + readme_ep_plan) and each layer is: readme_ep_dispatch, readme_ep_signal,
+ * readme_ep_wait, readme_ep_expert_ffn, readme_ep_signal, readme_ep_wait (k == 1; for k > 1 the rows
+ * return into the source's y_sorted and a local readme_combine follows). Nothing here synchronises the
+ * host; every call is stream-ordered and graph-capturable.
+ * Every buffer another rank writes or reads must come from readme_ep_alloc and be mapped into that rank with
+ * readme_ipc_handle / readme_ipc_open (CUDA IPC; peer access enabled lazily). "peer_*" arguments are HOST
+ * arrays of G DEVICE pointers, entry q = rank q's buffer as mapped in this process (entry me = own). */
+#define README_EP_MAX_RANKS 8
+#define README_IPC_HANDLE_BYTES 64
+readme_status readme_ep_alloc(size_t bytes, void** ptr); /* zero-filled device memory on the current device */
+readme_status readme_ep_free(void* ptr);
+readme_status readme_ipc_handle(const void* ptr, void* handle); /* handle: README_IPC_HANDLE_BYTES host bytes */
+readme_status readme_ipc_open(const void* handle, void** ptr);  /* a handle from another process */
+readme_status readme_ipc_close(void* ptr);
+/* Phase flags: peer_flags[q] -> rank q's uint64 [G] flag array for this phase; epoch -> this rank's uint64
+ * counter for the phase (device memory, zero-initialised, private to the rank). readme_ep_signal bumps
+ * *epoch and sets peer_flags[q][me] = *epoch for every q (release, system scope) after all earlier work on
+ * `stream`; readme_ep_wait blocks `stream` until flags[p] >= *epoch for every p (acquire), or sets
+ * README_DEV_EP_TIMEOUT after ~10 s instead of hanging. The epoch is read on the device, so a CUDA graph
+ * of a whole layer replays correctly. */
+readme_status readme_ep_signal(uint64_t* const* peer_flags, int32_t G, int32_t me, uint64_t* epoch,
+                               readme_stream_t stream);
+readme_status readme_ep_wait(const uint64_t* flags, int32_t G, const uint64_t* epoch, uint32_t* dev_status,
+                             readme_stream_t stream);
+/* Once per batch: counts [E] (this rank's readme_route histogram) -> peer_tables[q][me*E + e] for every q
+ * (each table int32 [G][E]); signal + wait, then readme_ep_plan turns the complete table into
+ * seg_offsets [G*E/G + 1] (this rank's receive layout: segment (source p, local expert el), source-major, so
+ * each expert's rows arrive in global token order — P12) and row_base [E] (where this rank's rows for
+ * global expert e start in the owner's receive buffer). E % G == 0 required. */
+readme_status readme_ep_publish_counts(const int32_t* counts, int32_t E, int32_t* const* peer_tables, int32_t G,
+                                       int32_t me, readme_stream_t stream);
+readme_status readme_ep_plan(const int32_t* table, int32_t G, int32_t E, int32_t me, int32_t* seg_offsets,
+                             int32_t* row_base, readme_stream_t stream);
+/* a5 fused with the dispatch all-to-all: slot s = t*k + j with sorted row r = dest[s] of expert e (offsets:
+ * this rank's readme_route offsets [E+1]) is stored to rank q = e/(E/G) at row row_base[e] + r - offsets[e]
+ * of peer_x[q] ([rows_cap, H] of dt), and peer_map[q][that row] = me*vrows + (to_token ? t : r): where the
+ * result must return (to_token = 1 with vrows = T for k == 1; to_token = 0 with vrows = T*k for k > 1).
+ * Out-of-range dest entries set README_DEV_BAD_INDEX and are skipped. */
+readme_status readme_ep_dispatch(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                 const int32_t* dest, const int32_t* offsets, const int32_t* row_base, int32_t E,
+                                 int32_t G, int32_t me, void* const* peer_x, int32_t* const* peer_map,
+                                 int64_t vrows, int32_t to_token, uint32_t* dev_status, readme_stream_t stream);
+/* a6 + a7 (+ a8) fused with the combine all-to-all (bf16): the grouped SwiGLU FFN over this rank's receive
+ * buffer x_recv [rows_cap, H] (segments from seg_offsets [G*E_local+1], expert g % E_local), whose result
+ * row r is stored to peer_out[p] + i*H (+ peer_res[p] + i*H when peer_res and its entry are non-NULL),
+ * with v = row_map[r], p = v / vrows, i = v % vrows. Weights as readme_expert_ffn (E_local experts).
+ * ws: readme_expert_ffn_workspace_bytes(rows_cap, H, E_local, d, dt). */
+readme_status readme_ep_expert_ffn(const void* x_recv, readme_dtype dt, int64_t rows_cap, int32_t H,
+                                   int32_t E_local, int32_t d, int32_t G, const int32_t* seg_offsets,
+                                   const void* w_gate, const void* w_up, const void* w_down, const int32_t* row_map,
+                                   void* const* peer_out, const void* const* peer_res, int64_t vrows,
+                                   uint32_t* dev_status, void* ws, size_t ws_bytes, readme_stream_t stream);
 
 /* Helpers. */
 /* The library links its own (static) CUDA runtime: bind the calling host thread to `device` before

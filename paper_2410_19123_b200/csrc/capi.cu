@@ -529,5 +529,141 @@ readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w
                               w_down, dev_status, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// ---- expert parallelism over peer memory (ep.cu) ----------------------------------------------------
+
+readme_status readme_ep_alloc(size_t bytes, void** ptr) {
+  README_CHECK_ARG(ptr != nullptr && bytes > 0, "ptr required, bytes > 0");
+  *ptr = nullptr;
+  README_CUDA(cudaMalloc(ptr, bytes));
+  cudaError_t e = cudaMemset(*ptr, 0, bytes);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return cuda_fail(e, "cudaMemset(ep arena)");
+  }
+  return README_OK;
+}
+
+readme_status readme_ep_free(void* ptr) {
+  if (ptr) README_CUDA(cudaFree(ptr));
+  return README_OK;
+}
+
+readme_status readme_ipc_handle(const void* ptr, void* handle) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == README_IPC_HANDLE_BYTES, "IPC handle size");
+  README_CHECK_ARG(ptr && handle, "ptr and handle are required");
+  cudaIpcMemHandle_t h;
+  README_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+  memcpy(handle, &h, sizeof(h));
+  return README_OK;
+}
+
+readme_status readme_ipc_open(const void* handle, void** ptr) {
+  README_CHECK_ARG(ptr && handle, "ptr and handle are required");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  *ptr = nullptr;
+  README_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return README_OK;
+}
+
+readme_status readme_ipc_close(void* ptr) {
+  if (ptr) README_CUDA(cudaIpcCloseMemHandle(ptr));
+  return README_OK;
+}
+
+namespace {
+readme_status check_peers(const void* const* v, int32_t G) {
+  README_CHECK_ARG(G >= 1 && G <= README_EP_MAX_RANKS, "G must be in [1, %d]", README_EP_MAX_RANKS);
+  README_CHECK_ARG(v != nullptr, "peer pointer array is required");
+  for (int i = 0; i < G; ++i) README_CHECK_ARG(v[i] != nullptr, "peer pointer %d is NULL", i);
+  return README_OK;
+}
+}  // namespace
+
+readme_status readme_ep_signal(uint64_t* const* peer_flags, int32_t G, int32_t me, uint64_t* epoch,
+                               readme_stream_t stream) {
+  README_TRY(check_peers(reinterpret_cast<const void* const*>(peer_flags), G));
+  README_CHECK_ARG(me >= 0 && me < G && epoch != nullptr, "me out of range or epoch missing");
+  return launch_ep_signal(peer_flags, G, me, epoch, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_ep_wait(const uint64_t* flags, int32_t G, const uint64_t* epoch, uint32_t* dev_status,
+                             readme_stream_t stream) {
+  README_CHECK_ARG(flags != nullptr && epoch != nullptr && G >= 1 && G <= README_EP_MAX_RANKS,
+                   "flags and epoch required, G in [1, 8]");
+  return launch_ep_wait(flags, G, epoch, dev_status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_ep_publish_counts(const int32_t* counts, int32_t E, int32_t* const* peer_tables, int32_t G,
+                                       int32_t me, readme_stream_t stream) {
+  README_TRY(check_peers(reinterpret_cast<const void* const*>(peer_tables), G));
+  README_CHECK_ARG(counts && E >= 1 && E <= README_MAX_EXPERTS && E % G == 0 && me >= 0 && me < G,
+                   "need counts, E in [1, 256] divisible by G, 0 <= me < G");
+  return launch_ep_publish(counts, E, peer_tables, G, me, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_ep_plan(const int32_t* table, int32_t G, int32_t E, int32_t me, int32_t* seg_offsets,
+                             int32_t* row_base, readme_stream_t stream) {
+  README_CHECK_ARG(table && seg_offsets && row_base, "table, seg_offsets and row_base are required");
+  README_CHECK_ARG(G >= 1 && G <= README_EP_MAX_RANKS && E >= 1 && E <= README_MAX_EXPERTS && E % G == 0 &&
+                       me >= 0 && me < G,
+                   "need G in [1, 8], E in [1, 256] divisible by G, 0 <= me < G");
+  return launch_ep_plan(table, G, E, me, seg_offsets, row_base, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_ep_dispatch(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t k,
+                                 const int32_t* dest, const int32_t* offsets, const int32_t* row_base, int32_t E,
+                                 int32_t G, int32_t me, void* const* peer_x, int32_t* const* peer_map,
+                                 int64_t vrows, int32_t to_token, uint32_t* dev_status, readme_stream_t stream) {
+  README_TRY(check_rows(dt, H));
+  README_CHECK_ARG(T >= 0 && k >= 1 && T * static_cast<int64_t>(k) < (int64_t(1) << 31), "bad T/k");
+  README_CHECK_ARG(E >= 1 && E <= README_MAX_EXPERTS && G >= 1 && E % G == 0 && me >= 0 && me < G,
+                   "need E in [1, 256] divisible by G and 0 <= me < G");
+  README_CHECK_ARG(vrows >= (to_token ? T : T * k) && vrows * G < (int64_t(1) << 31), "vrows out of range");
+  if (T == 0) return README_OK;
+  README_TRY(check_peers(peer_x, G));
+  README_TRY(check_peers(reinterpret_cast<const void* const*>(peer_map), G));
+  README_CHECK_ARG(x && dest && offsets && row_base && aligned16(x), "x (16-byte aligned), dest, offsets, row_base");
+  for (int i = 0; i < G; ++i) README_CHECK_ARG(aligned16(peer_x[i]), "peer_x must be 16-byte aligned");
+  return launch_ep_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, dest, offsets, row_base, E, G, me,
+                            peer_x, peer_map, vrows, to_token, dev_status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_ep_expert_ffn(const void* x_recv, readme_dtype dt, int64_t rows_cap, int32_t H,
+                                   int32_t E_local, int32_t d, int32_t G, const int32_t* seg_offsets,
+                                   const void* w_gate, const void* w_up, const void* w_down, const int32_t* row_map,
+                                   void* const* peer_out, const void* const* peer_res, int64_t vrows,
+                                   uint32_t* dev_status, void* ws, size_t ws_bytes, readme_stream_t stream) {
+  README_TRY(check_ffn_args(dt, rows_cap, H, E_local, d, G, seg_offsets));
+  if (dt != README_BF16) {
+    set_error("readme_ep_expert_ffn is bf16-only");
+    return README_ERR_UNSUPPORTED;
+  }
+  if (rows_cap == 0) return README_OK;
+  README_TRY(check_peers(peer_out, G));
+  README_CHECK_ARG(x_recv && w_gate && w_up && w_down && row_map && ws, "null pointer argument");
+  README_CHECK_ARG(vrows >= 1 && vrows * G < (int64_t(1) << 31), "vrows out of range");
+  README_CHECK_ARG(aligned16(x_recv) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(ws),
+                   "all tensors must be 16-byte aligned");
+  if (ws_bytes < ffn_ws_bytes(rows_cap, d, dt)) {
+    set_error("ep_expert_ffn workspace too small: %zu < %zu", ws_bytes, ffn_ws_bytes(rows_cap, d, dt));
+    return README_ERR_WORKSPACE;
+  }
+  PeerOut po{};
+  for (int i = 0; i < G; ++i) {
+    po.y[i] = static_cast<__nv_bfloat16*>(peer_out[i]);
+    po.res[i] = peer_res ? static_cast<const __nv_bfloat16*>(peer_res[i]) : nullptr;
+  }
+  po.npeer = G;
+  po.vrows = vrows;
+  uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows_cap, d, dt));
+  return launch_ffn_layer_2cta(static_cast<const __nv_bfloat16*>(x_recv), rows_cap, H, E_local, d, G * E_local,
+                               seg_offsets, static_cast<const __nv_bfloat16*>(w_gate),
+                               static_cast<const __nv_bfloat16*>(w_up), static_cast<const __nv_bfloat16*>(w_down),
+                               static_cast<__nv_bfloat16*>(ws), nullptr, row_map, nullptr, ready, dev_status,
+                               reinterpret_cast<cudaStream_t>(stream), nullptr, 0, &po);
+}
+
 }  // extern "C"
 #pragma GCC visibility pop

@@ -359,6 +359,13 @@ struct LayerArgs {
   uint32_t* dev_status;
   Fuse fz;
   const int32_t* expert_slot;  // nullable: expert e's weights live at slot expert_slot[e] of the weight pools
+  // kFuse == 2 (expert parallelism over peer memory): received row r came from rank p = v / vrows as its
+  // row i = v % vrows (v = fz.src[r]); the down epilogue stores it straight into that rank's output,
+  // peer_y[p] + i*H, adding peer_res[p] + i*H when non-null — the combine all-to-all fused into the GEMM.
+  __nv_bfloat16* peer_y[kMaxPeers];
+  const __nv_bfloat16* peer_res[kMaxPeers];
+  int npeer;
+  int64_t vrows;
 };
 
 struct LTile {
@@ -592,12 +599,31 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       } else {
         int64_t orow_idx = r;
         bool valid_row = valid;
-        if constexpr (kFuse == 1) {
-          orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
-          valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
+        __nv_bfloat16* orow;
+        const __nv_bfloat16* rrow = nullptr;
+        if constexpr (kFuse == 2) {
+          const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
+          valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
+          const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
+          const int64_t i = valid_row ? v - p * la.vrows : 0;
+          __nv_bfloat16* py = la.peer_y[0];
+          const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+          for (int j = 1; j < kMaxPeers; ++j)
+            if (p == j) {
+              py = la.peer_y[j];
+              pr = la.peer_res[j];
+            }
+          orow = py + i * H;
+          rrow = pr ? pr + i * H : nullptr;
+        } else {
+          if constexpr (kFuse == 1) {
+            orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
+            valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
+          }
+          orow = la.y + orow_idx * H;
+          rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
         }
-        __nv_bfloat16* orow = la.y + orow_idx * H;
-        const __nv_bfloat16* rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
         for (int w = 0; w < n_windows; ++w) {
           const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
 #pragma unroll 1
@@ -633,6 +659,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     }
   }
 
+  if constexpr (kFuse == 2) __threadfence_system();  // remote rows performed before the ready signal
   tc::fence_before();
   __syncthreads();
   tc::cluster_sync();
@@ -647,13 +674,14 @@ readme_status set_smem_attr() {
   README_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) dev = 0;
   std::call_once(once[dev], [&] {
-    const void* fns[5] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
+    const void* fns[6] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>),
                           reinterpret_cast<const void*>(ffn_layer2_kernel<0>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1>)};
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<2>)};
     err[dev] = cudaSuccess;
-    for (int i = 0; i < 5 && err[dev] == cudaSuccess; ++i)
+    for (int i = 0; i < 6 && err[dev] == cudaSuccess; ++i)
       err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   });
   if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
@@ -709,7 +737,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
-                                    const int32_t* expert_slot, int32_t n_slots) {
+                                    const int32_t* expert_slot, int32_t n_slots, const PeerOut* peers) {
   if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
@@ -732,8 +760,20 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   const int64_t tiles = mt_ub * ((d + 127) / 128 + (H + 255) / 256);
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
-               expert_slot};
-  if (src || residual)
+               expert_slot, {}, {}, 0, 0};
+  if (peers) {
+    if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
+      set_error("expert FFN remote scatter: need 1..%d peers, vrows >= 1 and a row map", kMaxPeers);
+      return README_ERR_INVALID_ARG;
+    }
+    for (int j = 0; j < peers->npeer; ++j) {
+      la.peer_y[j] = peers->y[j];
+      la.peer_res[j] = peers->res[j];
+    }
+    la.npeer = peers->npeer;
+    la.vrows = peers->vrows;
+    ffn_layer2_kernel<2><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
+  } else if (src || residual)
     ffn_layer2_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
   else
     ffn_layer2_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);

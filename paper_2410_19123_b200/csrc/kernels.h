@@ -44,14 +44,36 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
                                const __nv_bfloat16* B1, __nv_bfloat16* out, const int32_t* src,
                                const __nv_bfloat16* residual, cudaStream_t st);
 // a6 + a7 (+ a8 when src != null, k == 1) in one persistent CTA-pair launch; `ready` is a device scratch of
-// ffn_layer_ready_bytes() bytes (zeroed by the launcher).
+// ffn_layer_ready_bytes() bytes (zeroed by the launcher). With `peers`, received row r is stored to rank
+// p's output (peer memory) as described on LayerArgs (expert parallelism, ep.cu).
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  __nv_bfloat16* y[kMaxPeers];
+  const __nv_bfloat16* res[kMaxPeers];
+  int npeer;
+  int64_t vrows;
+};
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg);
+
+// Expert parallelism over peer memory (ep.cu).
+readme_status launch_ep_signal(uint64_t* const* peer_flags, int G, int me, uint64_t* epoch, cudaStream_t st);
+readme_status launch_ep_wait(const uint64_t* flags, int G, const uint64_t* epoch, uint32_t* dev_status,
+                             cudaStream_t st);
+readme_status launch_ep_publish(const int32_t* counts, int E, int32_t* const* peer_tables, int G, int me,
+                                cudaStream_t st);
+readme_status launch_ep_plan(const int32_t* table, int G, int E, int me, int32_t* seg_offsets, int32_t* row_base,
+                             cudaStream_t st);
+readme_status launch_ep_dispatch(const void* x, size_t row_bytes, int64_t T, int k, const int32_t* dest,
+                                 const int32_t* offsets, const int32_t* row_base, int E, int G, int me,
+                                 void* const* peer_x, int32_t* const* peer_map, int64_t vrows, int to_token,
+                                 uint32_t* dev_status, cudaStream_t st);
 readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                     int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                     const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
-                                    const int32_t* expert_slot = nullptr, int32_t n_slots = 0);
+                                    const int32_t* expert_slot = nullptr, int32_t n_slots = 0,
+                                    const PeerOut* peers = nullptr);
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                   const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);

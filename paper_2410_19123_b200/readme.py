@@ -29,6 +29,9 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
            "readme_scheduler_next_batch", "readme_expert_ffn_slots", "readme_cache_create", "readme_cache_destroy",
            "readme_cache_set_future", "readme_cache_access", "readme_cache_lookup", "readme_cache_stats",
+           "readme_ep_alloc", "readme_ep_free", "readme_ipc_handle", "readme_ipc_open", "readme_ipc_close",
+           "readme_ep_signal", "readme_ep_wait", "readme_ep_publish_counts", "readme_ep_plan", "readme_ep_dispatch",
+           "readme_ep_expert_ffn",
            "readme_set_device", "readme_status_string", "readme_last_error",
            "readme_version")
 
@@ -86,6 +89,19 @@ _SIGS = {
     "readme_cache_access": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "readme_cache_lookup": (_i32, [_vp, _i64]),
     "readme_cache_stats": (None, [_vp, _vp, _vp]),
+    "readme_ep_alloc": (ctypes.c_int, [_sz, _vp]),
+    "readme_ep_free": (ctypes.c_int, [_vp]),
+    "readme_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "readme_ipc_open": (ctypes.c_int, [_vp, _vp]),
+    "readme_ipc_close": (ctypes.c_int, [_vp]),
+    "readme_ep_signal": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
+    "readme_ep_wait": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp]),
+    "readme_ep_publish_counts": (ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _vp]),
+    "readme_ep_plan": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "readme_ep_dispatch": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _i32, _vp,
+                                          _vp, _i64, _i32, _vp, _vp]),
+    "readme_ep_expert_ffn": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                                            _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "readme_set_device": (ctypes.c_int, [ctypes.c_int]),
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
@@ -510,3 +526,114 @@ class ExpertCache:
         h, m = ctypes.c_int64(0), ctypes.c_int64(0)
         lib().readme_cache_stats(self._h, ctypes.byref(h), ctypes.byref(m))
         return int(h.value), int(m.value)
+
+
+# ---- expert parallelism over peer memory (readme_ep_*, readme_ipc_*) ----------------------------------
+
+IPC_HANDLE_BYTES = 64
+
+
+def _ptrs(v):
+    """Host array of device pointers (ints) for the peer_* arguments."""
+    return (ctypes.c_void_p * len(v))(*[None if p is None else int(p) for p in v])
+
+
+def _stream_for(device=None):
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    if getattr(_tls, "dev", None) != dev:
+        _check("readme_set_device", lib().readme_set_device(dev))
+        _tls.dev = dev
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def ep_alloc(nbytes: int, device=None) -> int:
+    """Zero-filled device memory owned by the library (IPC-exportable); returns the device pointer."""
+    _stream_for(device)
+    p = ctypes.c_void_p()
+    _check("readme_ep_alloc", lib().readme_ep_alloc(nbytes, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ep_free(ptr: int):
+    _check("readme_ep_free", lib().readme_ep_free(ctypes.c_void_p(ptr)))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check("readme_ipc_handle", lib().readme_ipc_handle(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device=None) -> int:
+    _stream_for(device)
+    p = ctypes.c_void_p()
+    _check("readme_ipc_open", lib().readme_ipc_open(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES),
+                                                    ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    _check("readme_ipc_close", lib().readme_ipc_close(ctypes.c_void_p(ptr)))
+
+
+class _CAI:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {torch.bfloat16: "<V2", torch.int32: "<i4", torch.int64: "<i8", torch.float32: "<f4",
+            torch.uint8: "|u1"}
+
+
+def device_view(ptr: int, shape, dtype, device) -> torch.Tensor:
+    """A torch tensor over library-owned device memory (no copy)."""
+    if dtype == torch.bfloat16:  # no bf16 typestr in the interface: view int16 storage as bf16
+        return torch.as_tensor(_CAI(ptr, shape, "<i2"), device=device).view(torch.bfloat16)
+    return torch.as_tensor(_CAI(ptr, shape, _TYPESTR[dtype]), device=device)
+
+
+def ep_signal(peer_flags, me: int, epoch: int, device=None):
+    """epoch: device pointer to this rank's uint64 phase counter."""
+    st = _stream_for(device)
+    _check("readme_ep_signal", lib().readme_ep_signal(_ptrs(peer_flags), len(peer_flags), me,
+                                                      ctypes.c_void_p(epoch), st))
+
+
+def ep_wait(flags: int, G: int, epoch: int, dev_status: torch.Tensor | None = None, device=None):
+    st = _stream_for(device)
+    _check("readme_ep_wait", lib().readme_ep_wait(ctypes.c_void_p(flags), G, ctypes.c_void_p(epoch),
+                                                  _ptr(dev_status), st))
+
+
+def ep_publish_counts(counts: torch.Tensor, peer_tables, me: int):
+    st = _prep(counts)
+    _check("readme_ep_publish_counts", lib().readme_ep_publish_counts(_ptr(counts), counts.numel(),
+                                                                      _ptrs(peer_tables), len(peer_tables), me, st))
+
+
+def ep_plan(table: int, G: int, E: int, me: int, seg_offsets: torch.Tensor, row_base: torch.Tensor):
+    st = _prep(seg_offsets, row_base)
+    _check("readme_ep_plan", lib().readme_ep_plan(ctypes.c_void_p(table), G, E, me, _ptr(seg_offsets),
+                                                  _ptr(row_base), st))
+
+
+def ep_dispatch(x: torch.Tensor, k: int, dest, offsets, row_base, E: int, me: int, peer_x, peer_map, vrows: int,
+                to_token: bool, dev_status: torch.Tensor | None = None):
+    st = _prep(x, dest, offsets, row_base, dev_status)
+    T, H = x.shape
+    _check("readme_ep_dispatch", lib().readme_ep_dispatch(
+        _ptr(x), _dt(x), T, H, k, _ptr(dest), _ptr(offsets), _ptr(row_base), E, len(peer_x), me, _ptrs(peer_x),
+        _ptrs(peer_map), vrows, int(bool(to_token)), _ptr(dev_status), st))
+
+
+def ep_expert_ffn(x_recv: torch.Tensor, seg_offsets, w_gate, w_up, w_down, row_map, peer_out, peer_res, vrows: int,
+                  ws: torch.Tensor, dev_status: torch.Tensor | None = None):
+    st = _prep(x_recv, seg_offsets, w_gate, w_up, w_down, row_map, ws, dev_status)
+    rows_cap, H = x_recv.shape
+    El, d, _ = w_gate.shape
+    G = len(peer_out)
+    res = _ptrs(peer_res) if peer_res is not None else None
+    _check("readme_ep_expert_ffn", lib().readme_ep_expert_ffn(
+        _ptr(x_recv), _dt(x_recv), rows_cap, H, El, d, G, _ptr(seg_offsets), _ptr(w_gate), _ptr(w_up),
+        _ptr(w_down), _ptr(row_map), _ptrs(peer_out), res, vrows, _ptr(dev_status), _ptr(ws), ws.numel(), st))

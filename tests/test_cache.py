@@ -158,3 +158,34 @@ def test_native_cache_all_protected_raises(rd):
     c.access(2, 1, protect_since=0)
     with pytest.raises(RuntimeError):
         c.access(3, 2, protect_since=0)
+
+
+# ---- the prefetch two-resource schedule (SPEC.md:413-420 hand Gantt charts) ---------------
+
+def test_prefetch_schedule_spec_examples():
+    from oracle.prefetch import simulate_prefetch
+    s, f, m = simulate_prefetch([2, 2, 2], [1, 1, 1], "prefetch")
+    assert (s, f, m) == ([1, 3, 5], [3, 5, 7], 7)
+    assert simulate_prefetch([2, 2, 2], [1, 1, 1], "on_demand")[2] == 9
+    s, f, m = simulate_prefetch([2, 2, 2], [0, 1, 1], "prefetch")  # first layer cached
+    assert (s, m) == ([0, 2, 4], 6)
+    for mode in ("prefetch", "on_demand"):
+        assert simulate_prefetch([2, 3, 4], [0, 0, 0], mode)[2] == 9  # all cached: sum of compute
+    with pytest.raises(ValueError):
+        simulate_prefetch([1], [-1], "prefetch")
+
+
+def test_prefetch_schedule_bounds():
+    """Prefetch never loses to on-demand, and its makespan lies between max(sum load + last compute,
+    first load + sum compute) and the on-demand sum."""
+    from oracle.prefetch import simulate_prefetch
+    g = np.random.default_rng(21)
+    for _ in range(300):
+        n = int(g.integers(1, 12))
+        c = g.uniform(0, 5, n).tolist()
+        x = (g.uniform(0, 5, n) * (g.random(n) < 0.7)).tolist()
+        pf = simulate_prefetch(c, x, "prefetch")[2]
+        od = simulate_prefetch(c, x, "on_demand")[2]
+        assert od == pytest.approx(sum(c) + sum(x))
+        assert pf <= od + 1e-9
+        assert pf >= max(sum(x) + c[-1], x[0] + sum(c)) - 1e-9
