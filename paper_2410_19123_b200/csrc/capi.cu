@@ -85,18 +85,28 @@ FfnPath ffn_path() {
 }
 
 // a6 + a7 (+ fused a8 when src != null) over the workspace `ws` (ffn_ws_bytes).
+// Whether the single-launch kernel runs (and may be launched as a programmatic dependent of the dispatch:
+// the caller then zeroes its readiness counters with zero_ready() BEFORE the dispatch, not between).
+bool merged_ffn(readme_dtype dt) { return dt == README_BF16 && ffn_path() == FfnPath::kMerged; }
+readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int32_t nseg, cudaStream_t st) {
+  README_CUDA(cudaMemsetAsync(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt), 0, ffn_layer_ready_bytes(rows, nseg),
+                              st));
+  return README_OK;
+}
+
 readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
                       int32_t n_src, const int32_t* offsets, const void* w_gate, const void* w_up,
                       const void* w_down, const int32_t* src, const void* residual, void* out, void* ws,
-                      uint32_t* dev_status, cudaStream_t st) {
+                      uint32_t* dev_status, cudaStream_t st, bool pdl = false) {
   readme_stream_t stream = reinterpret_cast<readme_stream_t>(st);
-  if (dt == README_BF16 && ffn_path() == FfnPath::kMerged) {
+  if (merged_ffn(dt)) {
     uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt));
     return launch_ffn_layer_2cta(static_cast<const __nv_bfloat16*>(x_sorted), rows, H, E, d, n_src * E, offsets,
                                  static_cast<const __nv_bfloat16*>(w_gate), static_cast<const __nv_bfloat16*>(w_up),
                                  static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(ws),
                                  static_cast<__nv_bfloat16*>(out), src,
-                                 static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st);
+                                 static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st, nullptr, 0,
+                                 nullptr, pdl);
   }
   README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
   return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, src, residual, out, stream);
@@ -343,6 +353,12 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   void* ws_ffn = w;
   w += ffn_ws_bytes(rows, d, dt);
   int32_t* src_ws = reinterpret_cast<int32_t*>(w);
+  const FfnPath path = ffn_path();
+  const bool fused = k == 1 && (src != nullptr || logits != nullptr) && path != FfnPath::k1cta &&
+                     path != FfnPath::kUnfused;
+  // the fused single-launch FFN follows the dispatch as a programmatic dependent (PDL)
+  const bool pdl = fused && merged_ffn(dt);
+  if (pdl) README_TRY(zero_ready(ws_ffn, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
     // a1-a4 with the finalize (offsets[e] + rank, src) fused into the a5 dispatch pass
@@ -357,15 +373,13 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   } else {
     README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   }
-  const FfnPath path = ffn_path();
-  const bool fused = k == 1 && src != nullptr && path != FfnPath::k1cta && path != FfnPath::kUnfused;
   if (fused) {
     // a6, then a7 with a8 fused into its epilogue: y[src[r]] = residual + h_r W_down^T (k == 1, weight 1).
     README_CHECK_ARG(aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y) &&
                          (!residual || aligned16(residual)),
                      "tensors must be 16-byte aligned");
     return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
-                   dev_status, reinterpret_cast<cudaStream_t>(stream));
+                   dev_status, reinterpret_cast<cudaStream_t>(stream), pdl);
   }
   README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
                                ffn_ws_bytes(rows, d, dt), stream));
@@ -427,12 +441,14 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
   if (logits)
     README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                             ws_route, route_ws_bytes(T, E, k), stream));
+  const bool pdl = k == 1 && merged_ffn(dt);
   for (int32_t l = 0; l < L; ++l) {
     README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
+    if (pdl) README_TRY(zero_ready(h, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
     README_TRY(readme_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status, stream));
     if (k == 1) {  // x <- x + MoE(RMSNorm(x)): the residual add is fused into the down epilogue, in place
       README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,
-                         dev_status, reinterpret_cast<cudaStream_t>(stream)));
+                         dev_status, reinterpret_cast<cudaStream_t>(stream), pdl));
     } else {
       README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], nullptr, nullptr,
                          y_sorted, h, dev_status, reinterpret_cast<cudaStream_t>(stream)));

@@ -34,6 +34,7 @@ constexpr int kMaxSeg = 512;
 constexpr int kStageA = 128 * 128;  // up to 128 rows x 128 B per CTA
 constexpr int kStageB = 128 * 128;  // 128 rows x 128 B per CTA (its half of N = 256)
 constexpr int kTmemCols = 512;      // two accumulators of 256 columns
+constexpr int kPrefetchK = 32;      // K stages of the first weight tile warmed in L2 before the PDL wait
 
 struct __align__(8) Smem {
   uint8_t a[kStages][kStageA];
@@ -366,6 +367,7 @@ struct LayerArgs {
   const __nv_bfloat16* peer_res[kMaxPeers];
   int npeer;
   int64_t vrows;
+  int pdl;  // launched as a programmatic dependent of the dispatch (wait before reading x_sorted)
 };
 
 struct LTile {
@@ -374,7 +376,7 @@ struct LTile {
 };
 
 __device__ __forceinline__ LTile decode_ltile(const Smem& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
-                                             int& gcur2) {
+                                             int& gcur2, int bn1, int bn2) {
   LTile tl;
   int local, g, NT;
   if (t < T1) {
@@ -400,7 +402,7 @@ __device__ __forceinline__ LTile decode_ltile(const Smem& s, int t, int nseg, in
   tl.m0 = s.seg_off[g] + mt * 256;
   tl.rows = min(256, cnt - mt * 256);
   tl.m256 = tl.rows > 128;
-  tl.n0 = nt * (tl.mode == 0 ? 128 : 256);
+  tl.n0 = nt * (tl.mode == 0 ? bn1 : bn2);
   return tl;
 }
 
@@ -410,7 +412,10 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
-template <int kFuse>
+// kNB = B rows each CTA stages per K step: 128 (default; a gate/up tile covers 128 h columns, a down tile
+// 256 output columns) or 64 (small batches: twice as many, half-width tiles, so every SM streams its
+// share of the touched experts' weights — decode is weight-bandwidth bound).
+template <int kFuse, int kNB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
@@ -422,7 +427,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const bool leader = cta == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
-  const int NT1 = (d + 127) / 128, NT2 = (H + 255) / 256;
+  constexpr int kBN1 = kNB, kBN2 = 2 * kNB;  // h columns per gate/up tile, output columns per down tile
+  constexpr int kN = 2 * kNB;               // MMA N (both CTAs' B halves)
+  static_assert(kNB == 128 || kNB == 64, "kNB");
+  const int NT1 = (d + kBN1 - 1) / kBN1, NT2 = (H + kBN2 - 1) / kBN2;
   const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
   const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
 
@@ -467,6 +475,23 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const int T1 = s.tile_start[nseg];
   const int ntiles = T1 + s.tile_start2[nseg];
   const uint32_t tmem_base = s.tmem_base;
+  // Launched with PDL behind the dispatch (la.pdl): everything above only read the routing offsets, which
+  // the route kernel wrote before the dispatch began. Before waiting for the dispatch's x_sorted, start
+  // pulling this pair's first gate/up weight tile into L2 — weights do not depend on the dispatch.
+  if (la.pdl) {
+    if (warp == 0 && lane == 0 && pair < T1) {
+      int g1 = 0, g2 = 0;
+      const LTile tl = decode_ltile(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
+      const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
+      const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
+      for (int kb = 0; kb < kbs; ++kb) {
+        tc::tma_prefetch_3d(&tmG, kb * kBK, nr, e);
+        tc::tma_prefetch_3d(&tmU, kb * kBK, nr, e);
+      }
+    }
+    tc::pdl_wait();
+  }
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
@@ -474,11 +499,11 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint32_t phase = 0;
     int g1 = 0, g2 = 0;
     for (int t = pair; t < ntiles; t += npairs) {
-      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kStageB);
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128);
       if (tl.mode == 1) {
         // wait until every gate/up tile of this m-tile has published its h rows
         if (lane == 0) {
@@ -505,12 +530,14 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
           tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
-          if (tl.mode == 0) {
-            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
-            tc::tma_load_3d_2sm(&tmU, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 64 * static_cast<int>(cta), e);
-          } else {
-            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, tl.n0 + 128 * static_cast<int>(cta), e);
-            tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 128 * static_cast<int>(cta) + 64, e);
+          if (tl.mode == 0) {  // kNB/2 rows of W_gate then the same rows of W_up (box height kNB/2)
+            const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
+            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nr, e);
+            tc::tma_load_3d_2sm(&tmU, s.b[stage] + (kNB / 2) * 128, fb, k0, nr, e);
+          } else {  // kNB rows of W_down in boxes of 64
+            const int nr = tl.n0 + kNB * static_cast<int>(cta);
+            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nr, e);
+            if constexpr (kNB == 128) tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nr + 64, e);
           }
         }
         if (++stage == kStages) {
@@ -522,13 +549,13 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   } else if (warp == 1) {
     if (leader && lane == 0) {
       // ===== MMA issuer (leader CTA, one thread) =====
-      constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
-      constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
+      constexpr uint32_t idesc256 = tc::idesc_bf16(256, kN);
+      constexpr uint32_t idesc128 = tc::idesc_bf16(128, kN);
       int stage = 0;
       uint32_t phase = 0;
       int g1 = 0, g2 = 0, i = 0;
       for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+        const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -559,42 +586,46 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint8_t* stg = s.stg[q];
     int g1 = 0, g2 = 0, i = 0;
     for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2);
+      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
       tc::fence_after();
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256);
-      int row_in_tile, n_windows, out_off;
-      const int bn_out = tl.mode == 0 ? 128 : 256;
+      // Accumulator columns of this warp's 32 rows: all kN (M=256), or half of them (M=128, "2x2" layout:
+      // lanes 64-127 hold columns [kN/2, kN) at TMEM columns [0, kN/2)).
+      int row_in_tile, ncols, acc_off;
       if (tl.m256) {
         row_in_tile = static_cast<int>(cta) * 128 + q * 32 + lane;
-        n_windows = 2;
-        out_off = 0;
+        ncols = kN;
+        acc_off = 0;
       } else {
         row_in_tile = static_cast<int>(cta) * 64 + (q & 1) * 32 + lane;
-        n_windows = 1;
-        out_off = (q >> 1) * (bn_out / 2);
+        ncols = kN / 2;
+        acc_off = (q >> 1) * (kN / 2);
       }
       const bool valid = row_in_tile < tl.rows;
       const int64_t r = tl.m0 + row_in_tile;
       if (tl.mode == 0) {
+        // windows of kNB columns: [gate kNB/2 | up kNB/2] of h columns n0 + (window) * kNB/2 + [0, kNB/2)
+        constexpr int kHalf = kNB / 2;
         __nv_bfloat16* orow = la.h + r * d;
-        for (int w = 0; w < n_windows; ++w) {
-          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
-          const int hcol0 = tl.n0 + out_off + w * 64;
+        for (int w = 0; w < ncols / kNB; ++w) {
+          const uint32_t wbase = tacc + static_cast<uint32_t>(w * kNB);
+          const int hcol0 = tl.n0 + (acc_off + w * kNB) / 2;
 #pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
+          for (int c = 0; c < kHalf; c += 32) {
             uint32_t gr[32], ur[32];
             tc::tmem_ld32(wbase + c, gr);
-            tc::tmem_ld32(wbase + 64 + c, ur);
+            tc::tmem_ld32(wbase + kHalf + c, ur);
             tc::tmem_wait_ld();
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
             stage_row_bf16x32(stg, lane, c / 8, v);
           }
-          stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, (d - hcol0) * 2, false);
+          const int lim = (d - hcol0) * 2 < kHalf * 2 ? (d - hcol0) * 2 : kHalf * 2;
+          stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, lim, false);
         }
       } else {
         int64_t orow_idx = r;
@@ -624,25 +655,21 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           orow = la.y + orow_idx * H;
           rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
         }
-        for (int w = 0; w < n_windows; ++w) {
-          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 64) {
-            const int col0 = tl.n0 + out_off + w * 128 + c0;
+        for (int c0 = 0; c0 < ncols; c0 += 64) {
+          const int col0 = tl.n0 + acc_off + c0;
 #pragma unroll 1
-            for (int c = 0; c < 64; c += 32) {
-              uint32_t vr[32];
-              tc::tmem_ld32(wbase + c0 + c, vr);
-              tc::tmem_wait_ld();
-              float v[32];
+          for (int c = 0; c < 64; c += 32) {
+            uint32_t vr[32];
+            tc::tmem_ld32(tacc + static_cast<uint32_t>(c0 + c), vr);
+            tc::tmem_wait_ld();
+            float v[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-              if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
-              stage_row_bf16x32(stg, lane, c / 8, v);
-            }
-            stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2,
-                        false);
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+            if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
+            stage_row_bf16x32(stg, lane, c / 8, v);
           }
+          stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2, false);
         }
       }
       tc::fence_before();
@@ -674,14 +701,17 @@ readme_status set_smem_attr() {
   README_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) dev = 0;
   std::call_once(once[dev], [&] {
-    const void* fns[6] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
+    const void* fns[9] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<0>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<2>)};
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 64>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 64>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 64>)};
     err[dev] = cudaSuccess;
-    for (int i = 0; i < 6 && err[dev] == cudaSuccess; ++i)
+    for (int i = 0; i < 9 && err[dev] == cudaSuccess; ++i)
       err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
   });
   if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
@@ -737,7 +767,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     const __nv_bfloat16* wu, const __nv_bfloat16* wd, __nv_bfloat16* h,
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
-                                    const int32_t* expert_slot, int32_t n_slots, const PeerOut* peers) {
+                                    const int32_t* expert_slot, int32_t n_slots, const PeerOut* peers,
+                                    bool pdl) {
   if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
@@ -745,22 +776,28 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   }
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
+  // Tile width: full width by default; README_FFN_NB=64 selects half-width tiles (twice as many tiles: more
+  // SMs share a small batch's weight stream, but measured slower at decode sizes — profiles/SUMMARY.md).
+  int nb = 128;
+  if (const char* v = getenv("README_FFN_NB")) nb = atoi(v) == 64 ? 64 : 128;
   CUtensorMap mX, mG, mU, mH, mD;
   const int32_t EW = expert_slot ? n_slots : E;  // outer extent of the weight tensors
-  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, 64) &&
-            tc::make_map_3d(&mU, wu, H, d, EW, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
+  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, nb / 2) &&
+            tc::make_map_3d(&mU, wu, H, d, EW, kBK, nb / 2) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
             tc::make_map_3d(&mD, wd, d, H, EW, kBK, 64);
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
     return README_ERR_CUDA;
   }
-  README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
+  // with pdl the caller zeroed `ready` before the dispatch (a memset here would sit between the two kernels)
+  if (!pdl) README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
   const int64_t mt_ub = nseg + (rows + 255) / 256;
   const int pairs = num_sms() / 2;
-  const int64_t tiles = mt_ub * ((d + 127) / 128 + (H + 255) / 256);
+  const int64_t tiles = mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
-               expert_slot, {}, {}, 0, 0};
+               expert_slot, {}, {}, 0, 0, pdl ? 1 : 0};
+  const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
       set_error("expert FFN remote scatter: need 1..%d peers, vrows >= 1 and a row map", kMaxPeers);
@@ -772,11 +809,29 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
     }
     la.npeer = peers->npeer;
     la.vrows = peers->vrows;
-    ffn_layer2_kernel<2><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
-  } else if (src || residual)
-    ffn_layer2_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
-  else
-    ffn_layer2_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(mX, mG, mU, mH, mD, la);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+#define README_LAYER_LAUNCH(F, NB) \
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, NB>, mX, mG, mU, mH, mD, la))
+  if (nb == 64) {
+    if (fuse == 2) README_LAYER_LAUNCH(2, 64);
+    else if (fuse == 1) README_LAYER_LAUNCH(1, 64);
+    else README_LAYER_LAUNCH(0, 64);
+  } else {
+    if (fuse == 2) README_LAYER_LAUNCH(2, 128);
+    else if (fuse == 1) README_LAYER_LAUNCH(1, 128);
+    else README_LAYER_LAUNCH(0, 128);
+  }
+#undef README_LAYER_LAUNCH
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

@@ -73,7 +73,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
                                     const int32_t* expert_slot = nullptr, int32_t n_slots = 0,
-                                    const PeerOut* peers = nullptr);
+                                    const PeerOut* peers = nullptr, bool pdl = false);
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                   const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);

@@ -15,6 +15,12 @@ namespace {
 
 constexpr int kPermThreads = 256;
 
+// The dispatch kernels let the expert FFN (launched as a programmatic dependent) start its prologue and
+// warm L2 with weights while they run; the FFN waits for their completion before reading x_sorted.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void set_offsets_kernel(int32_t* offs, int32_t T) {
   offs[0] = 0;
   offs[1] = T;
@@ -37,6 +43,7 @@ __device__ __forceinline__ void copy_row(const uint4* __restrict__ s, uint4* __r
 __global__ void __launch_bounds__(kPermThreads)
 dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, const int32_t* __restrict__ dest,
                 uint4* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+  pdl_launch_dependents();
   const int lane = threadIdx.x % kWarp;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
   for (int64_t s = blockIdx.x * static_cast<int64_t>(kPermThreads / kWarp) + threadIdx.x / kWarp; s < nslots;
@@ -91,6 +98,7 @@ template <typename Elt>
 __global__ void __launch_bounds__(kPermThreads)
 dispatch_rmsnorm_kernel(const Elt* __restrict__ x, int H, int64_t T, int k, const int32_t* __restrict__ dest,
                         float eps, Elt* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+  pdl_launch_dependents();
   const int lane = threadIdx.x % kWarp;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (kPermThreads / kWarp);
   const int groups = H / 8;
@@ -131,6 +139,7 @@ __global__ void __launch_bounds__(kPermThreads)
 finalize_dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, int E,
                          const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ offsets,
                          int32_t* __restrict__ dest, int32_t* __restrict__ src, uint4* __restrict__ xs) {
+  pdl_launch_dependents();
   __shared__ int s_off[README_MAX_EXPERTS + 1];
   for (int i = threadIdx.x; i <= E; i += blockDim.x) s_off[i] = offsets[i];
   __syncthreads();

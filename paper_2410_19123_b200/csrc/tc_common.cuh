@@ -110,6 +110,18 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* map, void* ds
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+// Warm L2 with a tile (no shared memory, no barrier): used before griddepcontrol.wait to start streaming
+// weights while the preceding kernel (the dispatch) still runs.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// Programmatic dependent launch (PDL): a primary kernel lets its dependent start early; the dependent
+// waits for the primary's completion (and memory flush) before touching what the primary writes.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, void* dst, uint32_t bar_cluster, int c0,
                                                 int c1, int c2) {
   asm volatile(

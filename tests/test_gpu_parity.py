@@ -168,6 +168,17 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
     return x, lg, wg, wu, wd
 
 
+def _set_kernel(monkeypatch, kernel):
+    """merged / merged-nb64 / merged-nb128 (single launch, tile width forced) / split / 1cta."""
+    if kernel.startswith("merged-nb"):
+        monkeypatch.setenv("README_FFN_NB", kernel[len("merged-nb"):])
+        kernel = "merged"
+    monkeypatch.setenv("README_FFN_KERNEL", kernel)
+
+
+KERNELS = ["merged-nb64", "merged-nb128", "split", "1cta"]
+
+
 @pytest.mark.parametrize("T,H,d,E,k,skew", [
     (1000, 256, 384, 8, 1, None),      # several M/N tiles, ragged segments
     (700, 512, 264, 8, 2, "empty"),    # empty experts, N tails (264 = 2*128 + 8), k = 2
@@ -177,9 +188,9 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
     (4000, 512, 256, 8, 1, "zipf"),    # many 256-row tiles, 128-row and 256-row tails
     (1024, 256, 128, 4, 1, None),      # counts ~256 -> exact and near-exact tiles
 ])
-@pytest.mark.parametrize("kernel", ["merged", "split", "1cta"])
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_expert_ffn_bf16_teacher_forced(rd, monkeypatch, kernel, T, H, d, E, k, skew):
-    monkeypatch.setenv("README_FFN_KERNEL", kernel)
+    _set_kernel(monkeypatch, kernel)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + H, skew=skew)
     plan = rd.route(torch.from_numpy(lg).to(DEV), k)
     xs = rd.dispatch(x.to(DEV), plan.dest, k)
@@ -220,10 +231,10 @@ def test_gate_up_and_down_separately(rd, dt):
     assert rel_err(_np(y), ref) <= tol
 
 
-@pytest.mark.parametrize("kernel", ["merged", "split", "1cta"])
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
     """Segment sizes on every tile boundary: empty, 1 row, 64/128/256 +- 1 (M=128 vs M=256 tails)."""
-    monkeypatch.setenv("README_FFN_KERNEL", kernel)
+    _set_kernel(monkeypatch, kernel)
     counts = [0, 1, 63, 64, 65, 127, 128, 129, 255, 256, 257, 383, 384, 385, 511, 512]
     E, H, d = len(counts), 128, 136
     off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
@@ -233,6 +244,25 @@ def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
     ys = rd.expert_ffn(xs.to(DEV), torch.from_numpy(off).to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV))
     ref = oracle.expert_ffn(xs, off, wg, wu, wd)
     assert rel_err(_np(ys), ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("T,d,skew", [(256, 5504, "zipf"), (2000, 264, None), (40, 136, "empty")])
+def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
+    """The half-width tiles (decode) and the full-width tiles compute every output element from the same
+    K-ordered MMAs: bitwise equal results, with and without the fused residual scatter."""
+    H, E = 4096 if d == 5504 else 256, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=T + d, skew=skew)
+    x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
+    wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
+    outs = []
+    for nb in ("64", "128"):
+        monkeypatch.setenv("README_FFN_NB", nb)
+        y, _ = rd.moe_layer(x, wg, wu, wd, logits=lg, residual=x)
+        plan = rd.route(lg, 1)
+        ys = rd.expert_ffn(rd.dispatch(x, plan.dest, 1), plan.offsets, wg, wu, wd)
+        outs.append((y, ys))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
 def test_expert_ffn_segments_n_src(rd):
