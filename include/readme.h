@@ -220,6 +220,20 @@ readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const i
                                     const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
                                     void* ws, size_t ws_bytes, readme_stream_t stream);
 
+/* Incremental evaluation (decode; SURVEY §8(f) NEXT-1 "run once per request, incrementally only for new
+ * tokens"): n new tokens, token i of request slot[i] at position pos[i] (0-based within its request). Each
+ * token's RoPE'd key and value are appended to kv_cache[slot][pos] (bf16 [n_slots, max_len, 2, 512]: k then v
+ * of all 4 heads; caller-owned, persists across calls), then every token attends to positions 0..pos[i] of
+ * its request (all appends of the call happen first, so several tokens of one request may be passed
+ * together, in any order), and logits [n, n_experts] f32 are written. Same block and readings as
+ * readme_router_forward; equal to it up to bf16 rounding order. Bad slot/pos set README_DEV_BAD_INDEX (that
+ * token's attention output is zero). max_len <= 32768. ws: readme_router_step_workspace_bytes(n). */
+size_t readme_router_step_workspace_bytes(int64_t n);
+readme_status readme_router_step(const int32_t* token_ids, int64_t n, const int32_t* slot, const int32_t* pos,
+                                 void* kv_cache, int32_t n_slots, int32_t max_len, const readme_router_weights* w,
+                                 float eps, float* logits, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                                 readme_stream_t stream);
+
 /* Setup (once per model load, not on the timed path): expert slicing, PAPER.md:159-163 (M_i is a
  * selection matrix without replacement).  dense_w_gate/up [D,H], dense_w_down [H,D] of dtype dt;
  * neuron_idx DEVICE int32 [E,d], each row strictly increasing in [0,D) (violations set

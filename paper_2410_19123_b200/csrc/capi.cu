@@ -492,11 +492,8 @@ size_t readme_router_workspace_bytes(int64_t T, int32_t nseq) {
   return router_ws_bytes(T < 0 ? 0 : T, nseq < 1 ? 1 : nseq);
 }
 
-readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
-                                    const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
-                                    void* ws, size_t ws_bytes, readme_stream_t stream) {
-  README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
-  README_CHECK_ARG(nseq >= 1, "nseq must be >= 1");
+namespace {
+readme_status check_router_weights(const readme_router_weights* w, float eps, RouterWeights* rw) {
   README_CHECK_ARG(w != nullptr, "weights are required");
   README_CHECK_ARG(w->vocab >= 1, "vocab must be >= 1");
   if (w->n_experts < 1 || w->n_experts > 16) {
@@ -504,31 +501,63 @@ readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const i
     return README_ERR_UNSUPPORTED;
   }
   README_CHECK_ARG(eps >= 0.f, "eps must be >= 0");
-  if (T == 0) return README_OK;
-  README_CHECK_ARG(token_ids && seq_starts && logits && ws, "null pointer argument");
   README_CHECK_ARG(w->emb && w->norm1 && w->w_qkv && w->w_o && w->norm2 && w->w_gate && w->w_up && w->w_down &&
                        w->norm_f && w->w_head,
                    "null weight pointer");
   README_CHECK_ARG(aligned16(w->w_qkv) && aligned16(w->w_o) && aligned16(w->w_gate) && aligned16(w->w_up) &&
-                       aligned16(w->w_down) && aligned16(ws),
-                   "projection weights and workspace must be 16-byte aligned");
+                       aligned16(w->w_down),
+                   "projection weights must be 16-byte aligned");
+  rw->vocab = w->vocab;
+  rw->n_experts = w->n_experts;
+  rw->emb = static_cast<const __nv_bfloat16*>(w->emb);
+  rw->g1 = static_cast<const __nv_bfloat16*>(w->norm1);
+  rw->wqkv = static_cast<const __nv_bfloat16*>(w->w_qkv);
+  rw->wo = static_cast<const __nv_bfloat16*>(w->w_o);
+  rw->g2 = static_cast<const __nv_bfloat16*>(w->norm2);
+  rw->wg = static_cast<const __nv_bfloat16*>(w->w_gate);
+  rw->wu = static_cast<const __nv_bfloat16*>(w->w_up);
+  rw->wd = static_cast<const __nv_bfloat16*>(w->w_down);
+  rw->gf = static_cast<const __nv_bfloat16*>(w->norm_f);
+  rw->whead = static_cast<const __nv_bfloat16*>(w->w_head);
+  return README_OK;
+}
+}  // namespace
+
+size_t readme_router_step_workspace_bytes(int64_t n) { return router_step_ws_bytes(n < 0 ? 0 : n); }
+
+readme_status readme_router_step(const int32_t* token_ids, int64_t n, const int32_t* slot, const int32_t* pos,
+                                 void* kv_cache, int32_t n_slots, int32_t max_len, const readme_router_weights* w,
+                                 float eps, float* logits, uint32_t* dev_status, void* ws, size_t ws_bytes,
+                                 readme_stream_t stream) {
+  README_CHECK_ARG(n >= 0 && n < (int64_t(1) << 31), "n out of range");
+  README_CHECK_ARG(n_slots >= 1 && max_len >= 1 && max_len <= 32768, "need n_slots >= 1 and 1 <= max_len <= 32768");
+  RouterWeights rw;
+  README_TRY(check_router_weights(w, eps, &rw));
+  if (n == 0) return README_OK;
+  README_CHECK_ARG(token_ids && slot && pos && kv_cache && logits && ws && aligned16(ws) && aligned16(kv_cache),
+                   "null pointer argument (or unaligned workspace / cache)");
+  if (ws_bytes < router_step_ws_bytes(n)) {
+    set_error("router step workspace too small: %zu < %zu", ws_bytes, router_step_ws_bytes(n));
+    return README_ERR_WORKSPACE;
+  }
+  return launch_router_step(token_ids, n, slot, pos, static_cast<__nv_bfloat16*>(kv_cache), n_slots, max_len, rw, eps,
+                            logits, ws, dev_status, reinterpret_cast<cudaStream_t>(stream));
+}
+
+readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
+                                    const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
+                                    void* ws, size_t ws_bytes, readme_stream_t stream) {
+  README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
+  README_CHECK_ARG(nseq >= 1, "nseq must be >= 1");
+  RouterWeights rw;
+  README_TRY(check_router_weights(w, eps, &rw));
+  if (T == 0) return README_OK;
+  README_CHECK_ARG(token_ids && seq_starts && logits && ws && aligned16(ws),
+                   "null pointer argument (or unaligned workspace)");
   if (ws_bytes < router_ws_bytes(T, nseq)) {
     set_error("router workspace too small: %zu < %zu", ws_bytes, router_ws_bytes(T, nseq));
     return README_ERR_WORKSPACE;
   }
-  RouterWeights rw;
-  rw.vocab = w->vocab;
-  rw.n_experts = w->n_experts;
-  rw.emb = static_cast<const __nv_bfloat16*>(w->emb);
-  rw.g1 = static_cast<const __nv_bfloat16*>(w->norm1);
-  rw.wqkv = static_cast<const __nv_bfloat16*>(w->w_qkv);
-  rw.wo = static_cast<const __nv_bfloat16*>(w->w_o);
-  rw.g2 = static_cast<const __nv_bfloat16*>(w->norm2);
-  rw.wg = static_cast<const __nv_bfloat16*>(w->w_gate);
-  rw.wu = static_cast<const __nv_bfloat16*>(w->w_up);
-  rw.wd = static_cast<const __nv_bfloat16*>(w->w_down);
-  rw.gf = static_cast<const __nv_bfloat16*>(w->norm_f);
-  rw.whead = static_cast<const __nv_bfloat16*>(w->w_head);
   return launch_router_forward(token_ids, T, seq_starts, nseq, rw, eps, logits, ws, dev_status,
                                reinterpret_cast<cudaStream_t>(stream));
 }

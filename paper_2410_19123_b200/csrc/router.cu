@@ -328,10 +328,132 @@ __global__ void router_tiles_kernel(const int32_t* __restrict__ seq_starts, int 
   *ntiles_out = n;
 }
 
+// ---- incremental evaluation (decode): one or more new tokens per request against a key/value cache ----
+
+// One warp per new token t at position pos[t] of request slot[t]: RoPE on q in place (as the prefill path),
+// RoPE'd k and raw v appended to the cache row kv[slot][pos] = [k (512) | v (512)].
+__global__ void router_rope_append_kernel(__nv_bfloat16* __restrict__ qkv, int64_t n, const int32_t* __restrict__ slot,
+                                          const int32_t* __restrict__ pos, __nv_bfloat16* __restrict__ kv,
+                                          int n_slots, int max_len, uint32_t* __restrict__ dev_status) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x / kWarp) + threadIdx.x / kWarp;
+  if (t >= n) return;
+  const int sl = slot[t], p = pos[t];
+  const bool ok = sl >= 0 && sl < n_slots && p >= 0 && p < max_len;
+  if (!ok) {
+    if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+    return;
+  }
+  __nv_bfloat16* row = qkv + t * (3 * kD);
+  __nv_bfloat16* cache = kv + (static_cast<int64_t>(sl) * max_len + p) * (2 * kD);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = lane + 32 * u;
+    const float inv = exp2f(-static_cast<float>(2 * i) / kHd * log2f(kTheta));
+    float sn, cs;
+    sincosf(static_cast<float>(p) * inv, &sn, &cs);
+#pragma unroll
+    for (int h = 0; h < kHeads; ++h) {
+      __nv_bfloat16* q = row + h * kHd;
+      float a = __bfloat162float(q[i]), b = __bfloat162float(q[i + 64]);
+      q[i] = __float2bfloat16_rn(a * cs - b * sn);
+      q[i + 64] = __float2bfloat16_rn(b * cs + a * sn);
+      const __nv_bfloat16* k = row + kD + h * kHd;
+      a = __bfloat162float(k[i]);
+      b = __bfloat162float(k[i + 64]);
+      cache[h * kHd + i] = __float2bfloat16_rn(a * cs - b * sn);
+      cache[h * kHd + i + 64] = __float2bfloat16_rn(b * cs + a * sn);
+    }
+  }
+  for (int c = lane; c < kD; c += kWarp) cache[kD + c] = row[2 * kD + c];
+}
+
+// One CTA (128 threads) per (new token, head): scores against the pos+1 cached keys (one thread per key,
+// fp32, in shared memory), softmax, then o[dim] = sum_j p_j v_j[dim] with one thread per dim (each V row
+// read coalesced). Weight-free and KV-bandwidth bound: 2 x 256 B per cached key per head.
+__global__ void __launch_bounds__(128)
+router_decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t n, const int32_t* __restrict__ slot,
+                               const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ kv, int n_slots,
+                               int max_len, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float s_sc[];  // [max_len] scores, then probabilities
+  __shared__ float s_q[kHd];
+  __shared__ float s_red[4];
+  const int64_t t = blockIdx.x;
+  const int head = blockIdx.y, tid = threadIdx.x, lane = tid % kWarp, warp = tid / kWarp;
+  const int sl = slot[t], p = pos[t];
+  if (sl < 0 || sl >= n_slots || p < 0 || p >= max_len) {  // flagged by the append kernel
+    out[t * kD + head * kHd + tid] = __float2bfloat16_rn(0.f);
+    return;
+  }
+  s_q[tid] = __bfloat162float(qkv[t * (3 * kD) + head * kHd + tid]);
+  __syncthreads();
+  const __nv_bfloat16* base = kv + static_cast<int64_t>(sl) * max_len * (2 * kD);
+  const float scale = rsqrtf(static_cast<float>(kHd));
+  float mx = -INFINITY;
+  for (int j = tid; j <= p; j += 128) {
+    const uint4* kr = reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * (2 * kD) + head * kHd);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < kHd / 8; ++c) {
+      const uint4 w = kr[c];
+      const float* q = s_q + c * 8;
+      acc = fmaf(q[0], bf16_lo(w.x), acc); acc = fmaf(q[1], bf16_hi(w.x), acc);
+      acc = fmaf(q[2], bf16_lo(w.y), acc); acc = fmaf(q[3], bf16_hi(w.y), acc);
+      acc = fmaf(q[4], bf16_lo(w.z), acc); acc = fmaf(q[5], bf16_hi(w.z), acc);
+      acc = fmaf(q[6], bf16_lo(w.w), acc); acc = fmaf(q[7], bf16_hi(w.w), acc);
+    }
+    acc *= scale;
+    s_sc[j] = acc;
+    mx = fmaxf(mx, acc);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0) s_red[warp] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = tid; j <= p; j += 128) {
+    const float e = __expf(s_sc[j] - mx);
+    s_sc[j] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  if (lane == 0) s_red[warp] = sum;
+  __syncthreads();
+  sum = s_red[0] + s_red[1] + s_red[2] + s_red[3];
+  const __nv_bfloat16* vcol = base + kD + head * kHd + tid;
+  float o = 0.f;
+  for (int j = 0; j <= p; ++j) o = fmaf(s_sc[j], __bfloat162float(vcol[static_cast<int64_t>(j) * (2 * kD)]), o);
+  out[t * kD + head * kHd + tid] = __float2bfloat16_rn(o / sum);
+}
+
 }  // namespace
 
 // Workspace layout: offsets (256 B) | h0 | a | qkv (3x) | att | h1 | h2 | tile_seq | tile_q0 | ntiles |
 // expert-FFN scratch (h [T, 512] + readiness counters).
+namespace {
+// h1 = h0 + att . Wo^T; h2 = h1 + MLP(RMSNorm_2(h1)); logits = RMSNorm_f(h2) . W_head^T.
+readme_status router_tail(int64_t T, const RouterWeights& w, float eps, float* logits, const int32_t* offs,
+                          const __nv_bfloat16* h0, __nv_bfloat16* a, const __nv_bfloat16* att, __nv_bfloat16* h1,
+                          __nv_bfloat16* h2, __nv_bfloat16* hff, uint32_t* ready, uint32_t* dev_status,
+                          cudaStream_t st) {
+  const int wpb = 8;
+  const unsigned gblocks = static_cast<unsigned>((T + wpb - 1) / wpb);
+  // h1 = h0 + att . Wo^T (the residual add fused into the GEMM epilogue)
+  README_TRY(launch_gemm_2cta(1, att, T, kD, kD, 1, 1, offs, w.wo, nullptr, h1, nullptr, h0, st));
+  // h2 = h1 + MLP(RMSNorm_2(h1)): the SwiGLU MLP is an expert FFN with one segment (E = 1, d = 512)
+  rmsnorm512_kernel<<<gblocks, 32 * wpb, 0, st>>>(h1, T, w.g2, eps, a);
+  README_CUDA(cudaGetLastError());
+  README_TRY(launch_ffn_layer_2cta(a, T, kD, 1, kD, 1, offs, w.wg, w.wu, w.wd, hff, h2, nullptr, h1, ready,
+                                   dev_status, st));
+  router_head_kernel<<<gblocks, 32 * wpb, w.n_experts * kD * sizeof(float), st>>>(h2, T, w.gf, w.whead,
+                                                                                   w.n_experts, eps, logits);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+}  // namespace
+
 size_t router_ws_bytes(int64_t T, int32_t nseq) {
   const size_t act = align_up(static_cast<size_t>(T) * kD * 2, 256);
   const size_t tiles = align_up(static_cast<size_t>(T / kQT + nseq + 1) * sizeof(int32_t), 256);
@@ -374,17 +496,47 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   dim3 ag(static_cast<unsigned>(max_tiles), kHeads);
   router_attention_kernel<<<ag, 128, 0, st>>>(qkv, seq_starts, tile_seq, tile_q0, ntiles, att);
   README_CUDA(cudaGetLastError());
-  // h1 = h0 + att . Wo^T (the residual add fused into the GEMM epilogue)
-  README_TRY(launch_gemm_2cta(1, att, T, kD, kD, 1, 1, offs, w.wo, nullptr, h1, nullptr, h0, st));
-  // h2 = h1 + MLP(RMSNorm_2(h1)): the SwiGLU MLP is an expert FFN with one segment (E = 1, d = 512)
-  rmsnorm512_kernel<<<gblocks, 32 * wpb, 0, st>>>(h1, T, w.g2, eps, a);
+  return router_tail(T, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
+}
+
+size_t router_step_ws_bytes(int64_t n) { return router_ws_bytes(n, 1); }
+
+readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* slot, const int32_t* pos,
+                                 __nv_bfloat16* kv, int32_t n_slots, int32_t max_len, const RouterWeights& w,
+                                 float eps, float* logits, void* ws, uint32_t* dev_status, cudaStream_t st) {
+  if (n == 0) return README_OK;
+  const size_t act = align_up(static_cast<size_t>(n) * kD * 2, 256);
+  const size_t tiles_b = align_up(static_cast<size_t>(n / kQT + 2) * sizeof(int32_t), 256);
+  char* p = static_cast<char*>(ws);
+  int32_t* offs = reinterpret_cast<int32_t*>(p);
+  p += 256;
+  auto* h0 = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  auto* a = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  auto* qkv = reinterpret_cast<__nv_bfloat16*>(p); p += 3 * act;
+  auto* att = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  auto* h1 = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  auto* h2 = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  p += 2 * tiles_b + 256;
+  auto* hff = reinterpret_cast<__nv_bfloat16*>(p); p += act;
+  uint32_t* ready = reinterpret_cast<uint32_t*>(p);
+
+  const int wpb = 8;
+  const unsigned gblocks = static_cast<unsigned>((n + wpb - 1) / wpb);
+  README_TRY(launch_set_offsets(offs, static_cast<int32_t>(n), st));
+  router_embed_norm_kernel<<<gblocks, 32 * wpb, 0, st>>>(ids, n, w.vocab, w.emb, w.g1, eps, h0, a, dev_status);
   README_CUDA(cudaGetLastError());
-  README_TRY(launch_ffn_layer_2cta(a, T, kD, 1, kD, 1, offs, w.wg, w.wu, w.wd, hff, h2, nullptr, h1, ready,
-                                   dev_status, st));
-  router_head_kernel<<<gblocks, 32 * wpb, w.n_experts * kD * sizeof(float), st>>>(h2, T, w.gf, w.whead,
-                                                                                   w.n_experts, eps, logits);
+  README_TRY(launch_gemm_2cta(1, a, n, kD, 3 * kD, 1, 1, offs, w.wqkv, nullptr, qkv, nullptr, nullptr, st));
+  // every new token's k/v reach the cache before any attention of this call reads it (causal within the
+  // call too: token t only reads positions <= pos[t])
+  router_rope_append_kernel<<<gblocks, 32 * wpb, 0, st>>>(qkv, n, slot, pos, kv, n_slots, max_len, dev_status);
   README_CUDA(cudaGetLastError());
-  return README_OK;
+  // up to 32768 cached positions: 128 KB of scores (a host-side attribute, cheap and capture-safe)
+  README_CUDA(cudaFuncSetAttribute(router_decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   128 * 1024));
+  router_decode_attention_kernel<<<dim3(static_cast<unsigned>(n), kHeads), 128, max_len * sizeof(float), st>>>(
+      qkv, n, slot, pos, kv, n_slots, max_len, att);
+  README_CUDA(cudaGetLastError());
+  return router_tail(n, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
 }
 
 }  // namespace readme

@@ -25,7 +25,8 @@ STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTE
 EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "readme_expert_ffn_workspace_bytes",
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
            "readme_build_experts", "readme_permanent_expert_workspace_bytes", "readme_permanent_expert",
-           "readme_router_workspace_bytes", "readme_router_forward", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
+           "readme_router_workspace_bytes", "readme_router_forward", "readme_router_step_workspace_bytes",
+           "readme_router_step", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
            "readme_scheduler_next_batch", "readme_expert_ffn_slots", "readme_cache_create", "readme_cache_destroy",
            "readme_cache_set_future", "readme_cache_access", "readme_cache_lookup", "readme_cache_stats",
@@ -80,6 +81,9 @@ _SIGS = {
     "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
                                                _vp]),
     "readme_router_workspace_bytes": (_sz, [_i64, _i32]),
+    "readme_router_step_workspace_bytes": (_sz, [_i64]),
+    "readme_router_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, ctypes.c_float, _vp, _vp, _vp,
+                                          _sz, _vp]),
     "readme_router_forward": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
     "readme_expert_ffn_slots": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                                                _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -462,6 +466,32 @@ def router_forward(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: d
     _check("readme_router_forward", lib().readme_router_forward(
         _ptr(token_ids), T, _ptr(seq_starts), nseq, ctypes.cast(ctypes.pointer(w), ctypes.c_void_p),
         ctypes.c_float(eps), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
+    return out
+
+
+def new_router_cache(n_slots: int, max_len: int, device) -> torch.Tensor:
+    """Key/value cache for readme_router_step: bf16 [n_slots, max_len, 2, 512]."""
+    return torch.zeros((n_slots, max_len, 2, 512), dtype=torch.bfloat16, device=device)
+
+
+def router_step(token_ids: torch.Tensor, slot: torch.Tensor, pos: torch.Tensor, kv_cache: torch.Tensor,
+                weights: dict, eps: float = 1e-5, out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """Incremental router (readme_router_step): new tokens (request slot, position) -> logits [n, N] f32; their
+    keys/values are appended to kv_cache."""
+    n = token_ids.numel()
+    N = weights["w_head"].shape[0]
+    n_slots, max_len = kv_cache.shape[0], kv_cache.shape[1]
+    out = out if out is not None else torch.empty((n, N), dtype=torch.float32, device=token_ids.device)
+    need = int(lib().readme_router_step_workspace_bytes(n))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=token_ids.device)
+    st = _prep(token_ids, slot, pos, kv_cache, out, ws, dev_status, *[weights[k] for k in ROUTER_KEYS])
+    w = _RouterWeights(weights["emb"].shape[0], N, *[weights[k].data_ptr() for k in ROUTER_KEYS])
+    _check("readme_router_step", lib().readme_router_step(
+        _ptr(token_ids), n, _ptr(slot), _ptr(pos), _ptr(kv_cache), n_slots, max_len,
+        ctypes.cast(ctypes.pointer(w), ctypes.c_void_p), ctypes.c_float(eps), _ptr(out), _ptr(dev_status), _ptr(ws),
+        ws.numel(), st))
     return out
 
 

@@ -598,3 +598,65 @@ def test_offloaded_queue_matches_resident_and_cache_oracle(rd, policy, prefetch)
         assert torch.equal(y, r)
     hits, misses, _ = ocache.simulate(trace, cap, policy, protect_since=prot)
     assert (stats["hits"], stats["misses"]) == (hits, misses)
+
+
+# ---- NEXT-1, incremental: the router over a key/value cache (decode) ----------------------------------
+
+def test_router_step_token_by_token_matches_oracle(rd):
+    """Requests advance one token per call (interleaved, ragged lengths) through readme_router_step; every
+    logit row matches the fp64 oracle (bf16 rule) and the prefill path within the same bound, and decisions
+    follow the near-tie rule of test_router_forward_parity (reading Q16)."""
+    from oracle import router
+    vocab, N = 32000, 8
+    W = {k: synth.to_torch(v, "bf16") for k, v in synth.router_weights(vocab=vocab, n_experts=N, seed=195).items()}
+    Wd = {k: v.to(DEV) for k, v in W.items()}
+    lens = [1, 70, 33, 129]
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ids = synth.token_ids(int(starts[-1]), vocab=vocab, seed=196)
+    cache = rd.new_router_cache(len(lens), 256, DEV)
+    got = np.zeros((int(starts[-1]), N))
+    status = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for step in range(max(lens)):
+        live = [r for r in range(len(lens)) if step < lens[r]]
+        tok = torch.tensor([ids[starts[r] + step] for r in live], dtype=torch.int32, device=DEV)
+        sl = torch.tensor(live, dtype=torch.int32, device=DEV)
+        ps = torch.full((len(live),), step, dtype=torch.int32, device=DEV)
+        lg = rd.router_step(tok, sl, ps, cache, Wd, dev_status=status)
+        got[[starts[r] + step for r in live]] = _np(lg)
+    assert int(status.item()) == 0
+    ref = router.forward(ids, starts, W)
+    assert rel_err(got, ref) <= BF16_TOL
+    pre = _np(rd.router_forward(torch.from_numpy(ids).to(DEV), torch.from_numpy(starts).to(DEV), Wd))
+    assert rel_err(got, pre) <= BF16_TOL
+    band = 4.0 * np.max(np.abs(got - ref))
+    top = np.sort(ref, axis=1)
+    clear = (top[:, -1] - top[:, -2]) > band
+    assert np.array_equal(got.argmax(axis=1)[clear], ref.argmax(axis=1)[clear])
+
+
+def test_router_step_chunk_equals_token_by_token(rd):
+    """Several tokens of one request in one call (a prefill chunk, any order) == one token per call, bitwise:
+    all appends of a call precede its attention, and no kernel mixes rows."""
+    vocab, N = 32000, 8
+    Wd = {k: synth.to_torch(v, "bf16").to(DEV) for k, v in synth.router_weights(vocab=vocab, n_experts=N, seed=197).items()}
+    n = 50
+    ids = torch.from_numpy(synth.token_ids(n, vocab=vocab, seed=198)).to(DEV)
+    c1, c2 = rd.new_router_cache(2, 64, DEV), rd.new_router_cache(2, 64, DEV)
+    one = torch.cat([rd.router_step(ids[i:i + 1], torch.tensor([1], dtype=torch.int32, device=DEV),
+                                    torch.tensor([i], dtype=torch.int32, device=DEV), c1, Wd) for i in range(n)])
+    perm = torch.from_numpy(np.random.default_rng(5).permutation(n)).to(DEV)
+    chunk = rd.router_step(ids[perm].contiguous(), torch.ones(n, dtype=torch.int32, device=DEV),
+                           perm.to(torch.int32).contiguous(), c2, Wd)
+    torch.cuda.synchronize()
+    assert torch.equal(chunk, one[perm]) and torch.equal(c1, c2)
+
+
+def test_router_step_bad_slot_flagged(rd):
+    vocab, N = 1000, 4
+    Wd = {k: synth.to_torch(v, "bf16").to(DEV) for k, v in synth.router_weights(vocab=vocab, n_experts=N, seed=199).items()}
+    cache = rd.new_router_cache(2, 8, DEV)
+    status = torch.zeros(1, dtype=torch.int32, device=DEV)
+    rd.router_step(torch.tensor([1, 2], dtype=torch.int32, device=DEV), torch.tensor([0, 5], dtype=torch.int32, device=DEV),
+                   torch.tensor([0, 0], dtype=torch.int32, device=DEV), cache, Wd, dev_status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) & rd.README_DEV_BAD_INDEX
