@@ -306,6 +306,32 @@ def run_decode(args):
     from paper_2410_19123_b200 import serving
     serve = [serving.simulate(pol, eg, eu, ed, n_requests=512, max_tokens=256, steps=48, device=dev)
              for pol in ("expert_aware", "fifo")]
+    # the incremental router (readme_router_step) for the same 256 decode tokens: each request has a cached
+    # history of 0..4095 tokens (uniform), one new token each; run once per token for the whole 32-layer model
+    RW = {kk: synth.to_torch(v, "bf16").to(dev) for kk, v in synth.router_weights(n_experts=E, seed=31).items()}
+    max_len = 4096
+    cache = rd.new_router_cache(256, max_len, dev)
+    pos = torch.from_numpy(synth.rng(32, 0).integers(0, max_len, size=256).astype(np.int32)).to(dev)
+    tok = torch.from_numpy(synth.token_ids(256, seed=33)).to(dev)
+    slots = torch.arange(256, dtype=torch.int32, device=dev)
+    r_out = torch.empty((256, E), dtype=torch.float32, device=dev)
+    r_ws = torch.empty(int(rd.lib().readme_router_step_workspace_bytes(256, max_len)), dtype=torch.uint8, device=dev)
+    rstep = lambda: rd.router_step(tok, slots, pos, cache, RW, out=r_out, ws=r_ws)
+    for _ in range(args.warmup):
+        rstep()
+    torch.cuda.synchronize()
+    r_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rstep()
+        b.record()
+        torch.cuda.synchronize()
+        r_ms.append(a.elapsed_time(b))
+    router_ms = float(np.mean(r_ms))
+    kv_bytes = float((pos.double() + 1).sum().item()) * 2 * 512 * 2
+    del cache
     main_pt = sweep[2]
     U = int(len(np.unique(ids256)))
     ffn_bytes = U * 3.0 * H * d * 2 + 2.0 * 256 * k * H * 2 + 2.0 * 256 * k * d * 2  # weights + x_s, y + h
@@ -352,6 +378,11 @@ def run_decode(args):
                          "step_GBps": main_pt["GBps"], "step_frac": main_pt["hbm_frac"]},
             "stage_ms_mean": {"route": float(np.mean(st[:, 0])), "dispatch": float(np.mean(st[:, 1])),
                               "expert_ffn": ffn_ms},
+            "router_step": {"ms": router_ms, "kv_GBps": kv_bytes / (router_ms * 1e-3) / 1e9,
+                            "share_of_32_layer_step": router_ms / (router_ms + 32 * main_pt["ms"]),
+                            "note": "readme_router_step: 256 decode tokens, cached histories uniform in [0, 4096), "
+                                    "once per token for all 32 layers; paper: router 1.26-1.50 % of batched step "
+                                    "latency (PAPER.md:647)"},
             "e2e": {"value": 256 / (float(np.mean(e_ms)) * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": x_h.numel() * 2 + lg_h.numel() * 4, "d2h_bytes_per_step": y_h.numel() * 2,
                     "ms_per_step": float(np.mean(e_ms))},

@@ -227,8 +227,9 @@ readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const i
  * its request (all appends of the call happen first, so several tokens of one request may be passed
  * together, in any order), and logits [n, n_experts] f32 are written. Same block and readings as
  * readme_router_forward; equal to it up to bf16 rounding order. Bad slot/pos set README_DEV_BAD_INDEX (that
- * token's attention output is zero). max_len <= 32768. ws: readme_router_step_workspace_bytes(n). */
-size_t readme_router_step_workspace_bytes(int64_t n);
+ * token's attention output is zero). max_len <= 32768. ws: readme_router_step_workspace_bytes(n, max_len). Attention is split over chunks of
+ * 256 cached positions (flash-decoding) and merged. */
+size_t readme_router_step_workspace_bytes(int64_t n, int32_t max_len);
 readme_status readme_router_step(const int32_t* token_ids, int64_t n, const int32_t* slot, const int32_t* pos,
                                  void* kv_cache, int32_t n_slots, int32_t max_len, const readme_router_weights* w,
                                  float eps, float* logits, uint32_t* dev_status, void* ws, size_t ws_bytes,

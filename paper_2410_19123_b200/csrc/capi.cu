@@ -523,7 +523,9 @@ readme_status check_router_weights(const readme_router_weights* w, float eps, Ro
 }
 }  // namespace
 
-size_t readme_router_step_workspace_bytes(int64_t n) { return router_step_ws_bytes(n < 0 ? 0 : n); }
+size_t readme_router_step_workspace_bytes(int64_t n, int32_t max_len) {
+  return router_step_ws_bytes(n < 0 ? 0 : n, max_len < 1 ? 1 : max_len);
+}
 
 readme_status readme_router_step(const int32_t* token_ids, int64_t n, const int32_t* slot, const int32_t* pos,
                                  void* kv_cache, int32_t n_slots, int32_t max_len, const readme_router_weights* w,
@@ -536,8 +538,8 @@ readme_status readme_router_step(const int32_t* token_ids, int64_t n, const int3
   if (n == 0) return README_OK;
   README_CHECK_ARG(token_ids && slot && pos && kv_cache && logits && ws && aligned16(ws) && aligned16(kv_cache),
                    "null pointer argument (or unaligned workspace / cache)");
-  if (ws_bytes < router_step_ws_bytes(n)) {
-    set_error("router step workspace too small: %zu < %zu", ws_bytes, router_step_ws_bytes(n));
+  if (ws_bytes < router_step_ws_bytes(n, max_len)) {
+    set_error("router step workspace too small: %zu < %zu", ws_bytes, router_step_ws_bytes(n, max_len));
     return README_ERR_WORKSPACE;
   }
   return launch_router_step(token_ids, n, slot, pos, static_cast<__nv_bfloat16*>(kv_cache), n_slots, max_len, rw, eps,

@@ -90,7 +90,7 @@ size_t router_ws_bytes(int64_t T, int32_t nseq);
 readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
                                     const RouterWeights& w, float eps, float* logits, void* ws,
                                     uint32_t* dev_status, cudaStream_t st);
-size_t router_step_ws_bytes(int64_t n);
+size_t router_step_ws_bytes(int64_t n, int32_t max_len);
 readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* slot, const int32_t* pos,
                                  __nv_bfloat16* kv, int32_t n_slots, int32_t max_len, const RouterWeights& w,
                                  float eps, float* logits, void* ws, uint32_t* dev_status, cudaStream_t st);

@@ -368,43 +368,69 @@ __global__ void router_rope_append_kernel(__nv_bfloat16* __restrict__ qkv, int64
   for (int c = lane; c < kD; c += kWarp) cache[kD + c] = row[2 * kD + c];
 }
 
-// One CTA (128 threads) per (new token, head): scores against the pos+1 cached keys (one thread per key,
-// fp32, in shared memory), softmax, then o[dim] = sum_j p_j v_j[dim] with one thread per dim (each V row
-// read coalesced). Weight-free and KV-bandwidth bound: 2 x 256 B per cached key per head.
+// Split-K decode attention (flash-decoding), KV-bandwidth bound (2 x 256 B per cached key per head). One
+// CTA (128 threads) per (new token, head, chunk of kChunk cached positions): 8 groups of 16 threads, group g
+// takes keys g, g+8, ... of the chunk and a thread owns 8 of the 128 dims, so every K / V row is read as 16
+// coalesced 16-byte pieces. Each CTA leaves its chunk's (max m, sum l, o = sum_j e^(s_j - m) v_j); the merge
+// kernel combines the chunks. Long histories thus spread over many SMs instead of serialising in one CTA.
+constexpr int kChunk = 256;
+constexpr int kPart = kHd + 2;  // floats per partial: o[128], m, l
+
 __global__ void __launch_bounds__(128)
 router_decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t n, const int32_t* __restrict__ slot,
                                const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ kv, int n_slots,
-                               int max_len, __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float s_sc[];  // [max_len] scores, then probabilities
-  __shared__ float s_q[kHd];
+                               int max_len, int nchunk, float* __restrict__ part) {
+  __shared__ float s_sc[kChunk];
+  __shared__ float s_o[8][kHd];
   __shared__ float s_red[4];
   const int64_t t = blockIdx.x;
-  const int head = blockIdx.y, tid = threadIdx.x, lane = tid % kWarp, warp = tid / kWarp;
+  const int head = blockIdx.y, c = blockIdx.z, tid = threadIdx.x, lane = tid % kWarp, warp = tid / kWarp;
+  const int grp = tid / 16, l16 = tid % 16;
   const int sl = slot[t], p = pos[t];
-  if (sl < 0 || sl >= n_slots || p < 0 || p >= max_len) {  // flagged by the append kernel
-    out[t * kD + head * kHd + tid] = __float2bfloat16_rn(0.f);
+  float* pp = part + ((t * kHeads + head) * nchunk + c) * kPart;
+  if (sl < 0 || sl >= n_slots || p < 0 || p >= max_len || c * kChunk > p) {  // empty chunk (or bad index)
+    if (tid == 0) {
+      pp[kHd] = -INFINITY;
+      pp[kHd + 1] = 0.f;
+    }
     return;
   }
-  s_q[tid] = __bfloat162float(qkv[t * (3 * kD) + head * kHd + tid]);
-  __syncthreads();
-  const __nv_bfloat16* base = kv + static_cast<int64_t>(sl) * max_len * (2 * kD);
+  const int j_lo = c * kChunk, j_hi = min(p, j_lo + kChunk - 1);  // inclusive
+  float q[8];
+  {
+    const uint4 w = *reinterpret_cast<const uint4*>(qkv + t * (3 * kD) + head * kHd + 8 * l16);
+    q[0] = bf16_lo(w.x); q[1] = bf16_hi(w.x); q[2] = bf16_lo(w.y); q[3] = bf16_hi(w.y);
+    q[4] = bf16_lo(w.z); q[5] = bf16_hi(w.z); q[6] = bf16_lo(w.w); q[7] = bf16_hi(w.w);
+  }
   const float scale = rsqrtf(static_cast<float>(kHd));
+  const int64_t rs = 2 * kD;  // cache row stride (elements)
+  const __nv_bfloat16* kbase = kv + static_cast<int64_t>(sl) * max_len * rs + head * kHd + 8 * l16;
+  const __nv_bfloat16* vbase = kbase + kD;
   float mx = -INFINITY;
-  for (int j = tid; j <= p; j += 128) {
-    const uint4* kr = reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * (2 * kD) + head * kHd);
-    float acc = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < kHd / 8; ++c) {
-      const uint4 w = kr[c];
-      const float* q = s_q + c * 8;
-      acc = fmaf(q[0], bf16_lo(w.x), acc); acc = fmaf(q[1], bf16_hi(w.x), acc);
-      acc = fmaf(q[2], bf16_lo(w.y), acc); acc = fmaf(q[3], bf16_hi(w.y), acc);
-      acc = fmaf(q[4], bf16_lo(w.z), acc); acc = fmaf(q[5], bf16_hi(w.z), acc);
-      acc = fmaf(q[6], bf16_lo(w.w), acc); acc = fmaf(q[7], bf16_hi(w.w), acc);
+  // uniform trip count for the whole CTA (the 16-lane shuffles below need both half-warps present)
+  for (int jb = j_lo; jb <= j_hi; jb += 32) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = jb + grp + 8 * u;
+      w[u] = j <= j_hi ? ld_nc_v4(reinterpret_cast<const uint4*>(kbase + j * rs)) : make_uint4(0, 0, 0, 0);
     }
-    acc *= scale;
-    s_sc[j] = acc;
-    mx = fmaxf(mx, acc);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float acc = q[0] * bf16_lo(w[u].x);
+      acc = fmaf(q[1], bf16_hi(w[u].x), acc); acc = fmaf(q[2], bf16_lo(w[u].y), acc);
+      acc = fmaf(q[3], bf16_hi(w[u].y), acc); acc = fmaf(q[4], bf16_lo(w[u].z), acc);
+      acc = fmaf(q[5], bf16_hi(w[u].z), acc); acc = fmaf(q[6], bf16_lo(w[u].w), acc);
+      acc = fmaf(q[7], bf16_hi(w[u].w), acc);
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      const int j = jb + grp + 8 * u;
+      if (j <= j_hi) {
+        acc *= scale;
+        if (l16 == 0) s_sc[j - j_lo] = acc;
+        mx = fmaxf(mx, acc);
+      }
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
@@ -413,20 +439,68 @@ router_decode_attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t n,
   mx = fmaxf(fmaxf(s_red[0], s_red[1]), fmaxf(s_red[2], s_red[3]));
   __syncthreads();
   float sum = 0.f;
-  for (int j = tid; j <= p; j += 128) {
-    const float e = __expf(s_sc[j] - mx);
-    s_sc[j] = e;
+  for (int j = j_lo + tid; j <= j_hi; j += 128) {
+    const float e = __expf(s_sc[j - j_lo] - mx);
+    s_sc[j - j_lo] = e;
     sum += e;
   }
   sum = warp_sum(sum);
   if (lane == 0) s_red[warp] = sum;
   __syncthreads();
   sum = s_red[0] + s_red[1] + s_red[2] + s_red[3];
-  const __nv_bfloat16* vcol = base + kD + head * kHd + tid;
-  float o = 0.f;
-  for (int j = 0; j <= p; ++j) o = fmaf(s_sc[j], __bfloat162float(vcol[static_cast<int64_t>(j) * (2 * kD)]), o);
-  out[t * kD + head * kHd + tid] = __float2bfloat16_rn(o / sum);
+  float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int jb = j_lo; jb <= j_hi; jb += 32) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = jb + grp + 8 * u;
+      w[u] = j <= j_hi ? ld_nc_v4(reinterpret_cast<const uint4*>(vbase + j * rs)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = jb + grp + 8 * u;
+      const float pj = j <= j_hi ? s_sc[j - j_lo] : 0.f;
+      o[0] = fmaf(pj, bf16_lo(w[u].x), o[0]); o[1] = fmaf(pj, bf16_hi(w[u].x), o[1]);
+      o[2] = fmaf(pj, bf16_lo(w[u].y), o[2]); o[3] = fmaf(pj, bf16_hi(w[u].y), o[3]);
+      o[4] = fmaf(pj, bf16_lo(w[u].z), o[4]); o[5] = fmaf(pj, bf16_hi(w[u].z), o[5]);
+      o[6] = fmaf(pj, bf16_lo(w[u].w), o[6]); o[7] = fmaf(pj, bf16_hi(w[u].w), o[7]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s_o[grp][8 * l16 + i] = o[i];
+  __syncthreads();
+  float acc = 0.f;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) acc += s_o[g][tid];
+  pp[tid] = acc;
+  if (tid == 0) {
+    pp[kHd] = mx;
+    pp[kHd + 1] = sum;
+  }
 }
+
+// Merge the chunks of one (token, head): o = sum_c e^(m_c - M) o_c / sum_c e^(m_c - M) l_c, c ascending.
+__global__ void __launch_bounds__(128)
+router_decode_merge_kernel(const float* __restrict__ part, int nchunk, __nv_bfloat16* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  const int head = blockIdx.y, tid = threadIdx.x;
+  const float* pp = part + (t * kHeads + head) * nchunk * kPart;
+  float M = -INFINITY;
+  for (int c = 0; c < nchunk; ++c) M = fmaxf(M, pp[c * kPart + kHd]);
+  float L = 0.f, O = 0.f;
+  if (M != -INFINITY) {
+    for (int c = 0; c < nchunk; ++c) {
+      const float m = pp[c * kPart + kHd];
+      if (m == -INFINITY) continue;
+      const float f = __expf(m - M);
+      L = fmaf(f, pp[c * kPart + kHd + 1], L);
+      O = fmaf(f, pp[c * kPart + tid], O);
+    }
+  }
+  out[t * kD + head * kHd + tid] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+}
+
+
 
 }  // namespace
 
@@ -499,7 +573,10 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   return router_tail(T, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
 }
 
-size_t router_step_ws_bytes(int64_t n) { return router_ws_bytes(n, 1); }
+size_t router_step_ws_bytes(int64_t n, int32_t max_len) {
+  const int nchunk = (max_len + kChunk - 1) / kChunk;
+  return router_ws_bytes(n, 1) + align_up(static_cast<size_t>(n) * kHeads * nchunk * kPart * sizeof(float), 256);
+}
 
 readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* slot, const int32_t* pos,
                                  __nv_bfloat16* kv, int32_t n_slots, int32_t max_len, const RouterWeights& w,
@@ -519,6 +596,8 @@ readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* s
   p += 2 * tiles_b + 256;
   auto* hff = reinterpret_cast<__nv_bfloat16*>(p); p += act;
   uint32_t* ready = reinterpret_cast<uint32_t*>(p);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + router_ws_bytes(n, 1));
+  const int nchunk = (max_len + kChunk - 1) / kChunk;
 
   const int wpb = 8;
   const unsigned gblocks = static_cast<unsigned>((n + wpb - 1) / wpb);
@@ -530,11 +609,10 @@ readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* s
   // call too: token t only reads positions <= pos[t])
   router_rope_append_kernel<<<gblocks, 32 * wpb, 0, st>>>(qkv, n, slot, pos, kv, n_slots, max_len, dev_status);
   README_CUDA(cudaGetLastError());
-  // up to 32768 cached positions: 128 KB of scores (a host-side attribute, cheap and capture-safe)
-  README_CUDA(cudaFuncSetAttribute(router_decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   128 * 1024));
-  router_decode_attention_kernel<<<dim3(static_cast<unsigned>(n), kHeads), 128, max_len * sizeof(float), st>>>(
-      qkv, n, slot, pos, kv, n_slots, max_len, att);
+  router_decode_attention_kernel<<<dim3(static_cast<unsigned>(n), kHeads, nchunk), 128, 0, st>>>(
+      qkv, n, slot, pos, kv, n_slots, max_len, nchunk, part);
+  README_CUDA(cudaGetLastError());
+  router_decode_merge_kernel<<<dim3(static_cast<unsigned>(n), kHeads), 128, 0, st>>>(part, nchunk, att);
   README_CUDA(cudaGetLastError());
   return router_tail(n, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
 }

@@ -81,7 +81,7 @@ _SIGS = {
     "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
                                                _vp]),
     "readme_router_workspace_bytes": (_sz, [_i64, _i32]),
-    "readme_router_step_workspace_bytes": (_sz, [_i64]),
+    "readme_router_step_workspace_bytes": (_sz, [_i64, _i32]),
     "readme_router_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, ctypes.c_float, _vp, _vp, _vp,
                                           _sz, _vp]),
     "readme_router_forward": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
@@ -483,7 +483,7 @@ def router_step(token_ids: torch.Tensor, slot: torch.Tensor, pos: torch.Tensor, 
     N = weights["w_head"].shape[0]
     n_slots, max_len = kv_cache.shape[0], kv_cache.shape[1]
     out = out if out is not None else torch.empty((n, N), dtype=torch.float32, device=token_ids.device)
-    need = int(lib().readme_router_step_workspace_bytes(n))
+    need = int(lib().readme_router_step_workspace_bytes(n, max_len))
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=token_ids.device)
     st = _prep(token_ids, slot, pos, kv_cache, out, ws, dev_status, *[weights[k] for k in ROUTER_KEYS])
