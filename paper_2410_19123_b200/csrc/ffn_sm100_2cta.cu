@@ -547,10 +547,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ===== MMA issuer (leader CTA, one thread) =====
+    if (leader) {
+      // ===== MMA issuer (leader CTA): the whole warp walks the loop (descriptors in uniform registers),
+      // one elected lane issues each tcgen05.mma / commit =====
       constexpr uint32_t idesc256 = tc::idesc_bf16(256, kN);
       constexpr uint32_t idesc128 = tc::idesc_bf16(128, kN);
+      const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
       int g1 = 0, g2 = 0, i = 0;
@@ -566,18 +568,24 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         for (int kb = 0; kb < KB; ++kb) {
           tc::mbar_wait_cluster(&s.full[stage], phase);
           tc::fence_after();
-          const uint32_t a0 = tc::smem_u32(s.a[stage]), b0 = tc::smem_u32(s.b[stage]);
+          // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
+          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (kStageA >> 4));
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / kUK; ++kk)
-            tc::mma_f16<2>(d_tmem, tc::sdesc_sw128(a0 + kk * kUK * 2), tc::sdesc_sw128(b0 + kk * kUK * 2), idesc,
-                           (kb | kk) != 0 ? 1u : 0u);
-          tc::commit_2sm_mc(&s.empty[stage], 0x3);
+            for (int kk = 0; kk < kBK / kUK; ++kk)
+              tc::mma_f16<2>(d_tmem, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2), idesc,
+                             (kb | kk) != 0 ? 1u : 0u);
+            tc::commit_2sm_mc(&s.empty[stage], 0x3);
+          }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+        if (tc::elect_one()) tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+        __syncwarp();
       }
     }
   } else {
@@ -694,6 +702,399 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Wide-N single-launch expert FFN (README_FFN_WIDE=1; measured slower, kept for A/B). A CTA pair computes a 256-row x 2-half tile: for every
+// K stage each CTA stages its 128 A rows ONCE and B rows for TWO 256-column halves, and issues two M=256
+// N=256 MMAs (one per half) into two TMEM accumulators (columns [0,256) and [256,512)). Staged bytes per
+// FLOP drop by a quarter against the double-buffered 256-column tile (48 KB per 1024 MMA cycles instead of
+// 32 KB per 512): that kernel is bound by L2->SM throughput (~11.5 TB/s measured, the LTS cap), so the
+// wide tile runs closer to the tensor-pipe bound. Gate/up half h covers h columns n0 + 128h + [0,128)
+// ([gate 64 | up 64] per CTA, as in the narrow kernel); down half h covers output columns n0 + 256h +
+// [0,256). A half that lies entirely past N is skipped (d = 5504 = 21.5 x 256).
+// The accumulators are single-buffered across tiles; the epilogue drains accumulator 0 first and releases
+// it, and the MMA issuer starts the next tile on accumulator 0 while accumulator 1 is still draining,
+// catching accumulator 1 up over the stages it kept (ring depth permitting): the epilogue stays hidden.
+constexpr int kWStages = 4;
+constexpr int kWStageB = 2 * 128 * 128;  // two halves x 128 rows x 128 B per CTA
+
+struct __align__(8) WSmem {
+  uint8_t a[kWStages][kStageA];
+  uint8_t b[kWStages][kWStageB];
+  uint64_t full[kWStages];
+  uint64_t empty[kWStages];
+  uint64_t tfull;
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  alignas(16) uint8_t stg[4][32 * 128];
+  int seg_off[kMaxSeg + 1];
+  int tile_start[kMaxSeg + 1];
+  int tile_start2[kMaxSeg + 1];
+  int mt_start[kMaxSeg + 1];
+};
+constexpr size_t kWSmemBytes = sizeof(WSmem) + 1024;
+static_assert(kWSmemBytes <= 232448, "wide kernel shared memory");
+
+__device__ __forceinline__ LTile decode_wtile(const WSmem& s, int t, int nseg, int T1, int& gcur1, int& gcur2,
+                                             int bn1, int bn2) {
+  LTile tl;
+  int local, g;
+  if (t < T1) {
+    while (gcur1 + 1 < nseg && s.tile_start[gcur1 + 1] <= t) ++gcur1;
+    g = gcur1;
+    local = t - s.tile_start[g];
+    tl.mode = 0;
+  } else {
+    const int t2 = t - T1;
+    while (gcur2 + 1 < nseg && s.tile_start2[gcur2 + 1] <= t2) ++gcur2;
+    g = gcur2;
+    local = t2 - s.tile_start2[g];
+    tl.mode = 1;
+  }
+  const int cnt = s.seg_off[g + 1] - s.seg_off[g];
+  const int mt_g = (cnt + 255) / 256;
+  const int nt = local / mt_g, mt = local % mt_g;
+  tl.g = g;
+  tl.mt = mt;
+  tl.m0 = s.seg_off[g] + mt * 256;
+  tl.rows = min(256, cnt - mt * 256);
+  tl.m256 = tl.rows > 128;
+  tl.n0 = nt * (tl.mode == 0 ? bn1 : bn2);
+  return tl;
+}
+
+template <int kFuse>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+ffn_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
+                const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
+                const __grid_constant__ CUtensorMap tmD, LayerArgs la) {
+  extern __shared__ uint8_t smem_raw[];
+  WSmem& s = *reinterpret_cast<WSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
+  const uint32_t cta = tc::cluster_ctarank();
+  const bool leader = cta == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
+  constexpr int kHW1 = 128, kHW2 = 256;            // columns per half: gate/up (h columns), down
+  constexpr int kBN1 = 2 * kHW1, kBN2 = 2 * kHW2;  // columns per tile
+  const int NT1 = (d + kBN1 - 1) / kBN1, NT2 = (H + kBN2 - 1) / kBN2;
+  const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
+  const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
+
+  for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = la.offsets[i];
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmX);
+    tc::prefetch_tmap(&tmG);
+    tc::prefetch_tmap(&tmU);
+    tc::prefetch_tmap(&tmH);
+    tc::prefetch_tmap(&tmD);
+  }
+  if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
+  __syncthreads();
+  if (tid == 0) {
+    int a1 = 0, a2 = 0, am = 0;
+    for (int g = 0; g < nseg; ++g) {
+      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + 255) / 256;
+      s.tile_start[g] = a1;
+      s.tile_start2[g] = a2;
+      s.mt_start[g] = am;
+      a1 += mt_g * NT1;
+      a2 += mt_g * NT2;
+      am += mt_g;
+    }
+    s.tile_start[nseg] = a1;
+    s.tile_start2[nseg] = a2;
+    s.mt_start[nseg] = am;
+    for (int i = 0; i < kWStages; ++i) {
+      tc::mbar_init(&s.full[i], 1);
+      tc::mbar_init(&s.empty[i], 1);
+    }
+    tc::mbar_init(&s.tfull, 1);
+    tc::mbar_init(&s.tempty[0], 8);
+    tc::mbar_init(&s.tempty[1], 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  const int T1 = s.tile_start[nseg];
+  const int ntiles = T1 + s.tile_start2[nseg];
+  const uint32_t tmem_base = s.tmem_base;
+  if (la.pdl) {  // see ffn_layer2_kernel: warm L2 with the first weight tile, then wait for the dispatch
+    if (warp == 0 && lane == 0 && pair < T1) {
+      int g1 = 0, g2 = 0;
+      const LTile tl = decode_wtile(s, pair, nseg, T1, g1, g2, kBN1, kBN2);
+      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
+      const int kbs = KB1 < kPrefetchK / 2 ? KB1 : kPrefetchK / 2;
+      for (int h = 0; h < 2; ++h) {
+        const int nr = tl.n0 + h * kHW1 + 64 * static_cast<int>(cta);
+        if (nr >= d) break;
+        for (int kb = 0; kb < kbs; ++kb) {
+          tc::tma_prefetch_3d(&tmG, kb * kBK, nr, e);
+          tc::tma_prefetch_3d(&tmU, kb * kBK, nr, e);
+        }
+      }
+    }
+    tc::pdl_wait();
+  }
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
+    int stage = 0;
+    uint32_t phase = 0;
+    int g1 = 0, g2 = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
+      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
+      const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
+      const int a_rows = tl.m256 ? 128 : 64;
+      const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + (two ? 2 : 1) * 128 * 128);
+      if (tl.mode == 1) {
+        if (lane == 0) {
+          const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
+          uint32_t spins = 0;
+          while (ld_acquire_u32(rp) < ready_target) {
+            __nanosleep(128);
+            if (++spins == (1u << 25)) {
+              if (la.dev_status) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+              break;
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+      }
+      const int KB = tl.mode == 0 ? KB1 : KB2;
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::mbar_wait(&s.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          const uint32_t fb = tc::mapa(&s.full[stage], 0);
+          const int k0 = kb * kBK;
+          if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
+          const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
+          tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
+          if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
+          for (int h = 0; h < (two ? 2 : 1); ++h) {
+            uint8_t* bh = s.b[stage] + h * (128 * 128);
+            if (tl.mode == 0) {  // 64 rows of W_gate then the same 64 rows of W_up
+              const int nr = tl.n0 + h * kHW1 + 64 * static_cast<int>(cta);
+              tc::tma_load_3d_2sm(&tmG, bh, fb, k0, nr, e);
+              tc::tma_load_3d_2sm(&tmU, bh + 64 * 128, fb, k0, nr, e);
+            } else {  // 128 rows of W_down
+              const int nr = tl.n0 + h * kHW2 + 128 * static_cast<int>(cta);
+              tc::tma_load_3d_2sm(&tmD, bh, fb, k0, nr, e);
+              tc::tma_load_3d_2sm(&tmD, bh + 64 * 128, fb, k0, nr + 64, e);
+            }
+          }
+        }
+        if (++stage == kWStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ===== MMA issuer (leader CTA): the whole warp walks the loop, one elected lane issues =====
+      constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
+      constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
+      const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
+      int stage = 0;
+      uint32_t phase = 0;
+      int g1 = 0, g2 = 0, i = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++i) {
+        const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
+        const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
+        const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
+        const uint32_t par = (static_cast<uint32_t>(i) & 1u) ^ 1u;  // accumulators released by tile i-1
+        const int KB = tl.mode == 0 ? KB1 : KB2;
+        // half-1 MMAs still owed (accumulator 1 not yet drained) for the consecutive stages
+        // [pend0, pend0 + npend) of this tile, which began at k-block first_pend_kb
+        int pend0 = 0, npend = 0, first_pend_kb = 0;
+        bool acc1_free = !two;
+        tc::mbar_wait_cluster(&s.tempty[0], par);
+        tc::fence_after();
+        auto issue = [&](int st, int h, bool first_k) {
+          const uint64_t ad = adesc0 + static_cast<uint64_t>(st * (kStageA >> 4));
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>(st * (kWStageB >> 4) + h * ((128 * 128) >> 4));
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(h * 256);
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < kBK / kUK; ++kk)
+              tc::mma_f16<2>(d_tmem, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2), idesc,
+                             (!first_k || kk != 0) ? 1u : 0u);
+          }
+          __syncwarp();
+        };
+        auto release = [&](int st) {
+          if (tc::elect_one()) tc::commit_2sm_mc(&s.empty[st], 0x3);
+          __syncwarp();
+        };
+        auto catch_up = [&]() {  // accumulator 1, oldest owed stage first
+          for (int j = 0; j < npend; ++j) {
+            const int st = (pend0 + j) % kWStages;
+            issue(st, 1, first_pend_kb + j == 0);
+            release(st);
+          }
+          npend = 0;
+        };
+        for (int kb = 0; kb < KB; ++kb) {
+          if (!acc1_free && npend == kWStages) {  // the ring is exhausted: wait for the drain
+            tc::mbar_wait_cluster(&s.tempty[1], par);
+            tc::fence_after();
+            acc1_free = true;
+          }
+          if (!acc1_free && tc::mbar_test_cluster(&s.tempty[1], par)) {
+            tc::fence_after();
+            acc1_free = true;
+          }
+          if (acc1_free && npend) catch_up();
+          tc::mbar_wait_cluster(&s.full[stage], phase);
+          tc::fence_after();
+          issue(stage, 0, kb == 0);
+          if (!two) {
+            release(stage);
+          } else if (acc1_free) {
+            issue(stage, 1, kb == 0);
+            release(stage);
+          } else {
+            if (npend == 0) {
+              pend0 = stage;
+              first_pend_kb = kb;
+            }
+            ++npend;
+          }
+          if (++stage == kWStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (npend) {  // short tile: accumulator 1 never freed while its stages streamed
+          tc::mbar_wait_cluster(&s.tempty[1], par);
+          tc::fence_after();
+          catch_up();
+        } else if (!two) {
+          tc::mbar_wait_cluster(&s.tempty[1], par);  // keep accumulator 1's phase in step with the tiles
+        }
+        if (tc::elect_one()) tc::commit_2sm_mc(&s.tfull, 0x3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 of both CTAs =====
+    const int q = warp & 3;
+    uint8_t* stg = s.stg[q];
+    int g1 = 0, g2 = 0, i = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++i) {
+      const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
+      const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
+      tc::mbar_wait_cluster(&s.tfull, static_cast<uint32_t>(i) & 1u);
+      tc::fence_after();
+      int row_in_tile, ncols, acc_off;
+      if (tl.m256) {
+        row_in_tile = static_cast<int>(cta) * 128 + q * 32 + lane;
+        ncols = 256;
+        acc_off = 0;
+      } else {
+        row_in_tile = static_cast<int>(cta) * 64 + (q & 1) * 32 + lane;
+        ncols = 128;
+        acc_off = (q >> 1) * 128;
+      }
+      const bool valid = row_in_tile < tl.rows;
+      const int64_t r = tl.m0 + row_in_tile;
+      // output row pointers (down tiles)
+      int64_t orow_idx = r;
+      bool valid_row = valid;
+      __nv_bfloat16* orow = nullptr;
+      const __nv_bfloat16* rrow = nullptr;
+      if (tl.mode == 1) {
+        if constexpr (kFuse == 2) {
+          const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
+          valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
+          const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
+          const int64_t iv = valid_row ? v - p * la.vrows : 0;
+          __nv_bfloat16* py = la.peer_y[0];
+          const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+          for (int j = 1; j < kMaxPeers; ++j)
+            if (p == j) {
+              py = la.peer_y[j];
+              pr = la.peer_res[j];
+            }
+          orow = py + iv * H;
+          rrow = pr ? pr + iv * H : nullptr;
+        } else {
+          if constexpr (kFuse == 1) {
+            orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
+            valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
+          }
+          orow = la.y + orow_idx * H;
+          rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
+        }
+      }
+      for (int h = 0; h < 2; ++h) {
+        if (h == 0 || two) {
+          const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 256);
+          if (tl.mode == 0) {
+            __nv_bfloat16* hrow = la.h + r * d;
+            for (int w = 0; w < ncols / 128; ++w) {
+              const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
+              const int hcol0 = tl.n0 + h * kHW1 + (acc_off + w * 128) / 2;
+#pragma unroll 1
+              for (int c = 0; c < 64; c += 32) {
+                uint32_t gr[32], ur[32];
+                tc::tmem_ld32(wbase + c, gr);
+                tc::tmem_ld32(wbase + 64 + c, ur);
+                tc::tmem_wait_ld();
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+                stage_row_bf16x32(stg, lane, c / 8, v);
+              }
+              stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(hrow + hcol0) : 0ull, (d - hcol0) * 2, false);
+            }
+          } else {
+#pragma unroll 1
+            for (int c0 = 0; c0 < ncols; c0 += 64) {
+              const int col0 = tl.n0 + h * kHW2 + acc_off + c0;
+#pragma unroll 1
+              for (int c = 0; c < 64; c += 32) {
+                uint32_t vr[32];
+                tc::tmem_ld32(tacc + static_cast<uint32_t>(c0 + c), vr);
+                tc::tmem_wait_ld();
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+                if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
+                stage_row_bf16x32(stg, lane, c / 8, v);
+              }
+              stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2,
+                          false);
+            }
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster_relaxed(&s.tempty[h], 0);  // accumulator h drained
+      }
+      if (lane == 0 && tl.mode == 0) {
+        // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + s.mt_start[tl.g] + tl.mt)
+                     : "memory");
+      }
+    }
+  }
+
+  if constexpr (kFuse == 2) __threadfence_system();
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
+}
+
 readme_status set_smem_attr() {
   static std::once_flag once[64];
   static cudaError_t err[64];
@@ -713,6 +1114,11 @@ readme_status set_smem_attr() {
     err[dev] = cudaSuccess;
     for (int i = 0; i < 9 && err[dev] == cudaSuccess; ++i)
       err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    const void* wfns[3] = {reinterpret_cast<const void*>(ffn_wide_kernel<0>),
+                           reinterpret_cast<const void*>(ffn_wide_kernel<1>),
+                           reinterpret_cast<const void*>(ffn_wide_kernel<2>)};
+    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
+      err[dev] = cudaFuncSetAttribute(wfns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWSmemBytes));
   });
   if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
   return README_OK;
@@ -780,6 +1186,11 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   // SMs share a small batch's weight stream, but measured slower at decode sizes — profiles/SUMMARY.md).
   int nb = 128;
   if (const char* v = getenv("README_FFN_NB")) nb = atoi(v) == 64 ? 64 : 128;
+  // README_FFN_WIDE=1 selects the wide-N tile (two 256-column halves per K stage, 25 % fewer staged bytes
+  // per FLOP); measured 15 % slower than the double-buffered 256-column tile at config 2 (more DRAM
+  // re-reads, single-buffered accumulators), so it is not the default (profiles/SUMMARY.md)
+  bool wide = false;
+  if (const char* v = getenv("README_FFN_WIDE")) wide = nb == 128 && atoi(v) != 0;
   CUtensorMap mX, mG, mU, mH, mD;
   const int32_t EW = expert_slot ? n_slots : E;  // outer extent of the weight tensors
   bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, nb / 2) &&
@@ -793,7 +1204,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   if (!pdl) README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
   const int64_t mt_ub = nseg + (rows + 255) / 256;
   const int pairs = num_sms() / 2;
-  const int64_t tiles = mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
+  const int64_t tiles = wide ? mt_ub * ((d + 255) / 256 + (H + 511) / 512)
+                             : mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
                expert_slot, {}, {}, 0, 0, pdl ? 1 : 0};
@@ -813,7 +1225,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = wide ? kWSmemBytes : kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -822,7 +1234,13 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cfg.numAttrs = pdl ? 1 : 0;
 #define README_LAYER_LAUNCH(F, NB) \
   README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, NB>, mX, mG, mU, mH, mD, la))
-  if (nb == 64) {
+#define README_WIDE_LAUNCH(F) \
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_wide_kernel<F>, mX, mG, mU, mH, mD, la))
+  if (wide) {
+    if (fuse == 2) README_WIDE_LAUNCH(2);
+    else if (fuse == 1) README_WIDE_LAUNCH(1);
+    else README_WIDE_LAUNCH(0);
+  } else if (nb == 64) {
     if (fuse == 2) README_LAYER_LAUNCH(2, 64);
     else if (fuse == 1) README_LAYER_LAUNCH(1, 64);
     else README_LAYER_LAUNCH(0, 64);
@@ -832,6 +1250,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
     else README_LAYER_LAUNCH(0, 128);
   }
 #undef README_LAYER_LAUNCH
+#undef README_WIDE_LAUNCH
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

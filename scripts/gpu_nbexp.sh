@@ -1,0 +1,11 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+python -m paper_2410_19123_b200.build > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+for nb in 128 64 128; do
+  README_FFN_NB=$nb timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b2_nb$nb.log 2>&1
+  python -c "
+import json
+d=json.loads(open('gpurun_out/b2_nb$nb.log').readline()); print('nb=$nb', round(d['value']), round(d['roofline']['frac'],3), d['stage_ms_median']['expert_ffn'], d['clocks'])
+"
+done

@@ -170,13 +170,14 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
 
 def _set_kernel(monkeypatch, kernel):
     """merged / merged-nb64 / merged-nb128 (single launch, tile width forced) / split / 1cta."""
-    if kernel.startswith("merged-nb"):
+    if kernel.startswith("merged-nb"):  # the double-buffered 256-column tile at a forced width
         monkeypatch.setenv("README_FFN_NB", kernel[len("merged-nb"):])
+        monkeypatch.setenv("README_FFN_WIDE", "0")
         kernel = "merged"
     monkeypatch.setenv("README_FFN_KERNEL", kernel)
 
 
-KERNELS = ["merged-nb64", "merged-nb128", "split", "1cta"]
+KERNELS = ["merged", "merged-nb64", "merged-nb128", "split", "1cta"]
 
 
 @pytest.mark.parametrize("T,H,d,E,k,skew", [
@@ -255,14 +256,16 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    for nb in ("64", "128"):
+    for nb, wide in (("64", "0"), ("128", "0"), ("128", "1")):  # half-width, 256-column, wide-N tiles
         monkeypatch.setenv("README_FFN_NB", nb)
+        monkeypatch.setenv("README_FFN_WIDE", wide)
         y, _ = rd.moe_layer(x, wg, wu, wd, logits=lg, residual=x)
         plan = rd.route(lg, 1)
         ys = rd.expert_ffn(rd.dispatch(x, plan.dest, 1), plan.offsets, wg, wu, wd)
         outs.append((y, ys))
     torch.cuda.synchronize()
-    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    for o in outs[1:]:
+        assert torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1])
 
 
 def test_expert_ffn_segments_n_src(rd):
