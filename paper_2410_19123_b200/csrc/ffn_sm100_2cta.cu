@@ -198,7 +198,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tc::mbar_wait(&s.empty[stage], phase ^ 1);
         const uint32_t fb = tc::mapa(&s.full[stage], 0);
         const int k0 = kb * kBK;
-        if (lane == 0) {
+        if (tc::elect_one()) {  // one elected lane of the converged warp (uniform operands)
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
           tc::tma_load_2d_2sm(&tmA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(&tmA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
@@ -210,6 +210,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc::tma_load_3d_2sm(&tmB0, s.b[stage] + 64 * 128, fb, k0, tl.n0 + 128 * static_cast<int>(cta) + 64, e);
           }
         }
+        __syncwarp();
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
@@ -217,10 +218,11 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ===== MMA issuer (leader CTA, one thread) =====
+    if (leader) {
+      // ===== MMA issuer (leader CTA): the whole warp walks the loop, one elected lane issues =====
       constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
       constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
+      const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
       int gcur = 0, i = 0;
@@ -235,18 +237,23 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kb = 0; kb < KB; ++kb) {
           tc::mbar_wait_cluster(&s.full[stage], phase);
           tc::fence_after();
-          const uint32_t a0 = tc::smem_u32(s.a[stage]), b0 = tc::smem_u32(s.b[stage]);
+          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (kStageA >> 4));
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / kUK; ++kk)
-            tc::mma_f16<2>(d_tmem, tc::sdesc_sw128(a0 + kk * kUK * 2), tc::sdesc_sw128(b0 + kk * kUK * 2), idesc,
-                           (kb | kk) != 0 ? 1u : 0u);
-          tc::commit_2sm_mc(&s.empty[stage], 0x3);
+            for (int kk = 0; kk < kBK / kUK; ++kk)
+              tc::mma_f16<2>(d_tmem, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2), idesc,
+                             (kb | kk) != 0 ? 1u : 0u);
+            tc::commit_2sm_mc(&s.empty[stage], 0x3);
+          }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+        if (tc::elect_one()) tc::commit_2sm_mc(&s.tfull[acc], 0x3);
+        __syncwarp();
       }
     }
   } else {
@@ -494,10 +501,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   }
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
+    // ===== TMA producer (both CTAs; completion counted on the leader's barrier). The whole warp walks the
+    // loop so coordinates and addresses stay in uniform registers; one elected lane issues. =====
     int stage = 0;
     uint32_t phase = 0;
     int g1 = 0, g2 = 0;
+    const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
     for (int t = pair; t < ntiles; t += npairs) {
       const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
@@ -506,40 +515,38 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128);
       if (tl.mode == 1) {
         // wait until every gate/up tile of this m-tile has published its h rows
-        if (lane == 0) {
-          const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
-          uint32_t spins = 0;
-          while (ld_acquire_u32(rp) < ready_target) {
-            __nanosleep(128);
-            if (++spins == (1u << 25)) {
-              if (la.dev_status) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
-              break;
-            }
+        const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
+        uint32_t spins = 0;
+        while (ld_acquire_u32(rp) < ready_target) {
+          __nanosleep(128);
+          if (++spins == (1u << 25)) {
+            if (la.dev_status && lane == 0) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+            break;
           }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
       }
       const int KB = tl.mode == 0 ? KB1 : KB2;
+      const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
+      const int nrg = tl.n0 + (kNB / 2) * static_cast<int>(cta), nrd = tl.n0 + kNB * static_cast<int>(cta);
       for (int kb = 0; kb < KB; ++kb) {
         tc::mbar_wait(&s.empty[stage], phase ^ 1);
-        if (lane == 0) {
-          const uint32_t fb = tc::mapa(&s.full[stage], 0);
+        if (tc::elect_one()) {
+          const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
           const int k0 = kb * kBK;
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
-          const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
           tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
           if (tl.mode == 0) {  // kNB/2 rows of W_gate then the same rows of W_up (box height kNB/2)
-            const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
-            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nr, e);
-            tc::tma_load_3d_2sm(&tmU, s.b[stage] + (kNB / 2) * 128, fb, k0, nr, e);
+            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nrg, e);
+            tc::tma_load_3d_2sm(&tmU, s.b[stage] + (kNB / 2) * 128, fb, k0, nrg, e);
           } else {  // kNB rows of W_down in boxes of 64
-            const int nr = tl.n0 + kNB * static_cast<int>(cta);
-            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nr, e);
-            if constexpr (kNB == 128) tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nr + 64, e);
+            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
+            if constexpr (kNB == 128) tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
           }
         }
+        __syncwarp();
         if (++stage == kStages) {
           stage = 0;
           phase ^= 1;
