@@ -19,6 +19,7 @@
 //            writes src (offsets need every tile's counts, so a second launch is the cheap barrier).
 //            readme_moe_layer fuses that finalize into the dispatch kernel (permute.cu).
 #include <math.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -41,7 +42,12 @@ RouteGeom route_geom(int64_t T, int32_t E, int32_t k) {
   int tt = kMaxTileSlots / k;
   int by_e = kMaxLogitFloats / E;
   if (by_e < tt) tt = by_e;
-  if (tt > 256) tt = 256;  // more CTAs in flight for small T; lookback chains stay short
+  // enough tiles to spread over the SMs (latency-bound: more CTAs in flight), at least 32 tokens per tile
+  // so lookback chains stay short; README_ROUTE_TILE overrides (A/B measurement)
+  int cap = 256;
+  while (cap > 32 && (T + cap - 1) / cap < 148) cap >>= 1;
+  if (const char* v = getenv("README_ROUTE_TILE")) cap = atoi(v) > 0 ? atoi(v) : cap;
+  if (tt > cap) tt = cap;
   if (tt < 1) tt = 1;
   RouteGeom g;
   g.tile_tokens = tt;
