@@ -663,3 +663,19 @@ def test_router_step_bad_slot_flagged(rd):
                    torch.tensor([0, 0], dtype=torch.int32, device=DEV), cache, Wd, dev_status=status)
     torch.cuda.synchronize()
     assert int(status.item()) & rd.README_DEV_BAD_INDEX
+
+
+def test_host_pipeline_equals_layer(rd):
+    """Batches streamed from pinned host memory with overlapped H2D / layer / D2H give exactly the layer's
+    output for every batch (double-buffered device buffers, event-ordered reuse)."""
+    from paper_2410_19123_b200.pipeline import HostPipeline
+    T, H, d, E, k = 700, 256, 256, 8, 1
+    W = [synth.to_torch(w, "bf16").to(DEV) for w in synth.expert_weights(E, d, H, seed=301)]
+    xs = [synth.to_torch(synth.tokens(T, H, seed=310 + i), "bf16").pin_memory() for i in range(5)]
+    lgs = [torch.from_numpy(synth.router_logits(T, E, seed=320 + i)).pin_memory() for i in range(5)]
+    ys = [torch.empty_like(x).pin_memory() for x in xs]
+    HostPipeline(T, H, E, k, *W, device=DEV).run(xs, lgs, ys)
+    torch.cuda.synchronize()
+    for x, lg, y in zip(xs, lgs, ys):
+        ref, _ = rd.moe_layer(x.to(DEV), *W, logits=lg.to(DEV))
+        assert torch.equal(y, ref.cpu())
