@@ -49,8 +49,13 @@ struct __align__(8) Smem {
   int tile_start[kMaxSeg + 1];
   int tile_start2[kMaxSeg + 1];  // merged a6+a7 kernel: the down tiles' prefix
   int mt_start[kMaxSeg + 1];     // merged kernel: first m-tile id of each segment (readiness counters)
+  // merged kernel, dynamic tile fetch: the leader's producer publishes each next tile id to both CTAs
+  int tq[4];
+  uint64_t tq_full[4];   // per CTA: the id in tq[slot] is valid (1 arrival: the leader's producer)
+  uint64_t tq_empty[4];  // leader only: every consumer warp of the pair has read tq[slot] (10 arrivals)
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+constexpr int kTQ = 4;
 
 struct Tile {
   int g, m0, rows, n0;
@@ -375,6 +380,8 @@ struct LayerArgs {
   int npeer;
   int64_t vrows;
   int pdl;  // launched as a programmatic dependent of the dispatch (wait before reading x_sorted)
+  int dyn;  // dynamic tile fetch: tiles after each pair's first come from an atomic counter (ready[sched])
+  int sched;
 };
 
 struct LTile {
@@ -473,6 +480,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       tc::mbar_init(&s.tfull[i], 1);
       tc::mbar_init(&s.tempty[i], 8);
     }
+    for (int i = 0; i < kTQ; ++i) {
+      tc::mbar_init(&s.tq_full[i], 1);
+      tc::mbar_init(&s.tq_empty[i], 10);  // leader MMA warp + 4 + 4 epilogue warps + the peer's producer
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc::fence_before();
@@ -499,6 +510,40 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     }
     tc::pdl_wait();
   }
+  // Tile sequence of this pair. Static: pair, pair + npairs, ... Dynamic (la.dyn): the first tile is still
+  // `pair`; each later one is npairs + atomicAdd(counter), fetched by the leader's producer when it moves on
+  // and published through a 4-deep queue to the pair's other warps — per-pair work evens out (tiles differ
+  // in cost: M=128 tails, gate/up vs down) while the global order (and the down tiles' readiness
+  // dependencies) stays the same. A consumer warp reads entry j and releases it on the leader.
+  const bool dyn = la.dyn != 0;
+  auto consume = [&](int j) -> int {
+    if (!dyn) return pair + j * npairs;
+    const int slot = j % kTQ;
+    tc::mbar_wait_cluster(&s.tq_full[slot], static_cast<uint32_t>(j / kTQ) & 1u);
+    const int t = *reinterpret_cast<volatile int*>(&s.tq[slot]);
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive_cluster(&s.tq_empty[slot], 0);
+    return t;
+  };
+  uint32_t fetched = 0;  // lane 0 of the leader's producer: the next tile's counter ticket, fetched one tile
+                         // ahead so the atomic's latency hides behind the current tile's loads
+  auto produce = [&](int j) -> int {  // the leader's producer warp
+    int t = pair + j * npairs;
+    if (dyn) {
+      if (j > 0) t = npairs + static_cast<int>(__shfl_sync(0xffffffffu, fetched, 0));
+      if (lane == 0) fetched = atomicAdd(la.ready + la.sched, 1u);
+      const int slot = j % kTQ;
+      tc::mbar_wait_cluster(&s.tq_empty[slot], (static_cast<uint32_t>(j / kTQ) & 1u) ^ 1u);
+      if (lane == 0) {
+        s.tq[slot] = t;
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(tc::mapa(&s.tq[slot], 1)), "r"(t) : "memory");
+        tc::mbar_arrive_cluster(&s.tq_full[slot], 0);  // release: the id stores are visible first
+        tc::mbar_arrive_cluster(&s.tq_full[slot], 1);
+      }
+      __syncwarp();
+    }
+    return t;
+  };
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion counted on the leader's barrier). The whole warp walks the
@@ -507,7 +552,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint32_t phase = 0;
     int g1 = 0, g2 = 0;
     const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
-    for (int t = pair; t < ntiles; t += npairs) {
+    for (int j = 0;; ++j) {
+      const int t = leader ? produce(j) : consume(j);
+      if (t >= ntiles) break;
       const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
@@ -562,8 +609,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
-      int g1 = 0, g2 = 0, i = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++i) {
+      int g1 = 0, g2 = 0;
+      for (int i = 0;; ++i) {
+        const int t = consume(i);
+        if (t >= ntiles) break;
         const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
@@ -599,8 +648,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
     uint8_t* stg = s.stg[q];
-    int g1 = 0, g2 = 0, i = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++i) {
+    int g1 = 0, g2 = 0;
+    for (int i = 0;; ++i) {
+      const int t = consume(i);
+      if (t >= ntiles) break;
       const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -1214,8 +1265,12 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   const int64_t tiles = wide ? mt_ub * ((d + 255) / 256 + (H + 511) / 512)
                              : mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
+  // README_FFN_DYNAMIC=1: dynamic tile fetch (counter = the spare readiness slot after the last m-tile).
+  // Measured 1-2 % slower than the static round-robin schedule at config 2 (profiles/SUMMARY.md), so off.
+  int dyn = 0;
+  if (const char* v = getenv("README_FFN_DYNAMIC")) dyn = atoi(v) != 0;
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
-               expert_slot, {}, {}, 0, 0, pdl ? 1 : 0};
+               expert_slot, {}, {}, 0, 0, pdl ? 1 : 0, dyn, static_cast<int>(nseg + (rows + 255) / 256)};
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
