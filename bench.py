@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the config-2 d=1376 / Markov / top-2 variants")
     ap.add_argument("--tokens", type=int, default=None, help="override T per rank")
     ap.add_argument("--eager", action="store_true", help="time eager calls instead of CUDA-graph replays")
     ap.add_argument("--ep", default="peer", choices=["peer", "nccl"],
@@ -861,6 +862,47 @@ def main():
         # dispatch, FFN, combine (+ NCCL's own kernels)
         line["gpu_launches"] = (12 if args.ep == "peer" else 5) * args.steps
     line["clocks"] = clk.summary()
+
+    if world == 1 and args.config == 2 and not args.no_variants:
+        # SURVEY §8(d) config-2 variants: the d = D/8 = 1376 partition experts, Markov-locality routing
+        # (2 requests x 4096, p = 0.672), and top-2. Each: graph-replayed readme_moe_layer step and the
+        # expert-FFN launch alone (events, L2 flushed), same protocol as the main line.
+        def variant(name, d_v, k_v, lg_np, w_v):
+            eg_v, eu_v, ed_v = w_v
+            lg_v = torch.from_numpy(lg_np).to(dev)
+            plan_v = rd.new_plan(T, E, k_v, dev)
+            y_v = torch.empty_like(x_dev)
+            ws_v = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d_v, k_v, torch.bfloat16), dtype=torch.uint8,
+                               device=dev)
+            fn = lambda: rd.moe_layer(x_dev, eg_v, eu_v, ed_v, k=k_v, logits=lg_v, plan=plan_v, out=y_v, ws=ws_v)
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            st_ms = timed(g.replay, args.steps)
+            xs_v = torch.empty((T * k_v, H), dtype=torch.bfloat16, device=dev)
+            rd.dispatch(x_dev, plan_v.dest, k_v, out=xs_v)
+            ys_v = torch.empty_like(xs_v)
+            wsf = torch.empty(rd.expert_ffn_workspace_bytes(T * k_v, H, E, d_v, torch.bfloat16), dtype=torch.uint8,
+                              device=dev)
+            f_ms = timed(lambda: rd.expert_ffn(xs_v, plan_v.offsets, eg_v, eu_v, ed_v, out=ys_v, ws=wsf), args.steps)
+            tf = 6.0 * T * k_v * H * d_v / (float(np.mean(f_ms)) * 1e-3) / 1e12
+            return {"variant": name, "d": d_v, "k": k_v, "tokens_per_s": T / (float(np.mean(st_ms)) * 1e-3),
+                    "ms_per_step": float(np.mean(st_ms)), "expert_ffn_ms": float(np.mean(f_ms)),
+                    "expert_ffn_tflops": tf, "frac": tf / pk["bf16_tflops"],
+                    "max_expert_rows": int(plan_v.counts.max().item())}
+        seedv = synth.MASTER_SEED + 22
+        variants = [
+            variant("d1376_partition", 1376, 1, inp["logits"],
+                    synth.expert_weights_device(E, 1376, H, dev, seed=seedv)),
+            variant("markov_locality_2x4096", d, 1,
+                    synth.logits_for_assignments(synth.assignments_markov(2, T // 2, E, 0.672, seed=seedv), E,
+                                                 seed=seedv), (eg, eu, ed)),
+            variant("top2", d, 2, inp["logits"], (eg, eu, ed)),
+        ]
+        line["variants"] = variants
 
     if world == 1 and not args.no_e2e:
         # e2e through the public API (readme_moe_layer) with pinned host buffers: H2D inputs, D2H result.
