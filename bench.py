@@ -845,17 +845,40 @@ def main():
                             "algorithmic": f"6*T*k*H*d = {f_all:.4g} FLOP per launch",
                             "split_launches": {"gate_up_tflops": a_gu, "gate_up_frac": a_gu / peak,
                                                "down_combine_tflops": a_dn, "down_combine_frac": a_dn / peak}}
-        # the standalone permutation entries (readme_dispatch / readme_combine), HBM-bound
+        # the standalone permutation entries (readme_dispatch / readme_combine), HBM-bound. Each is captured
+        # in a CUDA graph and replayed (an eager launch's host gap would land inside its events), L2 flushed.
         ys = torch.empty_like(xs)
-        comb_ms = timed(lambda: rd.combine(ys, plan.dest, plan.topk_w, k, out=y2), args.steps)
+
+        def graph_of(fn):
+            fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            return g.replay
+
+        # measured on 8x the rows (65536 tokens, 512 MiB each way) so the ~5 us launch of a one-kernel
+        # graph does not dominate a 20 us kernel; same kernels, same per-row work
+        Tb = 8 * T
+        xb = x_dev.repeat(8, 1)
+        lgb = torch.from_numpy(synth.router_logits(Tb, E, seed=synth.MASTER_SEED + 77)).to(dev)
+        planb = rd.route(lgb, k)
+        xsb = torch.empty((Tb * k, H), dtype=torch.bfloat16, device=dev)
+        ysb = torch.empty_like(xsb)
+        yb = torch.empty_like(xb)
+        disp_g_ms = timed(graph_of(lambda: rd.dispatch(xb, planb.dest, k, out=xsb)), args.steps)
+        comb_ms = timed(graph_of(lambda: rd.combine(ysb, planb.dest, planb.topk_w, k, out=yb)), args.steps)
+        del xb, xsb, ysb, yb
         hbm = pk["hbm_gbs"]
-        disp_bytes = 2.0 * T * k * H * 2
-        comb_bytes = (k + 1.0) * T * H * 2
-        dg = disp_bytes / (med(disp_ms) * 1e-3) / 1e9
+        disp_bytes = 2.0 * Tb * k * H * 2
+        comb_bytes = (k + 1.0) * Tb * H * 2
+        dg = disp_bytes / (med(disp_g_ms) * 1e-3) / 1e9
         cg = comb_bytes / (med(comb_ms) * 1e-3) / 1e9
         line["hbm"] = {"dispatch_GBps": dg, "combine_GBps": cg, "peak_GBps": hbm, "dispatch_frac": dg / hbm,
-                       "combine_frac": cg / hbm, "note": "readme_dispatch is on the step; readme_combine is the "
-                       "standalone entry (inside readme_moe_layer, k=1, it is fused into the down GEMM epilogue)"}
+                       "combine_frac": cg / hbm, "rows": Tb * k,
+                       "note": "readme_dispatch is on the step; readme_combine is the standalone entry (inside "
+                               "readme_moe_layer, k=1, it is fused into the down GEMM epilogue); graph-replayed at "
+                               "8x config-2 rows, L2 flushed"}
         line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + finalize/dispatch + expert FFN (+combine)
     else:
         # peer: route, finalize, publish, (signal, wait) x3, plan, dispatch, FFN = 12; nccl: route, finalize,
