@@ -770,13 +770,24 @@ def main():
         stage_fns = [lambda: rd.route(lg_dev, k, plan=plan, ws=ws_r),
                      lambda: rd.dispatch(x_dev, plan.dest, k, out=xs),
                      lambda: rd.expert_ffn(xs, plan.offsets, eg, eu, ed, out=y2, ws=ws_f)]
+        # each stage as its own CUDA graph: replays launch with ~us of host work, so the events between them
+        # measure the kernels rather than the Python/ctypes/tensor-map set-up of an eager call
+        stage_graphs = []
+        for f in stage_fns:
+            f()
+            torch.cuda.synchronize()
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                f()
+            stage_graphs.append(gph)
+        stage_fns = [gph.replay for gph in stage_graphs]
     with Clocks(local) as clk:
         if world > 1:
             step_ms = timed(step_fn, args.steps)
         else:
             # K timed steps (graph replays of readme_moe_layer); after each, in the same thermal/power
-            # window, one eager pass through the per-row C entries with events between the launches gives the
-            # live per-kernel breakdown (route | dispatch | a6 gate/up | a7 down + fused combine).
+            # window, one pass through the per-row C entries (each a graph replay) with events between them
+            # gives the live per-kernel breakdown (route | dispatch | expert FFN).
             step_ms, eager_ms, stages = [], [], []
             for _ in range(args.steps):
                 step_ms += timed(step_fn, 1)
