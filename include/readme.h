@@ -347,6 +347,15 @@ const char* readme_status_string(readme_status s);
 const char* readme_last_error(void); /* thread-local detail for the last non-OK return */
 int readme_version(void);
 
+/* Measurement only (not part of the hot-path contract): register a device buffer of 16 uint64 into which
+   the dispatch, route and expert-FFN kernels record %globaltimer extremes, or NULL to stop. Slots: 0/1
+   dispatch start (min) / end (max), 2 FFN past prologue (min), 3 first gate/up tile with its rows ready
+   (min), 4 FFN end (max), 5/6 route start (min) / end (max). */
+void readme_debug_trace(void* dev_buf);
+/* Measurement only: store %globaltimer into slot `slot` (8..15) of the registered trace buffer from a
+   one-thread kernel on `stream`. README_ERR_INVALID_ARG without a buffer or for another slot. */
+readme_status readme_debug_mark(int32_t slot, readme_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

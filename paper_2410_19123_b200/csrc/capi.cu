@@ -18,6 +18,7 @@ namespace readme {
 namespace {
 thread_local char g_err[512] = {0};
 }
+uint64_t* g_trace_buf = nullptr;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -94,10 +95,15 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
   return README_OK;
 }
 
+// x_sorted row flags inside the FFN workspace (see ffn_layer_ready_bytes)
+uint32_t* ffn_xready(void* ws, int64_t rows, int32_t d, readme_dtype dt) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt) + ffn_layer_xready_offset(rows));
+}
+
 readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
                       int32_t n_src, const int32_t* offsets, const void* w_gate, const void* w_up,
                       const void* w_down, const int32_t* src, const void* residual, void* out, void* ws,
-                      uint32_t* dev_status, cudaStream_t st, bool pdl = false) {
+                      uint32_t* dev_status, cudaStream_t st, bool pdl = false, bool xready = false) {
   readme_stream_t stream = reinterpret_cast<readme_stream_t>(st);
   if (merged_ffn(dt)) {
     uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt));
@@ -106,7 +112,7 @@ readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32
                                  static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(ws),
                                  static_cast<__nv_bfloat16*>(out), src,
                                  static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st, nullptr, 0,
-                                 nullptr, pdl);
+                                 nullptr, pdl, xready ? ffn_xready(ws, rows, d, dt) : nullptr);
   }
   README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
   return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, src, residual, out, stream);
@@ -135,6 +141,20 @@ const char* readme_status_string(readme_status s) {
 const char* readme_last_error(void) { return g_err; }
 
 int readme_version(void) { return README_VERSION; }
+
+// Measurement only: register (or clear, with NULL) a device buffer of 16 uint64 the hot-path kernels
+// record %globaltimer extremes into: [0] dispatch first CTA start (min), [1] dispatch last CTA end (max),
+// [2] expert FFN first CTA past its prologue (min), [3] first gate/up tile whose rows were ready (min),
+// [4] expert FFN last CTA end (max), [5] route start (min), [6] route end (max). The caller initialises
+// min slots to ~0 and max slots to 0. Not thread-safe; not for production use.
+void readme_debug_trace(void* dev_buf) { g_trace_buf = static_cast<uint64_t*>(dev_buf); }
+
+// Measurement only: a one-thread kernel that stores %globaltimer into slot `slot` (8..15) of the registered
+// trace buffer, stream-ordered (marks where a timed region starts / ends on the device clock).
+readme_status readme_debug_mark(int32_t slot, readme_stream_t stream) {
+  README_CHECK_ARG(g_trace_buf != nullptr && slot >= 8 && slot < 16, "no trace buffer, or slot not in [8, 16)");
+  return launch_debug_mark(g_trace_buf + slot, reinterpret_cast<cudaStream_t>(stream));
+}
 
 readme_status readme_set_device(int device) {
   int cur = -1;
@@ -359,17 +379,31 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   // the fused single-launch FFN follows the dispatch as a programmatic dependent (PDL)
   const bool pdl = fused && merged_ffn(dt);
   if (pdl) README_TRY(zero_ready(ws_ffn, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
+  bool xready = false;
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
-    // a1-a4 with the finalize (offsets[e] + rank, src) fused into the a5 dispatch pass
     README_TRY(check_route_call(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, ws_route,
                                 route_ws_bytes(T, E, k)));
     README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
-                            ws_route, st, /*finalize=*/false));
-    README_TRY(launch_finalize_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, E, topk_idx, offsets, dest,
-                                        src, x_sorted, st));
+    if (route_is_single_launch(T, k)) {
+      // a1-a4 in one cluster launch (dest and src final), then a5 in gather form publishing per-row flags:
+      // the fused FFN behind it (PDL) starts each gate/up tile as soon as its rows have landed
+      README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                              ws_route, st));
+      xready = pdl;
+      if (xready)
+        README_TRY(launch_dispatch_gather(x, static_cast<size_t>(H) * dt_size(dt), rows, k, src, x_sorted,
+                                          ffn_xready(ws_ffn, rows, d, dt), dev_status, st));
+      else
+        README_TRY(launch_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, dest, x_sorted, dev_status, st));
+    } else {
+      // a1-a4 with the finalize (offsets[e] + rank, src) fused into the a5 dispatch pass
+      README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                              ws_route, st, /*finalize=*/false));
+      README_TRY(launch_finalize_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, E, topk_idx, offsets, dest,
+                                          src, x_sorted, st));
+    }
   } else {
     README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   }
@@ -379,7 +413,7 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                          (!residual || aligned16(residual)),
                      "tensors must be 16-byte aligned");
     return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
-                   dev_status, reinterpret_cast<cudaStream_t>(stream), pdl);
+                   dev_status, reinterpret_cast<cudaStream_t>(stream), pdl, xready);
   }
   README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
                                ffn_ws_bytes(rows, d, dt), stream));

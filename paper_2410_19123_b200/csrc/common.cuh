@@ -81,4 +81,21 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Timeline trace for measurement only (readme_debug_trace): when a device buffer is registered, the
+// dispatch / route / expert FFN kernels record %globaltimer extremes into it (slot meanings in capi.cu).
+// Null by default: the kernels then skip it entirely.
+extern uint64_t* g_trace_buf;
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_min(uint64_t* tr, int i) {
+  if (tr) atomicMin(reinterpret_cast<unsigned long long*>(tr + i), static_cast<unsigned long long>(globaltimer_ns()));
+}
+__device__ __forceinline__ void trace_max(uint64_t* tr, int i) {
+  if (tr) atomicMax(reinterpret_cast<unsigned long long*>(tr + i), static_cast<unsigned long long>(globaltimer_ns()));
+}
+
 }  // namespace readme

@@ -35,6 +35,7 @@ constexpr int kStageA = 128 * 128;  // up to 128 rows x 128 B per CTA
 constexpr int kStageB = 128 * 128;  // 128 rows x 128 B per CTA (its half of N = 256)
 constexpr int kTmemCols = 512;      // two accumulators of 256 columns
 constexpr int kPrefetchK = 32;      // K stages of the first weight tile warmed in L2 before the PDL wait
+constexpr int kXokWords = 64;       // m-tiles whose x readiness is cached in shared memory (2048)
 
 struct __align__(8) Smem {
   uint8_t a[kStages][kStageA];
@@ -49,6 +50,7 @@ struct __align__(8) Smem {
   int tile_start[kMaxSeg + 1];
   int tile_start2[kMaxSeg + 1];  // merged a6+a7 kernel: the down tiles' prefix
   int mt_start[kMaxSeg + 1];     // merged kernel: first m-tile id of each segment (readiness counters)
+  uint32_t xok[kXokWords];       // merged kernel, pdl == 2: bit per m-tile, this CTA's A rows seen ready
   // merged kernel, dynamic tile fetch: the leader's producer publishes each next tile id to both CTAs
   int tq[4];
   uint64_t tq_full[4];   // per CTA: the id in tq[slot] is valid (1 arrival: the leader's producer)
@@ -379,9 +381,13 @@ struct LayerArgs {
   const __nv_bfloat16* peer_res[kMaxPeers];
   int npeer;
   int64_t vrows;
-  int pdl;  // launched as a programmatic dependent of the dispatch (wait before reading x_sorted)
+  int pdl;  // launched as a programmatic dependent of the dispatch: 1 = griddepcontrol.wait before reading
+            // x_sorted; 2 = per-row readiness flags (xready) instead, so gate/up tiles start while the
+            // dispatch is still writing later experts' rows (the wait moves to the kernel's end)
   int dyn;  // dynamic tile fetch: tiles after each pair's first come from an atomic counter (ready[sched])
   int sched;
+  const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
+  uint64_t* trace;         // measurement only (readme_debug_trace), normally null
 };
 
 struct LTile {
@@ -449,6 +455,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
 
   for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = la.offsets[i];
+  for (int i = tid; i < kXokWords; i += kThreads) s.xok[i] = 0u;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmX);
     tc::prefetch_tmap(&tmG);
@@ -508,8 +515,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         tc::tma_prefetch_3d(&tmU, kb * kBK, nr, e);
       }
     }
-    tc::pdl_wait();
+    if (la.pdl == 1) tc::pdl_wait();
   }
+  if (la.trace && tid == 0) trace_min(la.trace, 2);
   // Tile sequence of this pair. Static: pair, pair + npairs, ... Dynamic (la.dyn): the first tile is still
   // `pair`; each later one is npairs + atomicAdd(counter), fetched by the leader's producer when it moves on
   // and published through a 4-deep queue to the pair's other warps — per-pair work evens out (tiles differ
@@ -560,6 +568,30 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
       const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128);
+      if (tl.mode == 0 && la.pdl == 2) {
+        // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
+        // padding: their products are never stored, so they are not waited for)
+        const int mid = s.mt_start[tl.g] + tl.mt;
+        const bool cached = mid < kXokWords * 32 && (s.xok[mid >> 5] >> (mid & 31) & 1u);
+        if (!cached) {
+          const int lo = a_row0, hi = min(a_row0 + a_rows, tl.m0 + tl.rows);
+          uint32_t spins = 0;
+          for (;;) {
+            bool ok = true;
+            for (int r = lo + lane; r < hi; r += kWarp) ok = ok && ld_acquire_u32(la.xready + r) != 0u;
+            if (__all_sync(0xffffffffu, ok)) break;
+            __nanosleep(64);
+            if (++spins == (1u << 25)) {
+              if (la.dev_status && lane == 0) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+              break;
+            }
+          }
+          if (lane == 0 && mid < kXokWords * 32) s.xok[mid >> 5] |= 1u << (mid & 31);
+          if (la.trace && lane == 0) trace_min(la.trace, 3);
+          __syncwarp();
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       if (tl.mode == 1) {
         // wait until every gate/up tile of this m-tile has published its h rows
         const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
@@ -753,6 +785,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   }
 
   if constexpr (kFuse == 2) __threadfence_system();  // remote rows performed before the ready signal
+  if (la.pdl == 2) tc::pdl_wait();  // the dispatch is complete by now; keep the grid dependency explicit
+  if (la.trace && tid == 0) trace_max(la.trace, 4);
   tc::fence_before();
   __syncthreads();
   tc::cluster_sync();
@@ -1222,8 +1256,14 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   return README_OK;
 }
 
+// [readiness counters: <= kMaxSeg + #m-tiles + 1][x_sorted row flags: rows] (the flags are used when the
+// gather dispatch precedes the FFN, pdl == 2); one memset zeroes both
+size_t ffn_layer_xready_offset(int64_t rows) {
+  return align_up(static_cast<size_t>(kMaxSeg + (rows + 255) / 256 + 1) * sizeof(uint32_t), 256);
+}
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
-  return align_up(static_cast<size_t>(nseg + (rows + 255) / 256 + 1) * sizeof(uint32_t), 256);
+  (void)nseg;
+  return ffn_layer_xready_offset(rows) + align_up(static_cast<size_t>(rows) * sizeof(uint32_t), 256);
 }
 
 readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
@@ -1232,7 +1272,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
                                     const int32_t* expert_slot, int32_t n_slots, const PeerOut* peers,
-                                    bool pdl) {
+                                    bool pdl, const uint32_t* xready) {
   if (rows == 0) return README_OK;
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
@@ -1270,7 +1310,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   int dyn = 0;
   if (const char* v = getenv("README_FFN_DYNAMIC")) dyn = atoi(v) != 0;
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
-               expert_slot, {}, {}, 0, 0, pdl ? 1 : 0, dyn, static_cast<int>(nseg + (rows + 255) / 256)};
+               expert_slot, {}, {}, 0, 0, pdl ? (xready && !wide ? 2 : 1) : 0, dyn,
+               static_cast<int>(nseg + (rows + 255) / 256), xready, g_trace_buf};
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {

@@ -9,11 +9,20 @@ size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
                            int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize = true);
+// true when launch_route runs the single-launch cluster route for this batch: it then always finalizes
+// (dest = offsets + rank, src) regardless of `finalize`.
+bool route_is_single_launch(int64_t T, int32_t k);
 
 // permute.cu
 readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, const int32_t* dest,
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st);
+// Gather form of a5 for readme_moe_layer after the single-launch route: x_sorted[r] = x[src[r] / k], rows
+// in ascending waves, xready[r] set (release) once row r is written; the expert FFN launched behind it
+// (PDL) waits on those flags per tile instead of on the whole dispatch.
+readme_status launch_dispatch_gather(const void* x, size_t row_bytes, int64_t rows, int32_t k, const int32_t* src,
+                                     void* x_sorted, uint32_t* xready, uint32_t* dev_status, cudaStream_t st);
 readme_status launch_set_offsets(int32_t* offs, int32_t T, cudaStream_t st);  // {0, T}
+readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st);  // measurement only
 readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,
                                        const int32_t* topk_idx, const int32_t* offsets, int32_t* dest, int32_t* src,
                                        void* x_sorted, cudaStream_t st);
@@ -54,6 +63,7 @@ struct PeerOut {
   int64_t vrows;
 };
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg);
+size_t ffn_layer_xready_offset(int64_t rows);  // byte offset of the x_sorted row flags in `ready`
 
 // Expert parallelism over peer memory (ep.cu).
 readme_status launch_ep_signal(uint64_t* const* peer_flags, int G, int me, uint64_t* epoch, cudaStream_t st);
@@ -73,7 +83,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
                                     const int32_t* expert_slot = nullptr, int32_t n_slots = 0,
-                                    const PeerOut* peers = nullptr, bool pdl = false);
+                                    const PeerOut* peers = nullptr, bool pdl = false,
+                                    const uint32_t* xready = nullptr);
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                   const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);

@@ -7,6 +7,8 @@
 // All three are HBM-bound row moves. One warp per row; each lane keeps kUnroll 128-bit loads in flight
 // before storing (Little's law: ~6.4 TB/s x ~1 us needs ~45 KB in flight per SM; 64 warps x 32 lanes x
 // 4 x 16 B = 128 KB), L1 bypassed for the streamed source.
+#include <mutex>
+
 #include "kernels.h"
 
 namespace readme {
@@ -158,6 +160,52 @@ finalize_dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, i
   }
 }
 
+// readme_moe_layer's a5 after the single-launch route (dest/src final): gather form x_sorted[r] = x[src[r]/k].
+// Warp w of W moves rows w, w + W, w + 2W, ... so the rows complete in ascending waves of W rows; after each
+// row the warp publishes xready[r] = 1 (release, gpu scope) and the expert FFN, launched behind this kernel
+// as a programmatic dependent and co-resident with it, starts expert 0's gate/up tiles after the first wave
+// instead of after the whole dispatch. Co-residency is a register budget per SM sub-partition (16K each):
+// the FFN CTA puts up to 2 warps x 152 x 32 registers on one, which leaves room for 3 warps of <= 64
+// registers — hence ONE CTA of 12 warps per SM. The TMA (async proxy) reads x_sorted, hence the proxy
+// fence before the flag.
+constexpr int kGatherUnroll = 8;
+constexpr int kGatherThreads = 384;
+__global__ void __maxnreg__(64)
+dispatch_gather_kernel(const uint4* __restrict__ x, int vec, int64_t nrows, int k, const int32_t* __restrict__ src,
+                       uint4* __restrict__ xs, uint32_t* __restrict__ xready, uint32_t* __restrict__ dev_status,
+                       uint64_t* __restrict__ trace) {
+  pdl_launch_dependents();
+  if (trace && threadIdx.x == 0) trace_min(trace, 0);
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kGatherThreads / kWarp);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(kGatherThreads / kWarp) + threadIdx.x / kWarp; r < nrows;
+       r += warps) {
+    const int32_t sl = __ldg(src + r);
+    if (sl < 0 || sl >= nrows) {
+      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+    } else {
+      const uint4* srow = x + (sl / k) * static_cast<int64_t>(vec);
+      uint4* drow = xs + r * vec;
+      int i = lane;
+      for (; i + (kGatherUnroll - 1) * kWarp < vec; i += kGatherUnroll * kWarp) {
+        uint4 v[kGatherUnroll];
+#pragma unroll
+        for (int u = 0; u < kGatherUnroll; ++u) v[u] = ld_nc_v4(srow + i + u * kWarp);
+#pragma unroll
+        for (int u = 0; u < kGatherUnroll; ++u) st_v4(drow + i + u * kWarp, v[u]);
+      }
+      for (; i < vec; i += kWarp) st_v4(drow + i, ld_nc_v4(srow + i));
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(xready + r), "r"(1u) : "memory");
+    }
+  }
+  if (trace && threadIdx.x % kWarp == 0) trace_max(trace, 1);
+}
+
 // k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
 __global__ void __launch_bounds__(kPermThreads)
 gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
@@ -242,7 +290,27 @@ __global__ void slice_cols_kernel(const Elt* __restrict__ wd, int D, int H, int 
   }
 }
 
+// The kernels the expert FFN follows as a programmatic dependent run with the maximum shared-memory carveout:
+// an SM's L1/shared split only changes while it is idle, so a dispatch CTA running under an L1-heavy split
+// would keep the FFN's CTA (~200 KB of shared memory) off that SM until the dispatch retires there.
+void set_dispatch_carveout() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [] {
+    const void* fns[] = {reinterpret_cast<const void*>(dispatch_gather_kernel),
+                         reinterpret_cast<const void*>(finalize_dispatch_kernel),
+                         reinterpret_cast<const void*>(dispatch_kernel),
+                         reinterpret_cast<const void*>(dispatch_rmsnorm_kernel<__nv_bfloat16>),
+                         reinterpret_cast<const void*>(dispatch_rmsnorm_kernel<float>)};
+    for (const void* f : fns)
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaGetLastError();  // a hint only
+  });
+}
+
 int grid_for_rows(int64_t rows) {
+  set_dispatch_carveout();
   const int64_t want = (rows + (kPermThreads / kWarp) - 1) / (kPermThreads / kWarp);
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;  // 8 CTAs x 8 warps = 64 warps per SM
   return static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
@@ -257,6 +325,26 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
   dispatch_kernel<<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
       static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
       static_cast<uint4*>(x_sorted), dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_dispatch_gather(const void* x, size_t row_bytes, int64_t rows, int32_t k, const int32_t* src,
+                                     void* x_sorted, uint32_t* xready, uint32_t* dev_status, cudaStream_t st) {
+  if (rows == 0) return README_OK;
+  set_dispatch_carveout();
+  const int64_t want = (rows + (kGatherThreads / kWarp) - 1) / (kGatherThreads / kWarp);
+  const int64_t cap = num_sms();
+  dispatch_gather_kernel<<<static_cast<int>(want < cap ? want : cap), kGatherThreads, 0, st>>>(
+      static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), rows, k, src, static_cast<uint4*>(x_sorted),
+      xready, dev_status, g_trace_buf);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+__global__ void debug_mark_kernel(uint64_t* slot) { *slot = globaltimer_ns(); }
+readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st) {
+  debug_mark_kernel<<<1, 1, 0, st>>>(slot);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

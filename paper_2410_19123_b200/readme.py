@@ -34,7 +34,7 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_ep_signal", "readme_ep_wait", "readme_ep_publish_counts", "readme_ep_plan", "readme_ep_dispatch",
            "readme_ep_expert_ffn",
            "readme_set_device", "readme_status_string", "readme_last_error",
-           "readme_version")
+           "readme_version", "readme_debug_trace", "readme_debug_mark")
 
 
 class ReadmeError(RuntimeError):
@@ -110,6 +110,8 @@ _SIGS = {
     "readme_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "readme_last_error": (ctypes.c_char_p, []),
     "readme_version": (ctypes.c_int, []),
+    "readme_debug_trace": (None, [_vp]),
+    "readme_debug_mark": (ctypes.c_int, [_i32, _vp]),
 }
 
 

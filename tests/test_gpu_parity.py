@@ -63,14 +63,30 @@ ROUTE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("impl", ["cluster", "lookback"])
 @pytest.mark.parametrize("T,E,k,kind,ldt", ROUTE_CASES)
-def test_route_bit_exact(rd, T, E, k, kind, ldt):
+def test_route_bit_exact(rd, monkeypatch, impl, T, E, k, kind, ldt):
+    # both route implementations: the single-launch cluster route (default up to 256K slots) and the
+    # multi-CTA decoupled-lookback route (larger batches)
+    monkeypatch.setenv("README_ROUTE", impl)
     lg = synth.router_logits(T, E, seed=T + E) if kind == "normal" else synth.near_tie_logits(T, E, seed=T + E)
     lg_t = synth.to_torch(lg, ldt)
     ref = oracle.route(lg_t, k)  # the oracle sees exactly the bits the GPU sees
     plan = rd.route(lg_t.to(DEV), k)
     _check_plan(plan, ref, k)
     assert int(plan.dev_status.item()) == 0
+
+
+@pytest.mark.parametrize("impl", [None, "cluster"])
+def test_route_large_batch(rd, monkeypatch, impl):
+    # 300K slots: past the cluster route's default range (lookback), and forced through the cluster route
+    # (each of the 16 CTAs walks ~19 sub-tiles, carrying its running per-expert counts)
+    if impl:
+        monkeypatch.setenv("README_ROUTE", impl)
+    lg = synth.router_logits(150001, 8, seed=5)
+    ref = oracle.route(lg, 2)
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 2)
+    _check_plan(plan, ref, 2)
 
 
 def test_route_locality_runs(rd):
@@ -285,12 +301,16 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("path", ["fused", "split", "unfused", "1cta"])
+@pytest.mark.parametrize("path", ["fused", "lookback", "split", "unfused", "1cta"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
                                            ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
                                            ("bf16", 3000, 1024, 1376, 8, 1)])
 def test_moe_layer_end_to_end(rd, monkeypatch, path, dt, T, H, d, E, k):
-    if path != "fused":
+    # fused: cluster route -> gather dispatch with per-row flags -> single-launch FFN waiting per tile;
+    # lookback: multi-CTA route -> finalize fused into the dispatch -> FFN behind a whole-grid PDL wait
+    if path == "lookback":
+        monkeypatch.setenv("README_ROUTE", "lookback")
+    elif path != "fused":
         monkeypatch.setenv("README_FFN_KERNEL", path)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
     res = synth.to_torch(synth.residual(T, H, seed=12), dt)
