@@ -95,6 +95,13 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
   return README_OK;
 }
 
+// README_DISPATCH=scatter keeps the scatter-form dispatch and the FFN's whole-grid PDL wait (A/B measurement
+// of the gather dispatch with per-row readiness flags, the default)
+bool gather_dispatch() {
+  const char* v = getenv("README_DISPATCH");
+  return !(v && strcmp(v, "scatter") == 0);
+}
+
 // x_sorted row flags inside the FFN workspace (see ffn_layer_ready_bytes)
 uint32_t* ffn_xready(void* ws, int64_t rows, int32_t d, readme_dtype dt) {
   return reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt) + ffn_layer_xready_offset(rows));
@@ -391,7 +398,7 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
       // the fused FFN behind it (PDL) starts each gate/up tile as soon as its rows have landed
       README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                               ws_route, st));
-      xready = pdl;
+      xready = pdl && gather_dispatch();
       if (xready)
         README_TRY(launch_dispatch_gather(x, static_cast<size_t>(H) * dt_size(dt), rows, k, src, x_sorted,
                                           ffn_xready(ws_ffn, rows, d, dt), dev_status, st));
@@ -470,15 +477,28 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
   w += align_up(static_cast<size_t>(rows) * H * dt_size(dt), 256);
   void* h = w;
   w += ffn_ws_bytes(rows, d, dt);
-  if (!src) src = reinterpret_cast<int32_t*>(w);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool own_src = src == nullptr;
+  if (own_src) src = reinterpret_cast<int32_t*>(w);
   // a1-a4 once for the whole stack: the router does not depend on the layer.
   if (logits)
     README_TRY(readme_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                             ws_route, route_ws_bytes(T, E, k), stream));
+  else if (own_src)
+    README_TRY(launch_invert_perm(dest, rows, src, st));  // plan-in with dest only
   const bool pdl = k == 1 && merged_ffn(dt);
   for (int32_t l = 0; l < L; ++l) {
     README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
-    if (pdl) README_TRY(zero_ready(h, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
+    if (pdl && gather_dispatch()) {
+      // pre-norm dispatch in gather form with per-row flags; the FFN behind it starts tiles as rows land
+      README_TRY(zero_ready(h, rows, d, dt, E, st));
+      README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
+      README_TRY(launch_dispatch_rmsnorm_gather(x, dt, rows, H, k, src, eps, x_sorted, ffn_xready(h, rows, d, dt),
+                                                dev_status, st));
+      README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,
+                         dev_status, st, true, true));
+      continue;
+    }
     README_TRY(readme_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status, stream));
     if (k == 1) {  // x <- x + MoE(RMSNorm(x)): the residual add is fused into the down epilogue, in place
       README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,

@@ -21,6 +21,10 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
 // (PDL) waits on those flags per tile instead of on the whole dispatch.
 readme_status launch_dispatch_gather(const void* x, size_t row_bytes, int64_t rows, int32_t k, const int32_t* src,
                                      void* x_sorted, uint32_t* xready, uint32_t* dev_status, cudaStream_t st);
+readme_status launch_dispatch_rmsnorm_gather(const void* x, readme_dtype dt, int64_t rows, int32_t H, int32_t k,
+                                             const int32_t* src, float eps, void* x_sorted, uint32_t* xready,
+                                             uint32_t* dev_status, cudaStream_t st);
+readme_status launch_invert_perm(const int32_t* dest, int64_t n, int32_t* src, cudaStream_t st);  // src = dest^-1
 readme_status launch_set_offsets(int32_t* offs, int32_t T, cudaStream_t st);  // {0, T}
 readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st);  // measurement only
 readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,

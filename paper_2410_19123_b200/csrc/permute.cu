@@ -206,6 +206,63 @@ dispatch_gather_kernel(const uint4* __restrict__ x, int vec, int64_t nrows, int 
   if (trace && threadIdx.x % kWarp == 0) trace_max(trace, 1);
 }
 
+// The stack's pre-norm dispatch in the same gather form (readme_moe_stack with the fused FFN behind it):
+// x_sorted[r] = RMSNorm(x[src[r] / k]) with the row flags of dispatch_gather_kernel. The FFN of the same
+// layer updates x in place (residual fused), but only for rows of m-tiles whose flags it has acquired, i.e.
+// after this kernel has finished reading those tokens (k == 1: one row per token).
+template <typename Elt>
+__global__ void __maxnreg__(64)
+dispatch_rmsnorm_gather_kernel(const Elt* __restrict__ x, int H, int64_t nrows, int k,
+                               const int32_t* __restrict__ src, float eps, Elt* __restrict__ xs,
+                               uint32_t* __restrict__ xready, uint32_t* __restrict__ dev_status) {
+  pdl_launch_dependents();
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kGatherThreads / kWarp);
+  const int groups = H / 8;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(kGatherThreads / kWarp) + threadIdx.x / kWarp; r < nrows;
+       r += warps) {
+    const int32_t sl = __ldg(src + r);
+    if (sl < 0 || sl >= nrows) {
+      if (lane == 0 && dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+    } else {
+      const Elt* row = x + static_cast<int64_t>(sl / k) * H;
+      float ss = 0.f;
+      for (int g = lane; g < groups; g += kWarp) {
+        float v[8];
+        load8_cached(row + g * 8, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      const float rs = rsqrtf(ss / static_cast<float>(H) + eps);
+      Elt* drow = xs + r * H;
+      for (int g = lane; g < groups; g += kWarp) {
+        float v[8];
+        load8_cached(row + g * 8, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] *= rs;
+        store8(drow + g * 8, v);
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(xready + r), "r"(1u) : "memory");
+    }
+  }
+}
+
+// src = dest^-1 (plan-in callers that pass only dest)
+__global__ void invert_perm_kernel(const int32_t* __restrict__ dest, int64_t n, int32_t* __restrict__ src) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = dest[s];
+    if (r >= 0 && r < n) src[r] = static_cast<int32_t>(s);
+  }
+}
+
 // k == 1, no residual: y[t] = y_sorted[dest[t]] (a bit copy; the weight is exactly 1).
 __global__ void __launch_bounds__(kPermThreads)
 gather_kernel(const uint4* __restrict__ ys, int vec, int64_t T, const int32_t* __restrict__ dest,
@@ -302,7 +359,9 @@ void set_dispatch_carveout() {
                          reinterpret_cast<const void*>(finalize_dispatch_kernel),
                          reinterpret_cast<const void*>(dispatch_kernel),
                          reinterpret_cast<const void*>(dispatch_rmsnorm_kernel<__nv_bfloat16>),
-                         reinterpret_cast<const void*>(dispatch_rmsnorm_kernel<float>)};
+                         reinterpret_cast<const void*>(dispatch_rmsnorm_kernel<float>),
+                         reinterpret_cast<const void*>(dispatch_rmsnorm_gather_kernel<__nv_bfloat16>),
+                         reinterpret_cast<const void*>(dispatch_rmsnorm_gather_kernel<float>)};
     for (const void* f : fns)
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaGetLastError();  // a hint only
@@ -345,6 +404,33 @@ readme_status launch_dispatch_gather(const void* x, size_t row_bytes, int64_t ro
 __global__ void debug_mark_kernel(uint64_t* slot) { *slot = globaltimer_ns(); }
 readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st) {
   debug_mark_kernel<<<1, 1, 0, st>>>(slot);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_dispatch_rmsnorm_gather(const void* x, readme_dtype dt, int64_t rows, int32_t H, int32_t k,
+                                             const int32_t* src, float eps, void* x_sorted, uint32_t* xready,
+                                             uint32_t* dev_status, cudaStream_t st) {
+  if (rows == 0) return README_OK;
+  set_dispatch_carveout();
+  const int64_t want = (rows + (kGatherThreads / kWarp) - 1) / (kGatherThreads / kWarp);
+  const int64_t cap = num_sms();
+  const int grid = static_cast<int>(want < cap ? want : cap);
+  if (dt == README_BF16)
+    dispatch_rmsnorm_gather_kernel<__nv_bfloat16><<<grid, kGatherThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), H, rows, k, src, eps, static_cast<__nv_bfloat16*>(x_sorted), xready,
+        dev_status);
+  else
+    dispatch_rmsnorm_gather_kernel<float><<<grid, kGatherThreads, 0, st>>>(
+        static_cast<const float*>(x), H, rows, k, src, eps, static_cast<float*>(x_sorted), xready, dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+readme_status launch_invert_perm(const int32_t* dest, int64_t n, int32_t* src, cudaStream_t st) {
+  if (n == 0) return README_OK;
+  const int64_t want = (n + 255) / 256, cap = 4LL * num_sms();
+  invert_perm_kernel<<<static_cast<int>(want < cap ? want : cap), 256, 0, st>>>(dest, n, src);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

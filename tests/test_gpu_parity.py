@@ -482,8 +482,13 @@ def test_dispatch_rmsnorm(rd, dt, k):
     assert rel_err(_np(xs), ref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
 
 
+@pytest.mark.parametrize("path", ["fused", "split"])
 @pytest.mark.parametrize("dt,k,L", [("bf16", 1, 4), ("bf16", 2, 3), ("f32", 1, 3)])
-def test_moe_stack_end_to_end(rd, dt, k, L):
+def test_moe_stack_end_to_end(rd, monkeypatch, path, dt, k, L):
+    # fused: gather-form pre-norm dispatch with row flags + single-launch FFN (k = 1, bf16); split: the
+    # scatter dispatch + two-launch FFN
+    if path == "split":
+        monkeypatch.setenv("README_FFN_KERNEL", "split")
     T, H, d, E = 600, 256, 256, 8
     x = synth.to_torch(synth.tokens(T, H, seed=161), dt)
     ids = synth.assignments_markov(2, T // 2, E, 0.672, seed=162)
@@ -496,6 +501,18 @@ def test_moe_stack_end_to_end(rd, dt, k, L):
     yref, pref = oracle.moe_stack(x, lg, k, layers)
     _check_plan(plan, pref, k)
     assert rel_err(_np(yg), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+def test_moe_stack_plan_in_equals_routed(rd):
+    T, H, d, E, L = 700, 256, 384, 8, 3
+    x = synth.to_torch(synth.tokens(T, H, seed=181), "bf16").to(DEV)
+    lg = torch.from_numpy(synth.router_logits(T, E, seed=182)).to(DEV)
+    layers = [tuple(synth.to_torch(w, "bf16").to(DEV) for w in synth.expert_weights(E, d, H, seed=183, layer=l))
+              for l in range(L)]
+    y1, plan = rd.moe_stack(x.clone(), layers, logits=lg)
+    y2, _ = rd.moe_stack(x.clone(), layers, plan=plan)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
 
 
 # ---- NEXT-2: expert-aware batching on the GPU serving loop ---------------------------------------------
