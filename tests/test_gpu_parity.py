@@ -470,6 +470,110 @@ def test_config2_full_size_sampled(rd):
     assert rel_err(_np(y)[sample], yb) <= BF16_TOL
 
 
+def _dense_experts(rd, seed):
+    c = synth.CONFIGS[2]
+    H, D, d, E = c["H"], c["D"], c["d"], c["E"]
+    wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
+    S = synth.neuron_sets(E, D, d, seed=seed)
+    dense = [synth.to_torch(w, "bf16") for w in (wg, wu, wd)]
+    del wg, wu, wd
+    eg, eu, ed = rd.build_experts(*(t.to(DEV) for t in dense), torch.from_numpy(S).to(DEV))
+    return dense, S, (eg, eu, ed)
+
+
+@pytest.mark.parametrize("B,s", [(512, 1.0), (64, 2.0)])
+def test_config3_decode_full_shape(rd, B, s):
+    # config 3 as bench.py runs it: Zipf-skewed pre-gated assignments, Llama-2-7B expert shape, the whole
+    # layer captured in a CUDA graph and replayed; routing bit-exact on every token, outputs on 4 sampled
+    # tokens per touched expert by brute force from the dense weights
+    c = synth.CONFIGS[3]
+    H, E = c["H"], c["E"]
+    seed = synth.MASTER_SEED + 2
+    dense, S, (eg, eu, ed) = _dense_experts(rd, seed)
+    ids = synth.assignments_zipf(B, E, s, seed=seed + B)
+    lg = synth.logits_for_assignments(ids, E, seed=B)
+    x = synth.to_torch(synth.tokens(B, H, seed=B), "bf16")
+    xd, lgd = x.to(DEV), torch.from_numpy(lg).to(DEV)
+    plan = rd.new_plan(B, E, 1, DEV)
+    y = torch.empty_like(xd)
+    ws = torch.empty(rd.moe_layer_workspace_bytes(B, H, E, c["d"], 1, torch.bfloat16), dtype=torch.uint8,
+                     device=DEV)
+    fn = lambda: rd.moe_layer(xd, eg, eu, ed, k=1, logits=lgd, plan=plan, out=y, ws=ws)
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    _check_plan(plan, oracle.route(lg, 1), 1)
+    gs = synth.rng(seed, 98)
+    sample = np.concatenate([gs.choice(np.nonzero(ids == e)[0], size=min(4, int((ids == e).sum())), replace=False)
+                             for e in range(E) if (ids == e).any()])
+    yb = oracle.bruteforce(x[sample], lg[sample], 1, *dense, S)
+    assert rel_err(_np(y)[sample], yb) <= BF16_TOL
+
+
+def test_config5_full_size_sampled(rd):
+    # config 5 at G = 1 (T = 65536 on one GPU, the bench's single-GPU line): routing bit-exact on all tokens,
+    # outputs on 4 sampled tokens per expert by brute force from the dense weights
+    c = synth.CONFIGS[5]
+    T, H, E = c["T"], c["H"], c["E"]
+    seed = synth.MASTER_SEED + 2
+    dense, S, (eg, eu, ed) = _dense_experts(rd, seed)
+    x = synth.to_torch(synth.tokens(T, H, seed=seed + 5), "bf16")
+    lg = synth.router_logits(T, E, seed=seed + 5)
+    y, plan = rd.moe_layer(x.to(DEV), eg, eu, ed, logits=torch.from_numpy(lg).to(DEV))
+    torch.cuda.synchronize()
+    pref = oracle.route(lg, 1)
+    _check_plan(plan, pref, 1)
+    idx = pref["topk_idx"][:, 0]
+    gs = synth.rng(seed, 97)
+    sample = np.concatenate([gs.choice(np.nonzero(idx == e)[0], size=4, replace=False) for e in range(E)])
+    yb = oracle.bruteforce(x[sample], lg[sample], 1, *dense, S)
+    assert rel_err(_np(y)[sample], yb) <= BF16_TOL
+
+
+def test_config4_full_size_sampled(rd):
+    # config 4 as bench.py runs it (T = 16384, 32 layers, Markov routing, ONE readme_moe_stack call), then
+    # (i) the same stack as 32 plan-in calls of one layer each is bitwise identical, and (ii) each layer is
+    # teacher-forced against the oracle on sampled tokens: tokens are independent in the MoE-only stack,
+    # so the oracle runs a layer on 2 tokens of each of 2 experts with only that expert's weights
+    c = synth.CONFIGS[4]
+    T, H, d, E, L = c["T"], c["H"], c["d"], c["E"], c["L"]
+    seed = synth.MASTER_SEED + 4
+    layers = [synth.expert_weights_device(E, d, H, DEV, seed=seed, layer=l) for l in range(L)]
+    ids = synth.assignments_markov(T // 4096, 4096, E, 0.672, seed=seed)
+    lg = synth.logits_for_assignments(ids, E, seed=seed)
+    x0 = synth.to_torch(synth.tokens(T, H, seed=seed), "bf16").to(DEV)
+    x = x0.clone()
+    _, plan = rd.moe_stack(x, layers, logits=torch.from_numpy(lg).to(DEV))
+    torch.cuda.synchronize()
+    _check_plan(plan, oracle.route(lg, 1), 1)
+    gs = synth.rng(seed, 96)
+    experts = gs.choice(E, size=2, replace=False)
+    toks = {int(e): gs.choice(np.nonzero(ids == e)[0], size=2, replace=False) for e in experts}
+    xl = x0.clone()
+    worst = 0.0
+    for l in range(L):
+        xin = xl[np.concatenate(list(toks.values()))].cpu()
+        rd.moe_stack(xl, [layers[l]], plan=plan)
+        torch.cuda.synchronize()
+        out = _np(xl)
+        off = 0
+        for e, tk in toks.items():
+            w1 = tuple(w[e:e + 1].cpu() for w in layers[l])
+            lg1 = np.zeros((tk.size, 1), np.float32)
+            yref, _ = oracle.moe_stack(xin[off:off + tk.size], lg1, 1, [w1])
+            err = rel_err(out[tk], yref)
+            worst = max(worst, err)
+            assert err <= BF16_TOL, (l, e, err)
+            off += tk.size
+    assert torch.equal(xl, x)  # one L=32 call == 32 plan-in calls of one layer, bit for bit
+    assert worst > 0.0
+
+
 # ---- config 4: pre-norm dispatch and the route-once stack ----------------------------------------------
 
 @pytest.mark.parametrize("dt,k", [("bf16", 1), ("bf16", 2), ("f32", 1)])
