@@ -715,11 +715,26 @@ def main():
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in out]
 
+    ep_mode, ep_fallback = args.ep, None
     if world > 1:
         from paper_2410_19123_b200 import ep
-        if args.ep == "peer":
-            layer, lg_ep = ep.PeerEPLayer.from_config(cfg, T, dist.group.WORLD, dev)
-
+        layer = None
+        if ep_mode == "peer":
+            # peer-memory EP needs CUDA IPC mappings between the ranks' GPUs; if any rank cannot set them up,
+            # every rank falls back to the NCCL all-to-all path (decided collectively, reported in the line)
+            try:
+                layer, lg_ep = ep.PeerEPLayer.from_config(cfg, T, dist.group.WORLD, dev)
+                ok = 1
+            except Exception as e:  # noqa: BLE001 - any setup failure selects the fallback
+                ok, ep_fallback = 0, f"peer-memory setup failed on rank {rank}: {type(e).__name__}: {e}"[:300]
+            flag = torch.tensor([ok], device=dev, dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                if layer is not None:
+                    layer.close()
+                ep_mode = "nccl"
+                ep_fallback = ep_fallback or "peer-memory setup failed on another rank"
+        if ep_mode == "peer":
             def step_fn():  # route once (+ count exchange on the device), then the fused layer
                 layer.route(lg_ep)
                 layer.layer(residual=True)
@@ -742,7 +757,7 @@ def main():
         step_fn()
     torch.cuda.synchronize()
     eager_fn = step_fn
-    if world == 1 and not args.eager:
+    if (world == 1 or ep_mode == "peer") and not args.eager:
         # The C ABI is stream-ordered and allocation-free, so the whole step captures into one CUDA graph
         # (how a fixed-shape serving step runs); replays remove the per-call host launch cost.
         side = torch.cuda.Stream()
@@ -823,8 +838,9 @@ def main():
                        "T_per_gpu": T, "H": H, "D": cfg["D"], "E": E, "d": d, "k": k,
                        "parallelism": "single" if world == 1 else f"ep{world}",
                        **({} if world == 1 else {"ep_exchange": "peer-memory stores fused into the dispatch kernel "
-                                                 "and the down-GEMM epilogue" if args.ep == "peer" else
+                                                 "and the down-GEMM epilogue" if ep_mode == "peer" else
                                                  "NCCL all_to_all_single"}),
+                       **({"ep_fallback": ep_fallback} if ep_fallback else {}),
                        "l2": "flushed between timed steps (256 MiB write)"}}
     if world == 1:
         med = lambda a: float(np.median(a))
@@ -894,7 +910,18 @@ def main():
     else:
         # peer: route, finalize, publish, (signal, wait) x3, plan, dispatch, FFN = 12; nccl: route, finalize,
         # dispatch, FFN, combine (+ NCCL's own kernels)
-        line["gpu_launches"] = (12 if args.ep == "peer" else 5) * args.steps
+        line["gpu_launches"] = (12 if ep_mode == "peer" else 5) * args.steps
+        line["step_mode"] = "cuda_graph_replay" if (ep_mode == "peer" and not args.eager) else "eager"
+        # whole-step tensor roofline per rank: the rank's expert FFN FLOPs (its experts' rows: T per rank on
+        # average) over the max-over-ranks step time, which also holds the exchange phases
+        f_rank = 6.0 * T * k * H * d
+        ach = f_rank / (ms_per_step * 1e-3) / 1e12
+        line["roofline"] = {"bound": "tensor", "kernel": "whole expert-parallel step per rank (dispatch with the "
+                            "all-to-all, grouped expert FFN with the return all-to-all, flag phases)",
+                            "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                            "frac": ach / pk["bf16_tflops"], "traffic": None,
+                            "algorithmic": f"6*T_rank*k*H*d = {f_rank:.4g} FLOP per rank per step",
+                            "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)"}
     line["clocks"] = clk.summary()
 
     if world == 1 and args.config == 2 and not args.no_variants:
@@ -986,12 +1013,47 @@ def main():
                        "mode": "pipelined over K batches (HostPipeline: H2D / layer / D2H on three streams)",
                        "serial": serial}
 
+    if world > 1 and not args.no_e2e:
+        # e2e at N GPUs through the public API: every step each rank uploads its tokens and logits from
+        # pinned host memory, runs the EP layer, and reads its output back; max over ranks
+        lg_src = lg_ep if ep_mode == "peer" else layer.logits
+        x_src = layer.x
+        x_h = x_src.detach().cpu().pin_memory()
+        lg_h = lg_src.detach().cpu().pin_memory()
+        y_h = torch.empty_like(x_h).pin_memory()
+
+        def e2e_step():
+            x_src.copy_(x_h, non_blocking=True)
+            lg_src.copy_(lg_h, non_blocking=True)
+            out = eager_fn_out()
+            y_h.copy_(out, non_blocking=True)
+
+        def eager_fn_out():
+            if ep_mode == "peer":
+                layer.route(lg_src)
+                return layer.layer(residual=True)
+            return layer.step()
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e_ms = timed(e2e_step, args.steps)
+        dist.barrier()
+        et = torch.tensor([float(sum(e_ms))], device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_per = float(et.item()) / args.steps
+        line["e2e"] = {"value": T * world / (e_per * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": (x_h.numel() * 2 + lg_h.numel() * lg_h.element_size()) * world,
+                       "d2h_bytes_per_step": y_h.numel() * 2 * world, "ms_per_step": e_per,
+                       "mode": "eager, one batch at a time per rank (H2D, route + EP layer, D2H)"}
+
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, inp)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        if args.ep == "peer":
+        if ep_mode == "peer":
             layer.close()
         dist.destroy_process_group()
 
