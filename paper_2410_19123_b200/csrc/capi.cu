@@ -95,11 +95,17 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
   return README_OK;
 }
 
-// README_DISPATCH=scatter keeps the scatter-form dispatch and the FFN's whole-grid PDL wait (A/B measurement
-// of the gather dispatch with per-row readiness flags, the default)
-bool gather_dispatch() {
+// Whether the dispatch runs in gather form with per-row readiness flags (the FFN overlapping it) or in
+// scatter form behind the FFN's whole-grid PDL wait. Gather pays off once the dispatch is long enough to
+// hide (config 2: -1..2 %, config 4: -3.6 %); for decode-sized batches (the dispatch is ~2 MB) the
+// scatter form measured ~3 us (1.5 %) faster per step (globaltimer traces, scripts/trace_lab.py), so it
+// stays below kGatherMinRows. README_DISPATCH=scatter|gather overrides (A/B measurement).
+constexpr int64_t kGatherMinRows = 2048;
+bool gather_dispatch(int64_t rows) {
   const char* v = getenv("README_DISPATCH");
-  return !(v && strcmp(v, "scatter") == 0);
+  if (v && strcmp(v, "scatter") == 0) return false;
+  if (v && strcmp(v, "gather") == 0) return true;
+  return rows >= kGatherMinRows;
 }
 
 // x_sorted row flags inside the FFN workspace (see ffn_layer_ready_bytes)
@@ -398,7 +404,7 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
       // the fused FFN behind it (PDL) starts each gate/up tile as soon as its rows have landed
       README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                               ws_route, st));
-      xready = pdl && gather_dispatch();
+      xready = pdl && gather_dispatch(rows);
       if (xready)
         README_TRY(launch_dispatch_gather(x, static_cast<size_t>(H) * dt_size(dt), rows, k, src, x_sorted,
                                           ffn_xready(ws_ffn, rows, d, dt), dev_status, st));
@@ -489,7 +495,7 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
   const bool pdl = k == 1 && merged_ffn(dt);
   for (int32_t l = 0; l < L; ++l) {
     README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
-    if (pdl && gather_dispatch()) {
+    if (pdl && gather_dispatch(rows)) {
       // pre-norm dispatch in gather form with per-row flags; the FFN behind it starts tiles as rows land
       README_TRY(zero_ready(h, rows, d, dt, E, st));
       README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
@@ -499,6 +505,7 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
                          dev_status, st, true, true));
       continue;
     }
+    if (pdl) README_TRY(zero_ready(h, rows, d, dt, E, st));  // before the dispatch (see zero_ready)
     README_TRY(readme_dispatch_rmsnorm(x, dt, T, H, k, dest, eps, x_sorted, dev_status, stream));
     if (k == 1) {  // x <- x + MoE(RMSNorm(x)): the residual add is fused into the down epilogue, in place
       README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,

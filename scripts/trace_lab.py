@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2410_19123_b200 import readme as rd  # noqa: E402
 
-T, H, E, d = 8192, 4096, 8, 5504
+T, H, E, d = int(os.environ.get("TRACE_T", "8192")), 4096, 8, 5504
 g = torch.Generator(device="cuda").manual_seed(1)
 wg = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wu = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()

@@ -301,15 +301,18 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("path", ["fused", "lookback", "split", "unfused", "1cta"])
+@pytest.mark.parametrize("path", ["fused", "gather", "scatter", "lookback", "split", "unfused", "1cta"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
                                            ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
                                            ("bf16", 3000, 1024, 1376, 8, 1)])
 def test_moe_layer_end_to_end(rd, monkeypatch, path, dt, T, H, d, E, k):
     # fused: cluster route -> gather dispatch with per-row flags -> single-launch FFN waiting per tile;
     # lookback: multi-CTA route -> finalize fused into the dispatch -> FFN behind a whole-grid PDL wait
+    # gather / scatter force the dispatch form (by default gather from 2048 rows up)
     if path == "lookback":
         monkeypatch.setenv("README_ROUTE", "lookback")
+    elif path in ("gather", "scatter"):
+        monkeypatch.setenv("README_DISPATCH", path)
     elif path != "fused":
         monkeypatch.setenv("README_FFN_KERNEL", path)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
@@ -586,13 +589,15 @@ def test_dispatch_rmsnorm(rd, dt, k):
     assert rel_err(_np(xs), ref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
 
 
-@pytest.mark.parametrize("path", ["fused", "split"])
+@pytest.mark.parametrize("path", ["fused", "gather", "split"])
 @pytest.mark.parametrize("dt,k,L", [("bf16", 1, 4), ("bf16", 2, 3), ("f32", 1, 3)])
 def test_moe_stack_end_to_end(rd, monkeypatch, path, dt, k, L):
     # fused: gather-form pre-norm dispatch with row flags + single-launch FFN (k = 1, bf16); split: the
     # scatter dispatch + two-launch FFN
     if path == "split":
         monkeypatch.setenv("README_FFN_KERNEL", "split")
+    elif path == "gather":
+        monkeypatch.setenv("README_DISPATCH", "gather")
     T, H, d, E = 600, 256, 256, 8
     x = synth.to_torch(synth.tokens(T, H, seed=161), dt)
     ids = synth.assignments_markov(2, T // 2, E, 0.672, seed=162)
