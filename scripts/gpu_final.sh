@@ -21,7 +21,7 @@ B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 run ncu_launch 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B
 EXTRA=sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum
 run ncu_ffn 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:ffn_layer2 -s 2 -c 1 -o $O/prof_ffn $B
-run ncu_perm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"route_tile|finalize_dispatch" -s 2 -c 2 -o $O/prof_perm $B
+run ncu_perm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"route_cluster|dispatch_gather" -s 2 -c 2 -o $O/prof_perm $B
 B3="python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 run ncu_dec 900 ncu --set full --metrics $EXTRA --clock-control none -k regex:ffn_layer2 -s 3 -c 1 -o $O/prof_dec $B3
 cat $O/summary.txt
