@@ -1012,6 +1012,22 @@ def main():
                        "d2h_bytes_per_step": y_h.numel() * 2, "ms_per_step": p_ms,
                        "mode": "pipelined over K batches (HostPipeline: H2D / layer / D2H on three streams)",
                        "serial": serial}
+        # the e2e roofline: this step's bytes copied both ways at once on the copy streams, no compute
+        xd2 = torch.empty_like(x_d)
+
+        def copies_only():
+            with torch.cuda.stream(pipe.up):
+                xd2.copy_(x_h, non_blocking=True)
+                lg_d.copy_(lg_h, non_blocking=True)
+            with torch.cuda.stream(pipe.down):
+                y_h.copy_(y_d, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(pipe.up)
+            torch.cuda.current_stream().wait_stream(pipe.down)
+
+        c_ms = float(np.median(timed(copies_only, 5)))
+        line["e2e"]["roofline"] = {"bound": "pcie", "copies_only_ms": c_ms, "frac": c_ms / p_ms,
+                                   "note": "the step's H2D and D2H bytes copied concurrently, nothing else"}
+        del xd2
 
     if world > 1 and not args.no_e2e:
         # e2e at N GPUs through the public API: every step each rank uploads its tokens and logits from
