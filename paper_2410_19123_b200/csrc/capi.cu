@@ -391,7 +391,6 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                      path != FfnPath::kUnfused;
   // the fused single-launch FFN follows the dispatch as a programmatic dependent (PDL)
   const bool pdl = fused && merged_ffn(dt);
-  if (pdl) README_TRY(zero_ready(ws_ffn, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
   bool xready = false;
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
@@ -400,17 +399,24 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
     README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (route_is_single_launch(T, k)) {
-      // a1-a4 in one cluster launch (dest and src final), then a5 in gather form publishing per-row flags:
-      // the fused FFN behind it (PDL) starts each gate/up tile as soon as its rows have landed
-      README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
-                              ws_route, st));
+      // a1-a4 in one cluster launch (dest and src final), which also zeroes the FFN's readiness region (no
+      // memset node). Large batches: a5 in gather form publishing per-row flags, the fused FFN behind it
+      // (PDL) starting each gate/up tile as soon as its rows have landed; small batches: scatter form.
+      // (Running a5 inside the route launch for small batches, with the FFN as the route's programmatic
+      // dependent, measured no faster: the <= 16-CTA cluster copies 2 MB in ~4.5 us.)
+      uint32_t* ready = pdl ? reinterpret_cast<uint32_t*>(static_cast<char*>(ws_ffn) + ffn_h_bytes(rows, d, dt))
+                            : nullptr;
+      const int64_t ready_words = pdl ? static_cast<int64_t>(ffn_layer_ready_bytes(rows, E) / 4) : 0;
       xready = pdl && gather_dispatch(rows);
+      README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
+                              ws_route, st, true, ready, ready_words));
       if (xready)
         README_TRY(launch_dispatch_gather(x, static_cast<size_t>(H) * dt_size(dt), rows, k, src, x_sorted,
                                           ffn_xready(ws_ffn, rows, d, dt), dev_status, st));
       else
         README_TRY(launch_dispatch(x, static_cast<size_t>(H) * dt_size(dt), T, k, dest, x_sorted, dev_status, st));
     } else {
+      if (pdl) README_TRY(zero_ready(ws_ffn, rows, d, dt, E, st));
       // a1-a4 with the finalize (offsets[e] + rank, src) fused into the a5 dispatch pass
       README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                               ws_route, st, /*finalize=*/false));
@@ -418,6 +424,7 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                                           src, x_sorted, st));
     }
   } else {
+    if (pdl) README_TRY(zero_ready(ws_ffn, rows, d, dt, E, reinterpret_cast<cudaStream_t>(stream)));
     README_TRY(readme_dispatch(x, dt, T, H, k, dest, x_sorted, dev_status, stream));
   }
   if (fused) {

@@ -8,7 +8,10 @@ namespace readme {
 size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
-                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize = true);
+                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize = true,
+                           uint32_t* zero = nullptr, int64_t zero_words = 0);
+// zero/zero_words: words the launch zeroes (the FFN's readiness region, so no memset node precedes it; a
+// memset on the multi-CTA path).
 // true when launch_route runs the single-launch cluster route for this batch: it then always finalizes
 // (dest = offsets + rank, src) regardless of `finalize`.
 bool route_is_single_launch(int64_t T, int32_t k);

@@ -366,6 +366,11 @@ constexpr int kCMaxCluster = 16;
 constexpr int64_t kClusterMaxSlots = 256 * 1024;  // beyond: the multi-CTA lookback route
 constexpr int kCMaxSmem = (kMaxLogitFloats + kCWarps * README_MAX_EXPERTS) * 4;  // 64 KB
 
+struct RouteExtra {
+  uint32_t* zero;      // nullable: words zeroed by the launch (the FFN's readiness region)
+  int64_t zero_words;
+};
+
 struct ClusterGeom {
   int C;             // CTAs in the (single) cluster
   int tile_tokens;   // tokens per sub-tile (<= 1024 slots, <= kMaxLogitFloats logits)
@@ -378,9 +383,18 @@ __global__ void __launch_bounds__(kCThreads, 1)
 route_cluster_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k, int tile_tokens, int64_t chunk,
                      int lpt, int items, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                      int32_t* __restrict__ counts, int32_t* __restrict__ offsets, int32_t* __restrict__ dest,
-                     int32_t* __restrict__ src, uint32_t* __restrict__ dev_status, uint64_t* __restrict__ trace) {
+                     int32_t* __restrict__ src, uint32_t* __restrict__ dev_status, uint64_t* __restrict__ trace,
+                     RouteExtra ex) {
   extern __shared__ __align__(16) uint8_t route_smem[];
   if (trace && threadIdx.x == 0) trace_min(trace, 5);
+  if (ex.zero) {  // the FFN's readiness counters / row flags (instead of a memset node before this launch)
+    uint32_t cr, cs;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+    for (int64_t i = static_cast<int64_t>(cr) * kCThreads + threadIdx.x; i < ex.zero_words;
+         i += static_cast<int64_t>(cs) * kCThreads)
+      ex.zero[i] = 0u;
+  }
   float* s_logit = reinterpret_cast<float*>(route_smem);                             // [tile_tokens * E]
   // [kCWarps][E], after the staged logits (lane-group path only)
   int* s_wcount = reinterpret_cast<int*>(route_smem + (NE > 0 ? 0 : sizeof(float) * tile_tokens * E));
@@ -649,7 +663,8 @@ size_t route_ws_bytes(int64_t T, int32_t E, int32_t k) {
 
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
-                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize) {
+                           int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize,
+                           uint32_t* zero, int64_t zero_words) {
   if (T == 0) {
     README_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st));
     README_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), st));
@@ -661,6 +676,7 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
   if (use_cluster_route(T, k)) {
     // one cluster launch: a1-a4 including the finalize (dest = offsets + rank, src)
     const ClusterGeom cg = cluster_geom(T, E, k);
+    RouteExtra ex{zero, zero_words};
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -675,11 +691,12 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
     cfg.numAttrs = 1;
     void* args[] = {const_cast<void**>(&logits), &T, &E, &k, const_cast<int*>(&cg.tile_tokens),
                     const_cast<int64_t*>(&cg.chunk), &lpt, const_cast<int*>(&items), &topk_idx, &topk_w, &counts,
-                    &offsets, &dest, &src, &dev_status, &g_trace_buf};
+                    &offsets, &dest, &src, &dev_status, &g_trace_buf, &ex};
     const void* fn = logits_dt == README_F32 ? cluster_fn<float>(topk_ne(E)) : cluster_fn<__nv_bfloat16>(topk_ne(E));
     README_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
     return README_OK;
   }
+  if (zero && zero_words > 0) README_CUDA(cudaMemsetAsync(zero, 0, sizeof(uint32_t) * zero_words, st));
   RouteGeom g = route_geom(T, E, k);
   uint64_t* status = static_cast<uint64_t*>(ws);
   README_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(g.ntiles) * E * sizeof(uint64_t), st));
