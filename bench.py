@@ -756,6 +756,19 @@ def main():
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
+    if world > 1 and ep_mode == "peer":
+        # a peer-memory exchange that never completes makes readme_ep_wait flag README_DEV_EP_TIMEOUT after
+        # ~10 s instead of hanging; if any rank saw that during warm-up, every rank switches to NCCL
+        bad = torch.tensor([int(layer.dev_status.item()) & rd.README_DEV_EP_TIMEOUT], device=dev, dtype=torch.int32)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()):
+            layer.close()
+            ep_mode, ep_fallback = "nccl", "peer-memory exchange timed out during warm-up (README_DEV_EP_TIMEOUT)"
+            layer = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
+            step_fn = layer.step
+            for _ in range(args.warmup):
+                step_fn()
+            torch.cuda.synchronize()
     eager_fn = step_fn
     if (world == 1 or ep_mode == "peer") and not args.eager:
         # The C ABI is stream-ordered and allocation-free, so the whole step captures into one CUDA graph

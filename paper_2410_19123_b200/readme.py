@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libreadme_b200.so")
 
 README_F32, README_BF16 = 0, 1
 README_DEV_NONFINITE_LOGIT, README_DEV_BAD_INDEX = 0x1, 0x2
+README_DEV_SCHED_TIMEOUT, README_DEV_EP_TIMEOUT = 0x4, 0x8  # include/readme.h
 STATUS = {0: "README_OK", 1: "README_ERR_INVALID_ARG", 2: "README_ERR_UNSUPPORTED", 3: "README_ERR_WORKSPACE",
           4: "README_ERR_CUDA"}
 
