@@ -389,8 +389,8 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   const FfnPath path = ffn_path();
   const bool fused = k == 1 && (src != nullptr || logits != nullptr) && path != FfnPath::k1cta &&
                      path != FfnPath::kUnfused;
-  // the fused single-launch FFN follows the dispatch as a programmatic dependent (PDL)
-  const bool pdl = fused && merged_ffn(dt);
+  // the single-launch FFN follows the dispatch as a programmatic dependent (PDL), fused combine or not
+  const bool pdl = merged_ffn(dt);
   bool xready = false;
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
@@ -435,8 +435,15 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
     return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
                    dev_status, reinterpret_cast<cudaStream_t>(stream), pdl, xready);
   }
-  README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
-                               ffn_ws_bytes(rows, d, dt), stream));
+  if (pdl) {
+    README_CHECK_ARG(aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y_sorted),
+                     "tensors must be 16-byte aligned");
+    README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted,
+                       ws_ffn, dev_status, reinterpret_cast<cudaStream_t>(stream), true, xready));
+  } else {
+    README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
+                                 ffn_ws_bytes(rows, d, dt), stream));
+  }
   return readme_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status, stream);
 }
 
