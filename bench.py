@@ -164,10 +164,16 @@ def cpu_baseline(cfg, inp, budget_s=15.0):
     cap = int(min(np.bincount(idx, minlength=E)))
     n_e = max(1, min(cap, int(budget_s / per_tok / E)))
     dt, n = run(n_e)
+    # the oracle also on ONE thread (results are identical for any thread count), 8 tokens
+    s1 = np.concatenate([g.choice(np.nonzero(idx == e)[0], size=1, replace=False) for e in range(E)])
+    t0 = time.perf_counter()
+    oracle.moe_layer(inp["x"][s1], lg[s1], cfg["k"], eg, eu, ed, nthreads=1)
+    dt1 = time.perf_counter() - t0
     del dense
     return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{n} tokens ({n_e} per expert) of config {cfg['name']}, full layer (route+dispatch+FFN+"
-                      f"combine) in fp64, {dt:.1f} s"}
+                      f"combine) in fp64, {dt:.1f} s",
+            "single_thread": {"value": s1.size / dt1, "unit": UNIT, "sample": f"{s1.size} tokens, {dt1:.1f} s"}}
 
 
 def run_reference(args):
@@ -859,6 +865,17 @@ def main():
         med = lambda a: float(np.median(a))
         line["step_mode"] = "cuda_graph_replay" if not args.eager else "eager"
         line["eager_ms_per_step"] = float(np.mean(eager_ms))
+        # SURVEY §8(d) protocol extras: spread of the timed (cold-L2) steps, and warm steps back to back
+        line["ms_p10_p50_p90"] = [float(np.percentile(step_ms, q)) for q in (10, 50, 90)]
+        warm = []
+        wa = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        wa[0].record()
+        for j in range(args.steps):
+            step_fn()
+            wa[j + 1].record()
+        torch.cuda.synchronize()
+        warm = [wa[j].elapsed_time(wa[j + 1]) for j in range(args.steps)]
+        line["warm_ms_per_step"] = float(np.mean(warm))
         line["stage_ms_median"] = {"step": med(step_ms), "route": med(route_ms), "dispatch": med(disp_ms),
                                    "expert_ffn": med(ffn_ms)}
         f_all, f_gu, f_dn = 6.0 * T * k * H * d, 4.0 * T * k * H * d, 2.0 * T * k * H * d
