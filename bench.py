@@ -314,6 +314,9 @@ def run_decode(args):
                  for B in (64, 128, 256, 512)]
         ids256 = synth.assignments_zipf(256, E, 1.0, seed=synth.MASTER_SEED + 3 + 256)
         st = stages(ids256)
+    # the Zipf exponent swept at B = 256 (s = 0 uniform, 1, 2 skewed)
+    zipf = [dict(measure(synth.assignments_zipf(256, E, s_z, seed=synth.MASTER_SEED + 40 + int(s_z))), s=s_z)
+            for s_z in (0.0, 1.0, 2.0)]
     uniq = [measure(synth.assignments_unique(256, u, E, seed=synth.MASTER_SEED + 30 + u)) for u in range(1, E + 1)]
     us = np.array([r["unique_experts"] for r in uniq], np.float64)
     ts = np.array([r["ms"] for r in uniq]) * 1e3
@@ -404,6 +407,7 @@ def run_decode(args):
                     "ms_per_step": float(np.mean(e_ms))},
             "clocks": clk.summary(),
             "decode_sweep": sweep,
+            "zipf_sweep": zipf,
             "unique_expert_sweep": {"points": uniq, "us_per_extra_expert": float(slope), "intercept_us": float(icpt),
                                     "r2_linear": float(r2), "paper": "linear per-token latency in unique experts "
                                                                    "(PAPER.md:234, fig:batching b)"},
