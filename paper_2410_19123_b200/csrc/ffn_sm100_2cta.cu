@@ -18,6 +18,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -37,11 +38,18 @@ constexpr int kTmemCols = 512;      // two accumulators of 256 columns
 constexpr int kPrefetchK = 32;      // K stages of the first weight tile warmed in L2 before the PDL wait
 constexpr int kXokWords = 64;       // m-tiles whose x readiness is cached in shared memory (2048)
 
-struct __align__(8) Smem {
-  uint8_t a[kStages][kStageA];
-  uint8_t b[kStages][kStageB];
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+// Decode-sized launches use 128-row m-tiles only (M = 128 pair MMAs, 64 A rows per CTA): the A slot halves,
+// so the same ~192 KB ring holds 8 stages instead of 6 — a third more weight bytes in flight per SM.
+constexpr int kStagesD = 8;
+constexpr int kStageAD = 64 * 128;
+constexpr int64_t kDecodeRows = 1024;  // launches up to this many rows use the 128-row m-tile variant
+
+template <int S, int SA>
+struct __align__(8) SmemT {
+  uint8_t a[S][SA];
+  uint8_t b[S][kStageB];
+  uint64_t full[S];
+  uint64_t empty[S];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
@@ -56,7 +64,11 @@ struct __align__(8) Smem {
   uint64_t tq_full[4];   // per CTA: the id in tq[slot] is valid (1 arrival: the leader's producer)
   uint64_t tq_empty[4];  // leader only: every consumer warp of the pair has read tq[slot] (10 arrivals)
 };
+using Smem = SmemT<kStages, kStageA>;
+using SmemD = SmemT<kStagesD, kStageAD>;
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+constexpr size_t kSmemBytesD = sizeof(SmemD) + 1024;
+static_assert(kSmemBytesD <= 232448 && kSmemBytes <= 232448, "shared memory");
 constexpr int kTQ = 4;
 
 struct Tile {
@@ -395,7 +407,8 @@ struct LTile {
   bool m256;
 };
 
-__device__ __forceinline__ LTile decode_ltile(const Smem& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
+template <int kMT, class SM>
+__device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
                                              int& gcur2, int bn1, int bn2) {
   LTile tl;
   int local, g, NT;
@@ -415,12 +428,12 @@ __device__ __forceinline__ LTile decode_ltile(const Smem& s, int t, int nseg, in
   }
   (void)NT;
   const int cnt = s.seg_off[g + 1] - s.seg_off[g];
-  const int mt_g = (cnt + 255) / 256;
+  const int mt_g = (cnt + kMT - 1) / kMT;
   const int nt = local / mt_g, mt = local % mt_g;
   tl.g = g;
   tl.mt = mt;
-  tl.m0 = s.seg_off[g] + mt * 256;
-  tl.rows = min(256, cnt - mt * 256);
+  tl.m0 = s.seg_off[g] + mt * kMT;
+  tl.rows = min(kMT, cnt - mt * kMT);
   tl.m256 = tl.rows > 128;
   tl.n0 = nt * (tl.mode == 0 ? bn1 : bn2);
   return tl;
@@ -435,13 +448,17 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 // kNB = B rows each CTA stages per K step: 128 (default; a gate/up tile covers 128 h columns, a down tile
 // 256 output columns) or 64 (small batches: twice as many, half-width tiles, so every SM streams its
 // share of the touched experts' weights — decode is weight-bandwidth bound).
-template <int kFuse, int kNB>
+template <int kFuse, int kNB, int kMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
                   const __grid_constant__ CUtensorMap tmD, LayerArgs la) {
   extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using SM = typename std::conditional<kMT == 256, Smem, SmemD>::type;
+  constexpr int kS = kMT == 256 ? kStages : kStagesD;     // ring stages
+  constexpr int kSA = kMT == 256 ? kStageA : kStageAD;    // A bytes per stage per CTA
+  static_assert(kMT == 256 || kMT == 128, "kMT");
+  SM& s = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
   const uint32_t cta = tc::cluster_ctarank();
   const bool leader = cta == 0;
@@ -468,7 +485,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (tid == 0) {
     int a1 = 0, a2 = 0, am = 0;
     for (int g = 0; g < nseg; ++g) {
-      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + 255) / 256;
+      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + kMT - 1) / kMT;
       s.tile_start[g] = a1;
       s.tile_start2[g] = a2;
       s.mt_start[g] = am;
@@ -479,7 +496,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     s.tile_start[nseg] = a1;
     s.tile_start2[nseg] = a2;
     s.mt_start[nseg] = am;
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kS; ++i) {
       tc::mbar_init(&s.full[i], 1);
       tc::mbar_init(&s.empty[i], 1);
     }
@@ -506,7 +523,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
       int g1 = 0, g2 = 0;
-      const LTile tl = decode_ltile(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
@@ -563,7 +580,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int j = 0;; ++j) {
       const int t = leader ? produce(j) : consume(j);
       if (t >= ntiles) break;
-      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
@@ -629,7 +646,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           }
         }
         __syncwarp();
-        if (++stage == kStages) {
+        if (++stage == kS) {
           stage = 0;
           phase ^= 1;
         }
@@ -648,7 +665,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       for (int i = 0;; ++i) {
         const int t = consume(i);
         if (t >= ntiles) break;
-        const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -660,7 +677,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           tc::mbar_wait_cluster(&s.full[stage], phase);
           tc::fence_after();
           // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
-          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (kStageA >> 4));
+          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (kSA >> 4));
           const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
           if (tc::elect_one()) {
 #pragma unroll
@@ -670,7 +687,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             tc::commit_2sm_mc(&s.empty[stage], 0x3);
           }
           __syncwarp();
-          if (++stage == kStages) {
+          if (++stage == kS) {
             stage = 0;
             phase ^= 1;
           }
@@ -687,7 +704,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int i = 0;; ++i) {
       const int t = consume(i);
       if (t >= ntiles) break;
-      const LTile tl = decode_ltile(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -1200,15 +1217,20 @@ readme_status set_smem_attr() {
     const void* fns[9] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
                           reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 64>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 64>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 64>)};
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128, 256>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128, 256>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128, 256>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 64, 256>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 64, 256>),
+                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 64, 256>)};
     err[dev] = cudaSuccess;
     for (int i = 0; i < 9 && err[dev] == cudaSuccess; ++i)
       err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    const void* dfns[3] = {reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128, 128>),
+                           reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128, 128>),
+                           reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128, 128>)};
+    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
+      err[dev] = cudaFuncSetAttribute(dfns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytesD));
     const void* wfns[3] = {reinterpret_cast<const void*>(ffn_wide_kernel<0>),
                            reinterpret_cast<const void*>(ffn_wide_kernel<1>),
                            reinterpret_cast<const void*>(ffn_wide_kernel<2>)};
@@ -1261,8 +1283,8 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
 
 // [readiness counters: <= kMaxSeg + #m-tiles + 1][x_sorted row flags: rows] (the flags are used when the
 // gather dispatch precedes the FFN, pdl == 2); one memset zeroes both
-size_t ffn_layer_xready_offset(int64_t rows) {
-  return align_up(static_cast<size_t>(kMaxSeg + (rows + 255) / 256 + 1) * sizeof(uint32_t), 256);
+size_t ffn_layer_xready_offset(int64_t rows) {  // counters sized for 128-row m-tiles (either kMT)
+  return align_up(static_cast<size_t>(kMaxSeg + (rows + 127) / 128 + 1) * sizeof(uint32_t), 256);
 }
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
   (void)nseg;
@@ -1303,7 +1325,12 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   }
   // with pdl the caller zeroed `ready` before the dispatch (a memset here would sit between the two kernels)
   if (!pdl) README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
-  const int64_t mt_ub = nseg + (rows + 255) / 256;
+  // 128-row m-tiles with the 8-stage ring for decode-sized launches (weight streaming: more bytes in flight,
+  // no B reuse to lose); README_FFN_MT=128|256 overrides (A/B measurement)
+  int mt = rows <= kDecodeRows ? 128 : 256;
+  if (const char* v = getenv("README_FFN_MT")) mt = atoi(v) == 128 ? 128 : 256;
+  if (wide || nb == 64) mt = 256;
+  const int64_t mt_ub = nseg + (rows + mt - 1) / mt;
   const int pairs = num_sms() / 2;
   const int64_t tiles = wide ? mt_ub * ((d + 255) / 256 + (H + 511) / 512)
                              : mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
@@ -1314,7 +1341,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   if (const char* v = getenv("README_FFN_DYNAMIC")) dyn = atoi(v) != 0;
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
                expert_slot, {}, {}, 0, 0, pdl ? (xready && !wide ? 2 : 1) : 0, dyn,
-               static_cast<int>(nseg + (rows + 255) / 256), xready, g_trace_buf};
+               static_cast<int>(nseg + (rows + 127) / 128), xready, g_trace_buf};
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
@@ -1331,7 +1358,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = wide ? kWSmemBytes : kSmemBytes;
+  cfg.dynamicSmemBytes = wide ? kWSmemBytes : (mt == 128 ? kSmemBytesD : kSmemBytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1339,7 +1366,9 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
 #define README_LAYER_LAUNCH(F, NB) \
-  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, NB>, mX, mG, mU, mH, mD, la))
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, NB, 256>, mX, mG, mU, mH, mD, la))
+#define README_LAYER_LAUNCH_D(F) \
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, 128, 128>, mX, mG, mU, mH, mD, la))
 #define README_WIDE_LAUNCH(F) \
   README_CUDA(cudaLaunchKernelEx(&cfg, ffn_wide_kernel<F>, mX, mG, mU, mH, mD, la))
   if (wide) {
@@ -1350,12 +1379,17 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
     if (fuse == 2) README_LAYER_LAUNCH(2, 64);
     else if (fuse == 1) README_LAYER_LAUNCH(1, 64);
     else README_LAYER_LAUNCH(0, 64);
+  } else if (mt == 128) {
+    if (fuse == 2) README_LAYER_LAUNCH_D(2);
+    else if (fuse == 1) README_LAYER_LAUNCH_D(1);
+    else README_LAYER_LAUNCH_D(0);
   } else {
     if (fuse == 2) README_LAYER_LAUNCH(2, 128);
     else if (fuse == 1) README_LAYER_LAUNCH(1, 128);
     else README_LAYER_LAUNCH(0, 128);
   }
 #undef README_LAYER_LAUNCH
+#undef README_LAYER_LAUNCH_D
 #undef README_WIDE_LAUNCH
   README_CUDA(cudaGetLastError());
   return README_OK;

@@ -272,11 +272,14 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    # half-width, 256-column, wide-N tiles, and the 256-column tile with dynamic tile fetch
-    for nb, wide, dyn in (("64", "0", "0"), ("128", "0", "0"), ("128", "1", "0"), ("128", "0", "1")):
+    # half-width, 256-column, wide-N tiles, the 256-column tile with dynamic tile fetch, and 128-row vs
+    # 256-row m-tiles (the decode variant with the 8-stage ring)
+    for nb, wide, dyn, mt in (("64", "0", "0", "256"), ("128", "0", "0", "256"), ("128", "1", "0", "256"),
+                              ("128", "0", "1", "256"), ("128", "0", "0", "128"), ("128", "0", "1", "128")):
         monkeypatch.setenv("README_FFN_NB", nb)
         monkeypatch.setenv("README_FFN_WIDE", wide)
         monkeypatch.setenv("README_FFN_DYNAMIC", dyn)
+        monkeypatch.setenv("README_FFN_MT", mt)
         y, _ = rd.moe_layer(x, wg, wu, wd, logits=lg, residual=x)
         plan = rd.route(lg, 1)
         ys = rd.expert_ffn(rd.dispatch(x, plan.dest, 1), plan.offsets, wg, wu, wd)
