@@ -323,6 +323,8 @@ def run_decode(args):
     slope, icpt = np.polyfit(us, ts, 1)
     r2 = 1 - np.sum((ts - (slope * us + icpt)) ** 2) / np.sum((ts - ts.mean()) ** 2)
     from paper_2410_19123_b200 import serving
+    for pol in ("expert_aware", "fifo"):  # warm-up: first-call costs (allocations, module loads) stay out
+        serving.simulate(pol, eg, eu, ed, n_requests=512, max_tokens=256, steps=8, device=dev)
     serve = [serving.simulate(pol, eg, eu, ed, n_requests=512, max_tokens=256, steps=48, device=dev)
              for pol in ("expert_aware", "fifo")]
     # the incremental router (readme_router_step) for the same 256 decode tokens: each request has a cached

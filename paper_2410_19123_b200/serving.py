@@ -50,7 +50,7 @@ def simulate(policy: str, w_gate, w_up, w_down, n_requests: int = 512, max_token
         lg = lg.to(device)
         x = x_pool[torch.from_numpy(req.astype(np.int64)).to(device)]
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(200_000)  # let the host enqueue the whole step first: the events then time the GPU only
+        torch.cuda._sleep(500_000)  # ~0.25 ms: the host enqueues the whole step first, so the events time the GPU only
         a.record()
         y, plan = rd.moe_layer(x, w_gate, w_up, w_down, k=1, logits=lg)
         b.record()
