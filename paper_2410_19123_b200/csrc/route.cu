@@ -693,8 +693,12 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
                     const_cast<int64_t*>(&cg.chunk), &lpt, const_cast<int*>(&items), &topk_idx, &topk_w, &counts,
                     &offsets, &dest, &src, &dev_status, &g_trace_buf, &ex};
     const void* fn = logits_dt == README_F32 ? cluster_fn<float>(topk_ne(E)) : cluster_fn<__nv_bfloat16>(topk_ne(E));
-    README_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
-    return README_OK;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e == cudaSuccess) return README_OK;
+    // the cluster could not be placed (e.g. SMs partitioned away): the multi-CTA route gives the same
+    // result, finalized as the caller expects from the single-launch path
+    cudaGetLastError();
+    finalize = true;
   }
   if (zero && zero_words > 0) README_CUDA(cudaMemsetAsync(zero, 0, sizeof(uint32_t) * zero_words, st));
   RouteGeom g = route_geom(T, E, k);
