@@ -327,6 +327,43 @@ def test_moe_layer_end_to_end(rd, monkeypatch, path, dt, T, H, d, E, k):
     assert rel_err(_np(y), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
 
 
+def _fuzz_cases(n=24, seed=2410):
+    g = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        E = int(g.integers(1, 17))
+        k = int(g.integers(1, min(E, 4) + 1))
+        T = int(g.choice([1, 7, 64, 129, 511, 700, 1025, 2100, 3000]))
+        H = int(8 * g.integers(4, 97))     # 32..768, any multiple of 8
+        d = int(8 * g.integers(2, 81))     # 16..640
+        out.append((T, E, k, H, d))
+    return out
+
+
+@pytest.mark.parametrize("T,E,k,H,d", _fuzz_cases())
+def test_moe_layer_fuzz_bf16(rd, T, E, k, H, d):
+    # seeded random shapes through the default path (cluster route; scatter or gather dispatch by size; the
+    # single-launch FFN with 128- or 256-row m-tiles by size; fused combine for k = 1, combine launch
+    # otherwise) against the oracle: routing bit-exact, outputs within the bf16 rule
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T * 7 + E + H + d)
+    res = synth.to_torch(synth.residual(T, H, seed=T + 3), "bf16")
+    y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k,
+                           logits=torch.from_numpy(lg).to(DEV), residual=res.to(DEV))
+    yref, pref = oracle.moe_layer(x, lg, k, wg, wu, wd, residual=res)
+    _check_plan(plan, pref, k)
+    assert int(plan.dev_status.item()) == 0
+    assert rel_err(_np(y), yref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("T,E,k,H,d", _fuzz_cases(8, seed=19123))
+def test_moe_layer_fuzz_f32(rd, T, E, k, H, d):
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "f32", seed=T * 5 + E + H + d)
+    y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k, logits=torch.from_numpy(lg).to(DEV))
+    yref, pref = oracle.moe_layer(x, lg, k, wg, wu, wd)
+    _check_plan(plan, pref, k)
+    assert rel_err(_np(y), yref) <= F32_TOL
+
+
 def test_moe_layer_plan_in_equals_route(rd):
     T, H, d, E = 800, 256, 256, 8
     x, lg, wg, wu, wd = (t.to(DEV) if isinstance(t, torch.Tensor) else t
