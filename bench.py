@@ -385,6 +385,24 @@ def run_decode(args):
         b.record()
         torch.cuda.synchronize()
         e_ms.append(a.elapsed_time(b))
+    # the same batches streamed through HostPipeline (H2D of batch i+1 and D2H of batch i-1 overlap the layer of
+    # batch i; every batch's bytes still cross PCIe)
+    from paper_2410_19123_b200.pipeline import HostPipeline
+    pipe = HostPipeline(256, H, E, k, eg, eu, ed, device=dev)
+    ys_h = [torch.empty_like(x_h).pin_memory() for _ in range(2)]
+    nb = max(8, args.steps)
+    pipe.run([x_h] * 2, [lg_h] * 2, ys_h)
+    torch.cuda.synchronize()
+    pa = torch.cuda.Event(enable_timing=True)
+    pa.record(pipe.up)
+    last = pipe.run([x_h] * nb, [lg_h] * nb, [ys_h[i % 2] for i in range(nb)])
+    pb = torch.cuda.Event(enable_timing=True)
+    for ev in last:
+        if ev is not None:
+            pipe.down.wait_event(ev)
+    pb.record(pipe.down)
+    torch.cuda.synchronize()
+    p_ms = pa.elapsed_time(pb) / nb
     line = {"metric": METRIC, "value": main_pt["tokens_per_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": main_pt["ms"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -404,9 +422,12 @@ def run_decode(args):
                             "note": "readme_router_step: 256 decode tokens, cached histories uniform in [0, 4096), "
                                     "once per token for all 32 layers; paper: router 1.26-1.50 % of batched step "
                                     "latency (PAPER.md:647)"},
-            "e2e": {"value": 256 / (float(np.mean(e_ms)) * 1e-3), "unit": UNIT,
+            "e2e": {"value": 256 / (p_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": x_h.numel() * 2 + lg_h.numel() * 4, "d2h_bytes_per_step": y_h.numel() * 2,
-                    "ms_per_step": float(np.mean(e_ms))},
+                    "ms_per_step": p_ms,
+                    "mode": "pipelined over K batches (HostPipeline: H2D / layer / D2H on three streams)",
+                    "serial": {"value": 256 / (float(np.mean(e_ms)) * 1e-3), "ms_per_step": float(np.mean(e_ms)),
+                               "note": "one batch at a time: H2D, layer, D2H back to back"}},
             "clocks": clk.summary(),
             "decode_sweep": sweep,
             "zipf_sweep": zipf,
