@@ -391,6 +391,10 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                      path != FfnPath::kUnfused;
   // the single-launch FFN follows the dispatch as a programmatic dependent (PDL), fused combine or not
   const bool pdl = merged_ffn(dt);
+  // every argument check precedes the first launch: an error return leaves no partial step behind
+  README_CHECK_ARG(aligned16(x) && aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y) &&
+                       (!residual || aligned16(residual)),
+                   "x, weights, residual and y must be 16-byte aligned");
   bool xready = false;
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
@@ -429,15 +433,10 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   }
   if (fused) {
     // a6, then a7 with a8 fused into its epilogue: y[src[r]] = residual + h_r W_down^T (k == 1, weight 1).
-    README_CHECK_ARG(aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y) &&
-                         (!residual || aligned16(residual)),
-                     "tensors must be 16-byte aligned");
     return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
                    dev_status, reinterpret_cast<cudaStream_t>(stream), pdl, xready);
   }
   if (pdl) {
-    README_CHECK_ARG(aligned16(w_gate) && aligned16(w_up) && aligned16(w_down) && aligned16(y_sorted),
-                     "tensors must be 16-byte aligned");
     README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted,
                        ws_ffn, dev_status, reinterpret_cast<cudaStream_t>(stream), true, xready));
   } else {
