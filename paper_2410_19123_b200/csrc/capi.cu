@@ -497,6 +497,16 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
   void* h = w;
   w += ffn_ws_bytes(rows, d, dt);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // every argument check precedes the first launch (x is updated in place: no partial stack on an error)
+  README_CHECK_ARG(aligned16(x), "x must be 16-byte aligned");
+  for (int32_t l = 0; l < L; ++l) {
+    README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
+    README_CHECK_ARG(aligned16(w_gate[l]) && aligned16(w_up[l]) && aligned16(w_down[l]),
+                     "layer %d: weights must be 16-byte aligned", l);
+  }
+  if (logits)
+    README_TRY(check_route_call(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, ws_route,
+                                route_ws_bytes(T, E, k)));
   const bool own_src = src == nullptr;
   if (own_src) src = reinterpret_cast<int32_t*>(w);
   // a1-a4 once for the whole stack: the router does not depend on the layer.
@@ -507,11 +517,9 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
     README_TRY(launch_invert_perm(dest, rows, src, st));  // plan-in with dest only
   const bool pdl = k == 1 && merged_ffn(dt);
   for (int32_t l = 0; l < L; ++l) {
-    README_CHECK_ARG(w_gate[l] && w_up[l] && w_down[l], "layer %d: null weight pointer", l);
     if (pdl && gather_dispatch(rows)) {
       // pre-norm dispatch in gather form with per-row flags; the FFN behind it starts tiles as rows land
       README_TRY(zero_ready(h, rows, d, dt, E, st));
-      README_CHECK_ARG(aligned16(x) && aligned16(x_sorted), "x must be 16-byte aligned");
       README_TRY(launch_dispatch_rmsnorm_gather(x, dt, rows, H, k, src, eps, x_sorted, ffn_xready(h, rows, d, dt),
                                                 dev_status, st));
       README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate[l], w_up[l], w_down[l], src, x, x, h,
