@@ -438,7 +438,7 @@ def run_decode(args):
                                                    "(decode- / prefill-prioritized), PAPER.md:426; A100 trace replay",
                             "workload": "512 concurrent requests, MaxTokenLen 256, locality p=0.672, 48 steps, "
                                         "one Llama-2-7B-shape MoE layer per step on the GPU"},
-            "gpu_launches": 3 * args.steps}  # route, finalize+dispatch, expert FFN
+            "gpu_launches": 3 * args.steps}  # route (one cluster launch), dispatch, expert FFN
     print(json.dumps(line), flush=True)
 
 
@@ -484,7 +484,8 @@ def run_tiny(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config1_tiny", "T": T, "H": H, "E": E, "d": d, "k": k,
                        "note": "latency-bound (12.6 MFLOP); graph replay", "l2": "flushed between steps"},
-            "latency_us": t * 1e3, "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+            "latency_us": t * 1e3, "gpu_launches": 4 * args.steps,  # route, dispatch, fp32 gate/up, fp32 down
+            "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
 
@@ -565,7 +566,7 @@ def run_stack(args):
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                          "traffic": None, "algorithmic": f"L*6*T*k*H*d = {flops:.4g} FLOP per step",
                          "peak_source": f"{pk_src} bf16 sustained (a ~80 ms step)"},
-            "gpu_launches": (2 + 2 * L) * args.steps, "clocks": clk.summary()}  # route+finalize, L x (norm-dispatch, FFN)
+            "gpu_launches": (1 + 2 * L) * args.steps, "clocks": clk.summary()}  # route, L x (norm-dispatch, FFN)
     print(json.dumps(line), flush=True)
 
 
@@ -963,11 +964,11 @@ def main():
                        "note": "readme_dispatch is on the step; readme_combine is the standalone entry (inside "
                                "readme_moe_layer, k=1, it is fused into the down GEMM epilogue); graph-replayed at "
                                "8x config-2 rows, L2 flushed"}
-        line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + finalize/dispatch + expert FFN (+combine)
+        line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + dispatch + expert FFN (+combine)
     else:
-        # peer: route, finalize, publish, (signal, wait) x3, plan, dispatch, FFN = 12; nccl: route, finalize,
-        # dispatch, FFN, combine (+ NCCL's own kernels)
-        line["gpu_launches"] = (12 if ep_mode == "peer" else 5) * args.steps
+        # peer: route, publish, (signal, wait) x3, plan, dispatch, FFN = 11; nccl: route, dispatch, FFN,
+        # combine (+ NCCL's own kernels)
+        line["gpu_launches"] = (11 if ep_mode == "peer" else 4) * args.steps
         line["step_mode"] = "cuda_graph_replay" if (ep_mode == "peer" and not args.eager) else "eager"
         # whole-step tensor roofline per rank: the rank's expert FFN FLOPs (its experts' rows: T per rank on
         # average) over the max-over-ranks step time, which also holds the exchange phases
