@@ -12,21 +12,22 @@ import synth  # noqa: E402
 from paper_2410_19123_b200 import readme as rd  # noqa: E402
 
 T, H, E, d = int(os.environ.get("TRACE_T", "8192")), 4096, 8, 5504
+K = int(os.environ.get("TRACE_K", "1"))
 g = torch.Generator(device="cuda").manual_seed(1)
 wg = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wu = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wd = (torch.randn(E, H, d, device="cuda", generator=g) / 74).bfloat16()
 x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
 lg = torch.from_numpy(synth.router_logits(T, E, seed=3)).cuda()
-plan = rd.new_plan(T, E, 1, "cuda")
-ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, 1, torch.bfloat16), dtype=torch.uint8, device="cuda")
+plan = rd.new_plan(T, E, K, "cuda")
+ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, K, torch.bfloat16), dtype=torch.uint8, device="cuda")
 y = torch.empty_like(x)
 tr = torch.zeros(16, dtype=torch.int64, device="cuda")
 MAXU = -1  # all ones as int64
 
 
 def run():
-    rd.moe_layer(x, wg, wu, wd, k=1, logits=lg, plan=plan, out=y, ws=ws)
+    rd.moe_layer(x, wg, wu, wd, k=K, logits=lg, plan=plan, out=y, ws=ws)
 
 
 GRAPH = os.environ.get("TRACE_GRAPH", "1") == "1"
