@@ -280,8 +280,8 @@ def run_decode(args):
                 "GBps": byts / (t * 1e-3) / 1e9, "hbm_frac": byts / (t * 1e-3) / 1e9 / pk["hbm_gbs"]}
 
     def stages(ids):
-        """Live per-kernel breakdown of one decode step (eager, events between the launches, L2 flushed):
-        route | dispatch | expert FFN (the dominant kernel, whose roofline the line reports)."""
+        """Live per-kernel breakdown of one decode step (per-stage graph replays, events between them, L2
+        flushed): route | dispatch | expert FFN (the dominant kernel, whose roofline the line reports)."""
         B = ids.shape[0]
         lg = torch.from_numpy(synth.logits_for_assignments(ids, E, seed=B)).to(dev)
         x = synth.to_torch(synth.tokens(B, H, seed=B), "bf16").to(dev)
@@ -297,6 +297,19 @@ def run_decode(args):
             for f in fns:
                 f()
         torch.cuda.synchronize()
+        if not args.eager:
+            # each stage as its own CUDA graph (as config 2 does): the events between them then time the
+            # kernels, not the host-side argument marshalling and tensor-map encoding of an eager call
+            graphs = []
+            for f in fns:
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph):
+                    f()
+                graphs.append(gph)
+            fns = [gph.replay for gph in graphs]
+            for f in fns:
+                f()
+            torch.cuda.synchronize()
         rows = []
         for _ in range(args.steps):
             flush.zero_()
