@@ -12,14 +12,17 @@ namespace readme {
 
 namespace {
 
-constexpr int kTm = 32, kTn = 32, kTk = 32;
+constexpr int kTm = 32, kTn = 32;
 constexpr int kMaxSeg = 512;
 
+// K per staged block: the whole K of the tiny config in as few serial load rounds as shared memory allows
+// (64 with three operand tiles, 128 with two)
 template <bool kSwiGLU>
 __global__ void __launch_bounds__(256)
 ffn_f32_kernel(const float* __restrict__ A, int64_t rows, int K, int N, int E, int nseg,
                const int32_t* __restrict__ offsets, const float* __restrict__ B0, const float* __restrict__ B1,
                float* __restrict__ C, const int32_t* __restrict__ src, const float* __restrict__ residual) {
+  constexpr int kTk = kSwiGLU ? 64 : 128;
   __shared__ int s_off[kMaxSeg + 1];
   __shared__ int s_tstart[kMaxSeg + 1];
   __shared__ float sA[kTm][kTk + 1];
@@ -52,11 +55,15 @@ ffn_f32_kernel(const float* __restrict__ A, int64_t rows, int K, int N, int E, i
   float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
   for (int k0 = 0; k0 < K; k0 += kTk) {
     for (int i = ty; i < kTm; i += 8) {
-      const int64_t r = r0 + i;
-      sA[i][tx] = (r < rend && k0 + tx < K) ? A[r * K + k0 + tx] : 0.f;
-      const int n = n0 + i;
-      sB0[i][tx] = (n < N && k0 + tx < K) ? Be0[static_cast<int64_t>(n) * K + k0 + tx] : 0.f;
-      if constexpr (kSwiGLU) sB1[i][tx] = (n < N && k0 + tx < K) ? Be1[static_cast<int64_t>(n) * K + k0 + tx] : 0.f;
+#pragma unroll
+      for (int cc = tx; cc < kTk; cc += kTn) {
+        const int64_t r = r0 + i;
+        sA[i][cc] = (r < rend && k0 + cc < K) ? A[r * K + k0 + cc] : 0.f;
+        const int n = n0 + i;
+        sB0[i][cc] = (n < N && k0 + cc < K) ? Be0[static_cast<int64_t>(n) * K + k0 + cc] : 0.f;
+        if constexpr (kSwiGLU)
+          sB1[i][cc] = (n < N && k0 + cc < K) ? Be1[static_cast<int64_t>(n) * K + k0 + cc] : 0.f;
+      }
     }
     __syncthreads();
     const int kk = min(kTk, K - k0);
