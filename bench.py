@@ -563,6 +563,37 @@ def run_stack(args):
         rms.append((a, b))
     torch.cuda.synchronize()
     router_ms = float(np.mean([a.elapsed_time(b) for a, b in rms]))
+    e2e = None
+    if not args.no_e2e:
+        # e2e through the public API: the step's tokens and logits from pinned host memory, the 32-layer
+        # stack, the result back to pinned host memory — one batch at a time (the PCIe copies are ~5 % of a
+        # ~60 ms step, so no pipelining)
+        x_h = x0.cpu().pin_memory()
+        lg_h = lg.cpu().pin_memory()
+        y_h = torch.empty_like(x_h).pin_memory()
+        lg_d = torch.empty_like(lg)
+
+        def e2e_step():
+            x.copy_(x_h, non_blocking=True)
+            lg_d.copy_(lg_h, non_blocking=True)
+            rd.moe_stack(x, layers, k=k, logits=lg_d, plan=plan, ws=ws)
+            y_h.copy_(x, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ems = []
+        for _ in range(max(2, args.steps)):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            e2e_step()
+            b.record()
+            ems.append((a, b))
+        torch.cuda.synchronize()
+        e_ms = float(np.mean([a.elapsed_time(b) for a, b in ems]))
+        e2e = {"value": T / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": x_h.numel() * 2 + lg_h.numel() * 4,
+               "d2h_bytes_per_step": y_h.numel() * 2, "ms_per_step": e_ms,
+               "mode": "one batch at a time: H2D, 32-layer stack, D2H"}
     pk, pk_src = peaks()
     flops = L * 6.0 * T * k * H * d
     ach = flops / (t * 1e-3) / 1e12
@@ -580,6 +611,8 @@ def run_stack(args):
                          "traffic": None, "algorithmic": f"L*6*T*k*H*d = {flops:.4g} FLOP per step",
                          "peak_source": f"{pk_src} bf16 sustained (a ~80 ms step)"},
             "gpu_launches": (1 + 2 * L) * args.steps, "clocks": clk.summary()}  # route, L x (norm-dispatch, FFN)
+    if e2e is not None:
+        line["e2e"] = e2e
     print(json.dumps(line), flush=True)
 
 
