@@ -364,6 +364,18 @@ def test_moe_layer_fuzz_f32(rd, T, E, k, H, d):
     assert rel_err(_np(y), yref) <= F32_TOL
 
 
+@pytest.mark.parametrize("T,E,k,H,d", [(8192, 64, 1, 512, 256), (4096, 128, 2, 256, 128), (3000, 256, 1, 128, 64)])
+def test_moe_layer_many_experts(rd, T, E, k, H, d):
+    # fine-grained expert counts (up to README_MAX_EXPERTS = 256 segments): many empty and one-row experts,
+    # 128-row tails everywhere
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=E + T)
+    y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k, logits=torch.from_numpy(lg).to(DEV))
+    yref, pref = oracle.moe_layer(x, lg, k, wg, wu, wd)
+    _check_plan(plan, pref, k)
+    assert int(plan.dev_status.item()) == 0
+    assert rel_err(_np(y), yref) <= BF16_TOL
+
+
 def test_moe_layer_plan_in_equals_route(rd):
     T, H, d, E = 800, 256, 256, 8
     x, lg, wg, wu, wd = (t.to(DEV) if isinstance(t, torch.Tensor) else t
