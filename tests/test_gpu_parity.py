@@ -376,6 +376,23 @@ def test_moe_layer_many_experts(rd, T, E, k, H, d):
     assert rel_err(_np(y), yref) <= BF16_TOL
 
 
+@pytest.mark.parametrize("T,sub", [(1500, 700), (4096, 512), (3000, 2100)])
+def test_batch_invariance_bitwise(rd, T, sub):
+    """P13: a token's output does not depend on the other tokens of its batch — bitwise, across batch sizes
+    that take different paths (128- vs 256-row m-tiles at <= / > 1024 rows, scatter vs gather dispatch at
+    < / >= 2048 rows): no split-K, the K order of every output element is fixed."""
+    H, d, E = 512, 384, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=T + sub)
+    W = tuple(w.to(DEV) for w in (wg, wu, wd))
+    xd, lgd = x.to(DEV), torch.from_numpy(lg).to(DEV)
+    y_all, _ = rd.moe_layer(xd, *W, logits=lgd, residual=xd)
+    idx = torch.from_numpy(synth.rng(T, 95).choice(T, size=sub, replace=False).astype(np.int64)).to(DEV)
+    xs_, lgs_ = xd[idx].contiguous(), lgd[idx].contiguous()
+    y_sub, _ = rd.moe_layer(xs_, *W, logits=lgs_, residual=xs_)
+    torch.cuda.synchronize()
+    assert torch.equal(y_all[idx], y_sub)
+
+
 def test_moe_layer_plan_in_equals_route(rd):
     T, H, d, E = 800, 256, 256, 8
     x, lg, wg, wu, wd = (t.to(DEV) if isinstance(t, torch.Tensor) else t
