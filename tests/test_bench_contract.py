@@ -37,3 +37,26 @@ def test_reference_arm_only_rank0_prints():
     assert p.returncode == 0, p.stderr[-2000:]
     lines = _json_lines(p.stdout)
     assert len(lines) == 1 and lines[0]["impl"] == "reference"
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_default_json_line_gpu():
+    """The driver's default run (config 2, N = 1): one line with roofline, clocks, e2e (real PCIe bytes),
+    cpu_baseline and the launch count of the product kernels."""
+    p = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert (KEYS - {"impl"}) <= set(d) and {"roofline", "clocks", "gpu_launches"} <= set(d)
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "tensor" and 0 < r["frac"] <= 1.2 and r["peak"] > 0 and r["achieved"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert d["gpu_launches"] >= 3 * d["steps"]
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
