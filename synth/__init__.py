@@ -178,6 +178,7 @@ def logits_for_assignments(ids: np.ndarray, E: int, margin: float = 0.5,
     rows = np.arange(ids.shape[0])
     lg[rows, ids] = -np.inf
     top = lg.max(axis=1)
+    top[~np.isfinite(top)] = 0.0  # E == 1: no runner-up
     lg[rows, ids] = top + np.float32(margin) + np.abs(normal((ids.shape[0],), seed, TID_LOGITS + 50))
     return lg.astype(np.float32)
 

@@ -46,3 +46,11 @@ def test_near_tie_logits_have_ties():
     lg = synth.near_tie_logits(256, 8)
     srt = np.sort(lg, axis=1)
     assert np.sum(srt[:, -1] == srt[:, -2]) > 10
+
+
+def test_logits_for_assignments_finite_and_argmax():
+    for E in (1, 2, 8):
+        ids = synth.assignments_zipf(257, E, 2.0, seed=3)
+        lg = synth.logits_for_assignments(ids, E, seed=3)
+        assert np.isfinite(lg).all()
+        assert np.array_equal(lg.argmax(axis=1), ids)
