@@ -400,6 +400,7 @@ struct LayerArgs {
   int sched;
   const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
+  int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (README_FFN_ASKIP)
 };
 
 struct LTile {
@@ -584,7 +585,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128);
+      // A tile of ≤ 64 rows: every row the second CTA would stage is past the tile's end, so it skips its A
+      // load (its MMA rows read stale shared memory; row m of the product depends on A row m only and rows
+      // past tl.rows are never stored). README_FFN_ASKIP=0 loads them anyway (A/B).
+      const bool a_skip = la.askip && !tl.m256 && tl.rows <= 64;
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128) -
+                             (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
       if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
         // padding: their products are never stored, so they are not waited for)
@@ -635,7 +641,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
           const int k0 = kb * kBK;
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
-          tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
+          if (!(a_skip && cta == 1)) tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
           if (tl.mode == 0) {  // kNB/2 rows of W_gate then the same rows of W_up (box height kNB/2)
             tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nrg, e);
@@ -1342,6 +1348,8 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
                expert_slot, {}, {}, 0, 0, pdl ? (xready && !wide ? 2 : 1) : 0, dyn,
                static_cast<int>(nseg + (rows + 127) / 128), xready, g_trace_buf};
+  la.askip = 1;
+  if (const char* v = getenv("README_FFN_ASKIP")) la.askip = atoi(v) != 0;
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {

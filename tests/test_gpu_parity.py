@@ -272,10 +272,13 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    # half-width, 256-column, wide-N tiles, the 256-column tile with dynamic tile fetch, and 128-row vs
-    # 256-row m-tiles (the decode variant with the 8-stage ring)
-    for nb, wide, dyn, mt in (("64", "0", "0", "256"), ("128", "0", "0", "256"), ("128", "1", "0", "256"),
-                              ("128", "0", "1", "256"), ("128", "0", "0", "128"), ("128", "0", "1", "128")):
+    # half-width, 256-column, wide-N tiles, the 256-column tile with dynamic tile fetch, 128-row vs
+    # 256-row m-tiles, and the second CTA loading its (unused) A rows of tiles of <= 64 rows or not
+    for nb, wide, dyn, mt, askip in (("64", "0", "0", "256", "1"), ("128", "0", "0", "256", "1"),
+                                     ("128", "1", "0", "256", "1"), ("128", "0", "1", "256", "1"),
+                                     ("128", "0", "0", "128", "1"), ("128", "0", "1", "128", "1"),
+                                     ("128", "0", "0", "128", "0"), ("128", "0", "0", "256", "0")):
+        monkeypatch.setenv("README_FFN_ASKIP", askip)
         monkeypatch.setenv("README_FFN_NB", nb)
         monkeypatch.setenv("README_FFN_WIDE", wide)
         monkeypatch.setenv("README_FFN_DYNAMIC", dyn)
