@@ -1337,7 +1337,10 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   if (const char* v = getenv("README_FFN_MT")) mt = atoi(v) == 128 ? 128 : 256;
   if (wide || nb == 64) mt = 256;
   const int64_t mt_ub = nseg + (rows + mt - 1) / mt;
-  const int pairs = num_sms() / 2;
+  int pairs = num_sms() / 2;
+  // README_FFN_PAIRS=n: at most n CTA pairs (measurement of placement-limited grids, e.g. 66 pairs = the
+  // 132 SMs that 4-CTA clusters place on)
+  if (const char* v = getenv("README_FFN_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(v)));
   const int64_t tiles = wide ? mt_ub * ((d + 255) / 256 + (H + 511) / 512)
                              : mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
