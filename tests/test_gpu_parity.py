@@ -274,10 +274,16 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
     outs = []
     # half-width, 256-column, wide-N tiles, the 256-column tile with dynamic tile fetch, 128-row vs
     # 256-row m-tiles, and the second CTA loading its (unused) A rows of tiles of <= 64 rows or not
-    for nb, wide, dyn, mt, askip in (("64", "0", "0", "256", "1"), ("128", "0", "0", "256", "1"),
-                                     ("128", "1", "0", "256", "1"), ("128", "0", "1", "256", "1"),
-                                     ("128", "0", "0", "128", "1"), ("128", "0", "1", "128", "1"),
-                                     ("128", "0", "0", "128", "0"), ("128", "0", "0", "256", "0")):
+    for cfg in (("64", "0", "0", "256", "1"), ("128", "0", "0", "256", "1"),
+                ("128", "1", "0", "256", "1"), ("128", "0", "1", "256", "1"),
+                ("128", "0", "0", "128", "1"), ("128", "0", "1", "128", "1"),
+                ("128", "0", "0", "128", "0"), ("128", "0", "0", "256", "0"),
+                ("128", "0", "0", "256", "1", "3"), ("128", "0", "0", "128", "1", "1")):
+        # optional 6th field: at most that many CTA pairs (every pair walks a long tile list; the down tiles
+        # wait on gate/up tiles of the same few pairs)
+        pairs = cfg[5] if len(cfg) > 5 else "1000"
+        nb, wide, dyn, mt, askip = cfg[:5]
+        monkeypatch.setenv("README_FFN_PAIRS", pairs)
         monkeypatch.setenv("README_FFN_ASKIP", askip)
         monkeypatch.setenv("README_FFN_NB", nb)
         monkeypatch.setenv("README_FFN_WIDE", wide)
