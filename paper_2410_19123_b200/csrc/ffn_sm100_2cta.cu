@@ -401,6 +401,7 @@ struct LayerArgs {
   const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
   int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (README_FFN_ASKIP)
+  int order;               // lab: 1 = gate/up tiles N-tile fastest (README_FFN_ORDER)
 };
 
 struct LTile {
@@ -410,7 +411,7 @@ struct LTile {
 
 template <int kMT, class SM>
 __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
-                                             int& gcur2, int bn1, int bn2) {
+                                             int& gcur2, int bn1, int bn2, bool nfast = false) {
   LTile tl;
   int local, g, NT;
   if (t < T1) {
@@ -427,10 +428,12 @@ __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int 
     tl.mode = 1;
     NT = NT2;
   }
-  (void)NT;
   const int cnt = s.seg_off[g + 1] - s.seg_off[g];
   const int mt_g = (cnt + kMT - 1) / kMT;
-  const int nt = local / mt_g, mt = local % mt_g;
+  // m-tile fastest (default: consecutive pairs share a weight tile) or, for gate/up tiles with nfast (lab
+  // knob README_FFN_ORDER=1), N-tile fastest (consecutive pairs share an A tile)
+  const bool nf = nfast && tl.mode == 0;
+  const int nt = nf ? local % NT : local / mt_g, mt = nf ? local / NT : local % mt_g;
   tl.g = g;
   tl.mt = mt;
   tl.m0 = s.seg_off[g] + mt * kMT;
@@ -524,7 +527,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
       int g1 = 0, g2 = 0;
-      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
@@ -581,7 +584,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int j = 0;; ++j) {
       const int t = leader ? produce(j) : consume(j);
       if (t >= ntiles) break;
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
@@ -671,7 +674,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       for (int i = 0;; ++i) {
         const int t = consume(i);
         if (t >= ntiles) break;
-        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -710,7 +713,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int i = 0;; ++i) {
       const int t = consume(i);
       if (t >= ntiles) break;
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -1353,6 +1356,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                static_cast<int>(nseg + (rows + 127) / 128), xready, g_trace_buf};
   la.askip = 1;
   if (const char* v = getenv("README_FFN_ASKIP")) la.askip = atoi(v) != 0;
+  if (const char* v = getenv("README_FFN_ORDER")) la.order = atoi(v);
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {

@@ -278,11 +278,14 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
                 ("128", "1", "0", "256", "1"), ("128", "0", "1", "256", "1"),
                 ("128", "0", "0", "128", "1"), ("128", "0", "1", "128", "1"),
                 ("128", "0", "0", "128", "0"), ("128", "0", "0", "256", "0"),
-                ("128", "0", "0", "256", "1", "3"), ("128", "0", "0", "128", "1", "1")):
+                ("128", "0", "0", "256", "1", "3"), ("128", "0", "0", "128", "1", "1"),
+                ("128", "0", "0", "256", "1", "1000", "1"), ("128", "0", "1", "128", "1", "1000", "1")):
         # optional 6th field: at most that many CTA pairs (every pair walks a long tile list; the down tiles
-        # wait on gate/up tiles of the same few pairs)
+        # wait on gate/up tiles of the same few pairs); 7th: gate/up tiles in N-tile-fastest order
         pairs = cfg[5] if len(cfg) > 5 else "1000"
+        order = cfg[6] if len(cfg) > 6 else "0"
         nb, wide, dyn, mt, askip = cfg[:5]
+        monkeypatch.setenv("README_FFN_ORDER", order)
         monkeypatch.setenv("README_FFN_PAIRS", pairs)
         monkeypatch.setenv("README_FFN_ASKIP", askip)
         monkeypatch.setenv("README_FFN_NB", nb)
