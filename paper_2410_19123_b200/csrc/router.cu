@@ -30,12 +30,21 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// One warp per token: h0 = Emb[id] (copied to the residual stream), a = RMSNorm(h0) * g.
+// One warp per token: h0 = Emb[id] (copied to the residual stream), a = RMSNorm(h0) * g. The grid also
+// writes the one-segment table offs = {0, T} of the block's GEMMs and zeroes the MLP FFN's readiness words
+// (so neither needs a launch of its own).
 __global__ void router_embed_norm_kernel(const int32_t* __restrict__ ids, int64_t T, int V,
                                          const __nv_bfloat16* __restrict__ emb, const __nv_bfloat16* __restrict__ g,
                                          float eps, __nv_bfloat16* __restrict__ h0, __nv_bfloat16* __restrict__ a,
-                                         uint32_t* __restrict__ dev_status) {
+                                         uint32_t* __restrict__ dev_status, int32_t* __restrict__ offs,
+                                         uint32_t* __restrict__ zero, int64_t zero_words) {
   const int lane = threadIdx.x % kWarp;
+  const int64_t gtid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t i = gtid; i < zero_words; i += static_cast<int64_t>(gridDim.x) * blockDim.x) zero[i] = 0u;
+  if (gtid == 0) {
+    offs[0] = 0;
+    offs[1] = static_cast<int32_t>(T);
+  }
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x / kWarp) + threadIdx.x / kWarp;
   if (t >= T) return;
   int id = ids[t];
@@ -519,8 +528,9 @@ readme_status router_tail(int64_t T, const RouterWeights& w, float eps, float* l
   // h2 = h1 + MLP(RMSNorm_2(h1)): the SwiGLU MLP is an expert FFN with one segment (E = 1, d = 512)
   rmsnorm512_kernel<<<gblocks, 32 * wpb, 0, st>>>(h1, T, w.g2, eps, a);
   README_CUDA(cudaGetLastError());
+  // `ready` was zeroed by the embed launch (pdl = true: no memset node; the FFN waits on the RMSNorm grid)
   README_TRY(launch_ffn_layer_2cta(a, T, kD, 1, kD, 1, offs, w.wg, w.wu, w.wd, hff, h2, nullptr, h1, ready,
-                                   dev_status, st));
+                                   dev_status, st, nullptr, 0, nullptr, true, nullptr));
   router_head_kernel<<<gblocks, 32 * wpb, w.n_experts * kD * sizeof(float), st>>>(h2, T, w.gf, w.whead,
                                                                                    w.n_experts, eps, logits);
   README_CUDA(cudaGetLastError());
@@ -554,11 +564,12 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   int32_t* ntiles = reinterpret_cast<int32_t*>(p); p += 256;
   auto* hff = reinterpret_cast<__nv_bfloat16*>(p); p += act;
   uint32_t* ready = reinterpret_cast<uint32_t*>(p);
+  const int64_t zero_words = static_cast<int64_t>(ffn_layer_ready_bytes(T, 1) / sizeof(uint32_t));
 
   const int wpb = 8;
   const unsigned gblocks = static_cast<unsigned>((T + wpb - 1) / wpb);
-  README_TRY(launch_set_offsets(offs, static_cast<int32_t>(T), st));
-  router_embed_norm_kernel<<<gblocks, 32 * wpb, 0, st>>>(ids, T, w.vocab, w.emb, w.g1, eps, h0, a, dev_status);
+  router_embed_norm_kernel<<<gblocks, 32 * wpb, 0, st>>>(ids, T, w.vocab, w.emb, w.g1, eps, h0, a, dev_status,
+                                                         offs, ready, zero_words);
   README_CUDA(cudaGetLastError());
   // q | k | v = a . Wqkv^T (tcgen05 CTA-pair GEMM over one segment)
   README_TRY(launch_gemm_2cta(1, a, T, kD, 3 * kD, 1, 1, offs, w.wqkv, nullptr, qkv, nullptr, nullptr, st));
@@ -596,13 +607,14 @@ readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* s
   p += 2 * tiles_b + 256;
   auto* hff = reinterpret_cast<__nv_bfloat16*>(p); p += act;
   uint32_t* ready = reinterpret_cast<uint32_t*>(p);
+  const int64_t zero_words = static_cast<int64_t>(ffn_layer_ready_bytes(n, 1) / sizeof(uint32_t));
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + router_ws_bytes(n, 1));
   const int nchunk = (max_len + kChunk - 1) / kChunk;
 
   const int wpb = 8;
   const unsigned gblocks = static_cast<unsigned>((n + wpb - 1) / wpb);
-  README_TRY(launch_set_offsets(offs, static_cast<int32_t>(n), st));
-  router_embed_norm_kernel<<<gblocks, 32 * wpb, 0, st>>>(ids, n, w.vocab, w.emb, w.g1, eps, h0, a, dev_status);
+  router_embed_norm_kernel<<<gblocks, 32 * wpb, 0, st>>>(ids, n, w.vocab, w.emb, w.g1, eps, h0, a, dev_status,
+                                                         offs, ready, zero_words);
   README_CUDA(cudaGetLastError());
   README_TRY(launch_gemm_2cta(1, a, n, kD, 3 * kD, 1, 1, offs, w.wqkv, nullptr, qkv, nullptr, nullptr, st));
   // every new token's k/v reach the cache before any attention of this call reads it (causal within the
