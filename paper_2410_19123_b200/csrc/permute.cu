@@ -12,6 +12,7 @@
 #include <mutex>
 
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace readme {
 
@@ -61,6 +62,72 @@ dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, con
     }
     copy_row<U>(x + (s / k) * vec, xs + static_cast<int64_t>(r) * vec, vec, lane);
   }
+}
+
+// Scatter dispatch through the bulk-copy engine (large batches): each of kBulkCopiers single-thread copiers
+// per CTA streams its rows global -> shared -> global with cp.async.bulk — a ring of kBulkSlots whole rows,
+// loads completing on per-slot mbarriers, stores tracked as bulk groups — so one thread keeps several 8 KB
+// rows in flight instead of a warp of 16-byte loads. Rows are byte copies (bit-exact).
+constexpr int kBulkCopiers = 4;
+constexpr int kBulkSlots = 4;
+constexpr size_t kBulkMaxSmem = 192 * 1024;
+
+__device__ __forceinline__ void bulk_load_row(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_row(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src_smem))), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kBulkCopiers * kWarp)
+dispatch_bulk_kernel(const uint8_t* __restrict__ x, uint32_t row_bytes, int64_t nslots, int k,
+                     const int32_t* __restrict__ dest, uint8_t* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+  pdl_launch_dependents();
+  extern __shared__ __align__(128) uint8_t bulk_ring[];
+  __shared__ __align__(8) uint64_t bar[kBulkCopiers][kBulkSlots];
+  const int copier = threadIdx.x / kWarp;
+  if (threadIdx.x % kWarp != 0) return;  // one thread per copier; its warp's other lanes have no work
+  uint8_t* ring = bulk_ring + static_cast<size_t>(copier) * kBulkSlots * row_bytes;
+  uint64_t* b = bar[copier];
+  for (int i = 0; i < kBulkSlots; ++i) tc::mbar_init(&b[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kBulkCopiers + copier;
+  const int64_t nc = static_cast<int64_t>(gridDim.x) * kBulkCopiers;
+  const int64_t mine = c < nslots ? (nslots - 1 - c) / nc + 1 : 0;
+  auto load = [&](int64_t j) {
+    const int slot = static_cast<int>(j % kBulkSlots);
+    const int64_t s = c + j * nc;
+    tc::mbar_expect_tx(&b[slot], row_bytes);
+    bulk_load_row(ring + static_cast<size_t>(slot) * row_bytes, x + (s / k) * static_cast<int64_t>(row_bytes),
+                  row_bytes, &b[slot]);
+  };
+  for (int64_t j = 0; j < mine && j < kBulkSlots; ++j) load(j);
+  for (int64_t j = 0; j < mine; ++j) {
+    const int slot = static_cast<int>(j % kBulkSlots);
+    const int64_t s = c + j * nc;
+    const int32_t r = __ldg(dest + s);
+    tc::mbar_wait(&b[slot], static_cast<uint32_t>(j / kBulkSlots) & 1u);
+    if (r < 0 || r >= nslots) {
+      if (dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
+    } else {
+      bulk_store_row(xs + static_cast<int64_t>(r) * row_bytes, ring + static_cast<size_t>(slot) * row_bytes,
+                     row_bytes);
+    }
+    if (j + kBulkSlots < mine) {
+      // the slot is refilled once this row's store has read it out of shared memory
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(j + kBulkSlots);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
@@ -384,6 +451,14 @@ int perm_unroll(bool gather) {
   return gather ? 8 : 4;
 }
 
+// Bulk-copy scatter dispatch for batches of >= 4096 slots whose 16-row ring fits in shared memory;
+// README_DISPATCH_BULK=0|1 overrides (A/B measurement).
+bool use_bulk_dispatch(int64_t nslots, size_t row_bytes) {
+  if (row_bytes % 16 != 0 || static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes > kBulkMaxSmem) return false;
+  if (const char* v = getenv("README_DISPATCH_BULK")) return atoi(v) != 0;
+  return nslots >= 4096;
+}
+
 int grid_for_rows(int64_t rows) {
   set_dispatch_carveout();
   const int64_t want = (rows + (kPermThreads / kWarp) - 1) / (kPermThreads / kWarp);
@@ -397,6 +472,23 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st) {
   const int64_t nslots = T * k;
   if (nslots == 0) return README_OK;
+  if (use_bulk_dispatch(nslots, row_bytes)) {
+    const size_t smem = static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes;
+    static std::once_flag once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    std::call_once(once[dev], [] {
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(dispatch_bulk_kernel),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBulkMaxSmem));
+    });
+    const int64_t want = (nslots + kBulkCopiers - 1) / kBulkCopiers;
+    const int64_t cap = num_sms();
+    dispatch_bulk_kernel<<<static_cast<int>(want < cap ? want : cap), kBulkCopiers * kWarp, smem, st>>>(
+        static_cast<const uint8_t*>(x), static_cast<uint32_t>(row_bytes), nslots, k, dest,
+        static_cast<uint8_t*>(x_sorted), dev_status);
+    README_CUDA(cudaGetLastError());
+    return README_OK;
+  }
   if (perm_unroll(false) == 8)
     dispatch_kernel<8><<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
         static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,

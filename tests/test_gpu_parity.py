@@ -136,8 +136,10 @@ def test_route_deterministic(rd):
 
 # ---- a5 dispatch / a8 combine -----------------------------------------------------------------------
 
+# >= 4096 slots take the bulk-copy kernel (rows of <= 12 KiB), the rest the warp-per-row kernel
 @pytest.mark.parametrize("T,H,k,dt", [(1000, 4096, 1, "bf16"), (333, 264, 2, "bf16"), (256, 64, 1, "f32"),
-                                      (100, 72, 3, "f32")])
+                                      (100, 72, 3, "f32"), (5000, 4096, 1, "bf16"), (2100, 264, 2, "bf16"),
+                                      (4500, 72, 1, "f32"), (1500, 1032, 3, "f32"), (4100, 4096, 1, "f32")])
 def test_dispatch_bit_exact(rd, T, H, k, dt):
     x = synth.to_torch(synth.tokens(T, H, seed=T), dt)
     ref_plan = oracle.route(synth.router_logits(T, 8, seed=T + 1), k)
@@ -145,6 +147,27 @@ def test_dispatch_bit_exact(rd, T, H, k, dt):
     xs = rd.dispatch(x.to(DEV), dest, k)
     ref = oracle.dispatch(x, ref_plan["dest"], k)
     assert np.array_equal(_np(xs).astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("bulk", ["0", "1"])
+def test_dispatch_bad_index_flagged(rd, monkeypatch, bulk):
+    """An out-of-range dest entry is flagged in dev_status and skipped; every other row still lands."""
+    monkeypatch.setenv("README_DISPATCH_BULK", bulk)
+    T, H = 6000, 256
+    x = synth.to_torch(synth.tokens(T, H, seed=5), "bf16").to(DEV)
+    dest = torch.from_numpy(np.random.default_rng(6).permutation(T).astype(np.int32)).to(DEV)
+    bad = 1234
+    lost = int(dest[bad].item())
+    dest[bad] = T + 7
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    out = torch.zeros((T, H), dtype=torch.bfloat16, device=DEV)
+    rd.dispatch(x, dest, 1, out=out, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & rd.README_DEV_BAD_INDEX
+    keep = torch.ones(T, dtype=torch.bool, device=DEV)
+    keep[bad] = False
+    assert torch.equal(out[dest[keep].long()], x[keep])
+    assert torch.count_nonzero(out[lost]) == 0
 
 
 def test_combine_k1_is_bit_gather(rd):
