@@ -64,8 +64,8 @@ dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, int k, con
   }
 }
 
-// Scatter dispatch through the bulk-copy engine (large batches): each of kBulkCopiers single-thread copiers
-// per CTA streams its rows global -> shared -> global with cp.async.bulk — a ring of kBulkSlots whole rows,
+// Row moves through the bulk-copy engine (large batches): each of kBulkCopiers single-thread copiers per CTA
+// streams its rows global -> shared -> global with cp.async.bulk — a ring of kBulkSlots whole rows,
 // loads completing on per-slot mbarriers, stores tracked as bulk groups — so one thread keeps several 8 KB
 // rows in flight instead of a warp of 16-byte loads. Rows are byte copies (bit-exact).
 constexpr int kBulkCopiers = 4;
@@ -86,9 +86,12 @@ __device__ __forceinline__ void bulk_store_row(void* dst, const void* src_smem, 
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// kGather = false: scatter dispatch, row s of x_sorted's input x[s / k] goes to x_sorted[dest[s]];
+// kGather = true: the k = 1 combine without residual, y[t] = y_sorted[dest[t]] (rows = T, k = 1).
+template <bool kGather>
 __global__ void __launch_bounds__(kBulkCopiers * kWarp)
-dispatch_bulk_kernel(const uint8_t* __restrict__ x, uint32_t row_bytes, int64_t nslots, int k,
-                     const int32_t* __restrict__ dest, uint8_t* __restrict__ xs, uint32_t* __restrict__ dev_status) {
+move_rows_bulk_kernel(const uint8_t* __restrict__ in, uint32_t row_bytes, int64_t nslots, int k,
+                      const int32_t* __restrict__ dest, uint8_t* __restrict__ out, uint32_t* __restrict__ dev_status) {
   pdl_launch_dependents();
   extern __shared__ __align__(128) uint8_t bulk_ring[];
   __shared__ __align__(8) uint64_t bar[kBulkCopiers][kBulkSlots];
@@ -102,11 +105,17 @@ dispatch_bulk_kernel(const uint8_t* __restrict__ x, uint32_t row_bytes, int64_t 
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kBulkCopiers + copier;
   const int64_t nc = static_cast<int64_t>(gridDim.x) * kBulkCopiers;
   const int64_t mine = c < nslots ? (nslots - 1 - c) / nc + 1 : 0;
+  auto valid = [&](int32_t r) { return r >= 0 && r < nslots; };
   auto load = [&](int64_t j) {
     const int slot = static_cast<int>(j % kBulkSlots);
     const int64_t s = c + j * nc;
+    int64_t src_row = s / k;
+    if constexpr (kGather) {
+      const int32_t r = __ldg(dest + s);
+      src_row = valid(r) ? r : 0;  // a bad index still fills the slot (row 0); its store is skipped
+    }
     tc::mbar_expect_tx(&b[slot], row_bytes);
-    bulk_load_row(ring + static_cast<size_t>(slot) * row_bytes, x + (s / k) * static_cast<int64_t>(row_bytes),
+    bulk_load_row(ring + static_cast<size_t>(slot) * row_bytes, in + src_row * static_cast<int64_t>(row_bytes),
                   row_bytes, &b[slot]);
   };
   for (int64_t j = 0; j < mine && j < kBulkSlots; ++j) load(j);
@@ -115,11 +124,11 @@ dispatch_bulk_kernel(const uint8_t* __restrict__ x, uint32_t row_bytes, int64_t 
     const int64_t s = c + j * nc;
     const int32_t r = __ldg(dest + s);
     tc::mbar_wait(&b[slot], static_cast<uint32_t>(j / kBulkSlots) & 1u);
-    if (r < 0 || r >= nslots) {
+    if (!valid(r)) {
       if (dev_status) atomicOr(dev_status, README_DEV_BAD_INDEX);
     } else {
-      bulk_store_row(xs + static_cast<int64_t>(r) * row_bytes, ring + static_cast<size_t>(slot) * row_bytes,
-                     row_bytes);
+      bulk_store_row(out + (kGather ? s : static_cast<int64_t>(r)) * row_bytes,
+                     ring + static_cast<size_t>(slot) * row_bytes, row_bytes);
     }
     if (j + kBulkSlots < mine) {
       // the slot is refilled once this row's store has read it out of shared memory
@@ -451,12 +460,32 @@ int perm_unroll(bool gather) {
   return gather ? 8 : 4;
 }
 
-// Bulk-copy scatter dispatch for batches of >= 4096 slots whose 16-row ring fits in shared memory;
-// README_DISPATCH_BULK=0|1 overrides (A/B measurement).
-bool use_bulk_dispatch(int64_t nslots, size_t row_bytes) {
+// Bulk-copy row moves (scatter dispatch; k = 1 combine without residual) for >= 4096 rows whose 16-row
+// ring fits in shared memory; README_DISPATCH_BULK / README_COMBINE_BULK = 0|1 override (A/B measurement).
+bool use_bulk_moves(int64_t rows, size_t row_bytes, const char* env) {
   if (row_bytes % 16 != 0 || static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes > kBulkMaxSmem) return false;
-  if (const char* v = getenv("README_DISPATCH_BULK")) return atoi(v) != 0;
-  return nslots >= 4096;
+  if (const char* v = getenv(env)) return atoi(v) != 0;
+  return rows >= 4096;
+}
+
+template <bool kGather>
+readme_status launch_move_rows_bulk(const void* in, size_t row_bytes, int64_t rows, int32_t k, const int32_t* dest,
+                                    void* out, uint32_t* dev_status, cudaStream_t st) {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [] {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(move_rows_bulk_kernel<kGather>),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBulkMaxSmem));
+  });
+  const size_t smem = static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes;
+  const int64_t want = (rows + kBulkCopiers - 1) / kBulkCopiers;
+  const int64_t cap = num_sms();
+  move_rows_bulk_kernel<kGather><<<static_cast<int>(want < cap ? want : cap), kBulkCopiers * kWarp, smem, st>>>(
+      static_cast<const uint8_t*>(in), static_cast<uint32_t>(row_bytes), rows, k, dest, static_cast<uint8_t*>(out),
+      dev_status);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
 }
 
 int grid_for_rows(int64_t rows) {
@@ -472,23 +501,8 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st) {
   const int64_t nslots = T * k;
   if (nslots == 0) return README_OK;
-  if (use_bulk_dispatch(nslots, row_bytes)) {
-    const size_t smem = static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes;
-    static std::once_flag once[64];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
-    std::call_once(once[dev], [] {
-      cudaFuncSetAttribute(reinterpret_cast<const void*>(dispatch_bulk_kernel),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBulkMaxSmem));
-    });
-    const int64_t want = (nslots + kBulkCopiers - 1) / kBulkCopiers;
-    const int64_t cap = num_sms();
-    dispatch_bulk_kernel<<<static_cast<int>(want < cap ? want : cap), kBulkCopiers * kWarp, smem, st>>>(
-        static_cast<const uint8_t*>(x), static_cast<uint32_t>(row_bytes), nslots, k, dest,
-        static_cast<uint8_t*>(x_sorted), dev_status);
-    README_CUDA(cudaGetLastError());
-    return README_OK;
-  }
+  if (use_bulk_moves(nslots, row_bytes, "README_DISPATCH_BULK"))
+    return launch_move_rows_bulk<false>(x, row_bytes, nslots, k, dest, x_sorted, dev_status, st);
   if (perm_unroll(false) == 8)
     dispatch_kernel<8><<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
         static_cast<const uint4*>(x), static_cast<int>(row_bytes / 16), nslots, k, dest,
@@ -585,6 +599,8 @@ readme_status launch_combine(const void* y_sorted, readme_dtype dt, int64_t T, i
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
                              uint32_t* dev_status, cudaStream_t st) {
   if (T == 0) return README_OK;
+  if (k == 1 && residual == nullptr && use_bulk_moves(T, static_cast<size_t>(H) * dt_size(dt), "README_COMBINE_BULK"))
+    return launch_move_rows_bulk<true>(y_sorted, static_cast<size_t>(H) * dt_size(dt), T, 1, dest, y, dev_status, st);
   const int grid = grid_for_rows(T);
   if (k == 1 && residual == nullptr) {
     if (perm_unroll(true) == 8)

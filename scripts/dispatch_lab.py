@@ -1,6 +1,6 @@
-"""readme_dispatch alone (scatter form) at T rows x H = 4096 bf16 under env variants (e.g.
-README_DISPATCH_BULK=0,1), CUDA-graph replays, L2 flushed before each; GB/s = 2 * rows * H * 2 / time.
-Measurement only. Usage: python scripts/dispatch_lab.py VAR=a,b [T1 T2 ...]"""
+"""readme_dispatch alone (scatter form; LAB_OP=combine: readme_combine, k = 1 gather) at T rows x H = 4096
+bf16 under env variants (e.g. README_DISPATCH_BULK=0,1), CUDA-graph replays, L2 flushed before each;
+GB/s = 2 * rows * H * 2 / time. Measurement only. Usage: python scripts/dispatch_lab.py VAR=a,b [T1 T2 ...]"""
 import json
 import os
 import sys
@@ -24,7 +24,10 @@ for T in Ts:
     ref = None
     for v in vals:
         os.environ[var] = v
-        fn = lambda: rd.dispatch(x, plan.dest, 1, out=xs)
+        if os.environ.get("LAB_OP") == "combine":
+            fn = lambda: rd.combine(x, plan.dest, None, 1, out=xs)
+        else:
+            fn = lambda: rd.dispatch(x, plan.dest, 1, out=xs)
         fn()
         torch.cuda.synchronize()
         if ref is None:

@@ -170,9 +170,30 @@ def test_dispatch_bad_index_flagged(rd, monkeypatch, bulk):
     assert torch.count_nonzero(out[lost]) == 0
 
 
-def test_combine_k1_is_bit_gather(rd):
-    T, H = 2000, 4096
-    ys = synth.to_torch(synth.tokens(T, H, seed=3), "bf16").to(DEV)
+@pytest.mark.parametrize("bulk", ["0", "1"])
+def test_combine_k1_bad_index_flagged(rd, monkeypatch, bulk):
+    """k = 1 gather combine: an out-of-range dest entry is flagged and its output row left untouched."""
+    monkeypatch.setenv("README_COMBINE_BULK", bulk)
+    T, H = 6000, 256
+    ys = synth.to_torch(synth.tokens(T, H, seed=7), "bf16").to(DEV)
+    dest = torch.from_numpy(np.random.default_rng(8).permutation(T).astype(np.int32)).to(DEV)
+    dest[77] = -3
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    y = torch.zeros((T, H), dtype=torch.bfloat16, device=DEV)
+    rd.combine(ys, dest, None, 1, out=y, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & rd.README_DEV_BAD_INDEX
+    keep = torch.ones(T, dtype=torch.bool, device=DEV)
+    keep[77] = False
+    assert torch.equal(y[keep], ys[dest[keep].long()])
+    assert torch.count_nonzero(y[77]) == 0
+
+
+@pytest.mark.parametrize("T,H,dt", [(2000, 4096, "bf16"), (5000, 4096, "bf16"), (4200, 264, "bf16"),
+                                    (4500, 1032, "f32"), (4100, 4096, "f32")])
+def test_combine_k1_is_bit_gather(rd, T, H, dt):
+    """>= 4096 rows take the bulk-copy kernel (rows of <= 12 KiB), the rest the warp-per-row kernel."""
+    ys = synth.to_torch(synth.tokens(T, H, seed=3), dt).to(DEV)
     plan = oracle.route(synth.router_logits(T, 8, seed=4), 1)
     y = rd.combine(ys, torch.from_numpy(plan["dest"]).to(DEV), None, 1)
     ys_np = _np(ys)
