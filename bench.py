@@ -1014,9 +1014,10 @@ def main():
         cg = comb_bytes / (med(comb_ms) * 1e-3) / 1e9
         line["hbm"] = {"dispatch_GBps": dg, "combine_GBps": cg, "peak_GBps": hbm, "dispatch_frac": dg / hbm,
                        "combine_frac": cg / hbm, "rows": Tb * k,
-                       "note": "readme_dispatch is on the step; readme_combine is the standalone entry (inside "
-                               "readme_moe_layer, k=1, it is fused into the down GEMM epilogue); graph-replayed at "
-                               "8x config-2 rows, L2 flushed"}
+                       "note": "standalone entries readme_dispatch (scatter) and readme_combine (k=1 gather), "
+                               "both bulk-copy row moves at this size; inside readme_moe_layer the dispatch is the "
+                               "gather form overlapped with the FFN and the k=1 combine is fused into the down GEMM "
+                               "epilogue; graph-replayed at 8x config-2 rows, L2 flushed"}
         line["gpu_launches"] = (3 if k == 1 else 4) * args.steps  # route + dispatch + expert FFN (+combine)
     else:
         # peer: route, publish, (signal, wait) x3, plan, dispatch, FFN = 11; nccl: route, dispatch, FFN,
