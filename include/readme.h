@@ -60,7 +60,9 @@ typedef enum { README_F32 = 0, README_BF16 = 1 } readme_dtype;
 
 #define README_DEV_NONFINITE_LOGIT 0x1u /* some logit was NaN/Inf (Q3: NaN ranks as -inf) */
 #define README_DEV_BAD_INDEX 0x2u       /* a caller-supplied plan held an id/row out of range */
-#define README_DEV_SCHED_TIMEOUT 0x4u   /* the single-launch expert FFN could not co-schedule its CTA pairs */
+#define README_DEV_SCHED_TIMEOUT 0x4u   /* the single-launch expert FFN could not co-schedule its CTA pairs: a
+                                          readiness wait gave up, and every output element is then either its
+                                          correct value or left untouched (never computed from unready rows) */
 #define README_DEV_EP_TIMEOUT 0x8u      /* readme_ep_wait gave up on a peer (~10 s) instead of hanging */
 
 #define README_MAX_EXPERTS 256
@@ -106,12 +108,17 @@ readme_status readme_dispatch(const void* x, readme_dtype dt, int64_t T, int32_t
  * bf16: tcgen05 tensor cores, fp32 accumulation in TMEM, fp32 SiLU, h rounded once to bf16 (Q11), y
  *       rounded once to bf16; requires H % 8 == 0 and d % 8 == 0.
  * f32:  CUDA-core FMA in fp32 (no TF32), for the tiny config.
- * Segments with no rows read no weights. ws: readme_expert_ffn_workspace_bytes(...) bytes. */
+ * Segments with no rows read no weights. ws: readme_expert_ffn_workspace_bytes(...) bytes.
+ * bf16 runs a6 and a7 in ONE persistent launch whose down tiles wait on other CTA pairs' gate/up tiles; its
+ * grid never exceeds the CTA pairs that can be co-resident (cudaOccupancyMaxActiveClusters). If SMs are
+ * held elsewhere (another stream or process) for seconds, a wait gives up: README_DEV_SCHED_TIMEOUT is
+ * OR-ed into dev_status (nullable) and the launch stores nothing more, so every element of y_sorted is
+ * either correct or untouched. */
 size_t readme_expert_ffn_workspace_bytes(int64_t rows, int32_t H, int32_t E, int32_t d, readme_dtype dt);
 readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
                                 int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
-                                const void* w_up, const void* w_down, void* y_sorted, void* ws,
-                                size_t ws_bytes, readme_stream_t stream);
+                                const void* w_up, const void* w_down, void* y_sorted, uint32_t* dev_status,
+                                void* ws, size_t ws_bytes, readme_stream_t stream);
 
 /* a6 alone: h = silu(x_sorted W_gate[e]^T) * (x_sorted W_up[e]^T) per segment; h [rows,d] of dtype dt (bf16 h is
  * rounded once, Q11). Same arguments as readme_expert_ffn; no workspace. */
@@ -182,11 +189,12 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
  *     y[t] <- y[t] + F_perm(x[t]),   F_perm(x) = W_down,p (silu(W_gate,p x) * (W_up,p x))   for EVERY token,
  * added in place to y (call it after readme_moe_layer). w_gate/w_up [d_perm,H], w_down [H,d_perm] of dtype
  * dt; runs the same grouped-GEMM kernels over one segment of T rows (no dispatch: token order), with the
- * add fused into the down projection's epilogue. ws: readme_permanent_expert_workspace_bytes(...). */
+ * add fused into the down projection's epilogue. ws: readme_permanent_expert_workspace_bytes(...).
+ * dev_status (nullable): README_DEV_SCHED_TIMEOUT as for readme_expert_ffn. */
 size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_perm, readme_dtype dt);
 readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t d_perm,
-                                      const void* w_gate, const void* w_up, const void* w_down, void* y, void* ws,
-                                      size_t ws_bytes, readme_stream_t stream);
+                                      const void* w_gate, const void* w_up, const void* w_down, void* y,
+                                      uint32_t* dev_status, void* ws, size_t ws_bytes, readme_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* The pre-gating router G (NEXT-1 of SURVEY §8(f)): PAPER.md:130-133 (§2.3, "one transformer block with
@@ -355,6 +363,17 @@ void readme_debug_trace(void* dev_buf);
 /* Measurement only: store %globaltimer into slot `slot` (8..15) of the registered trace buffer from a
    one-thread kernel on `stream`. README_ERR_INVALID_ARG without a buffer or for another slot. */
 readme_status readme_debug_mark(int32_t slot, readme_stream_t stream);
+/* Lab / test switches that select measured-slower kernel variants for A/B measurement (DESIGN.md §6 lists
+   every name, its values and its default). Each is read once from its README_* environment variable at the
+   first launch; set_knob overrides it for the whole process (not thread-safe against running launches),
+   reset_knob restores the environment's value. README_ERR_INVALID_ARG for an unknown name. */
+readme_status readme_debug_set_knob(const char* name, int32_t value);
+/* Test only: occupy n_ctas SMs (one CTA per SM, maximum shared memory) for ns nanoseconds on `stream`, so
+   a kernel launched behind it on another stream finds only the remaining SMs (the co-residency tests of
+   the single-launch expert FFN). */
+readme_status readme_debug_hold_sms(int32_t n_ctas, int64_t ns, readme_stream_t stream);
+readme_status readme_debug_get_knob(const char* name, int32_t* value);
+readme_status readme_debug_reset_knob(const char* name);
 
 #ifdef __cplusplus
 }

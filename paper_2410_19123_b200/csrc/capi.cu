@@ -72,17 +72,13 @@ size_t ffn_ws_bytes(int64_t rows, int32_t d, readme_dtype dt) {
   return ffn_h_bytes(rows, d, dt) + ffn_layer_ready_bytes(rows, 512) + 256;
 }
 
-// Which bf16 kernel family runs the expert FFN: the single-launch CTA-pair kernel by default;
-// README_FFN_KERNEL=split (two CTA-pair launches), =1cta (two single-CTA launches) or =unfused
-// (split, and no fused combine in readme_moe_layer) for A/B measurement.
-enum class FfnPath { kMerged, kSplit, k1cta, kUnfused };
+// Which bf16 kernel family runs the expert FFN: the single-launch CTA-pair kernel by default; knob
+// ffn_kernel = 1 (split: two CTA-pair launches) or 2 (unfused: split, and no fused combine in
+// readme_moe_layer) for A/B measurement.
+enum class FfnPath { kMerged, kSplit, kUnfused };
 FfnPath ffn_path() {
-  const char* v = getenv("README_FFN_KERNEL");
-  if (!v) return FfnPath::kMerged;
-  if (strcmp(v, "split") == 0) return FfnPath::kSplit;
-  if (strcmp(v, "1cta") == 0) return FfnPath::k1cta;
-  if (strcmp(v, "unfused") == 0) return FfnPath::kUnfused;
-  return FfnPath::kMerged;
+  const int v = knob(Knob::kFfnKernel);
+  return v == 1 ? FfnPath::kSplit : (v == 2 ? FfnPath::kUnfused : FfnPath::kMerged);
 }
 
 // a6 + a7 (+ fused a8 when src != null) over the workspace `ws` (ffn_ws_bytes).
@@ -99,12 +95,12 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
 // scatter form behind the FFN's whole-grid PDL wait. Gather pays off once the dispatch is long enough to
 // hide (config 2: -1..2 %, config 4: -3.6 %); for decode-sized batches (the dispatch is ~2 MB) the
 // scatter form measured ~3 us (1.5 %) faster per step (globaltimer traces, scripts/trace_lab.py), so it
-// stays below kGatherMinRows. README_DISPATCH=scatter|gather overrides (A/B measurement).
+// stays below kGatherMinRows. Knob dispatch = 1 (scatter) | 2 (gather) overrides (A/B measurement).
 constexpr int64_t kGatherMinRows = 2048;
 bool gather_dispatch(int64_t rows) {
-  const char* v = getenv("README_DISPATCH");
-  if (v && strcmp(v, "scatter") == 0) return false;
-  if (v && strcmp(v, "gather") == 0) return true;
+  const int v = knob(Knob::kDispatch);
+  if (v == 1) return false;
+  if (v == 2) return true;
   return rows >= kGatherMinRows;
 }
 
@@ -167,6 +163,12 @@ void readme_debug_trace(void* dev_buf) { g_trace_buf = static_cast<uint64_t*>(de
 readme_status readme_debug_mark(int32_t slot, readme_stream_t stream) {
   README_CHECK_ARG(g_trace_buf != nullptr && slot >= 8 && slot < 16, "no trace buffer, or slot not in [8, 16)");
   return launch_debug_mark(g_trace_buf + slot, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Test only: hold n_ctas SMs (one CTA each, maximum shared memory) for ns nanoseconds on `stream`.
+readme_status readme_debug_hold_sms(int32_t n_ctas, int64_t ns, readme_stream_t stream) {
+  README_CHECK_ARG(n_ctas >= 1 && n_ctas <= 4096 && ns >= 0 && ns <= 60000000000LL, "n_ctas in [1, 4096], ns in [0, 60 s]");
+  return launch_debug_hold_sms(n_ctas, ns, reinterpret_cast<cudaStream_t>(stream));
 }
 
 readme_status readme_set_device(int device) {
@@ -284,8 +286,8 @@ readme_status readme_expert_down(const void* h, readme_dtype dt, int64_t rows, i
 
 readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E,
                                 int32_t d, int32_t n_src, const int32_t* offsets, const void* w_gate,
-                                const void* w_up, const void* w_down, void* y_sorted, void* ws, size_t ws_bytes,
-                                readme_stream_t stream) {
+                                const void* w_up, const void* w_down, void* y_sorted, uint32_t* dev_status, void* ws,
+                                size_t ws_bytes, readme_stream_t stream) {
   README_TRY(check_ffn_args(dt, rows, H, E, d, n_src, offsets));
   if (rows == 0) return README_OK;
   README_CHECK_ARG(ws != nullptr && aligned16(ws), "workspace is required (16-byte aligned)");
@@ -298,7 +300,7 @@ readme_status readme_expert_ffn(const void* x_sorted, readme_dtype dt, int64_t r
                        aligned16(y_sorted),
                    "all tensors must be 16-byte aligned");
   return run_ffn(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted, ws,
-                 nullptr, reinterpret_cast<cudaStream_t>(stream));
+                 dev_status, reinterpret_cast<cudaStream_t>(stream));
 }
 
 
@@ -387,8 +389,7 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   w += ffn_ws_bytes(rows, d, dt);
   int32_t* src_ws = reinterpret_cast<int32_t*>(w);
   const FfnPath path = ffn_path();
-  const bool fused = k == 1 && (src != nullptr || logits != nullptr) && path != FfnPath::k1cta &&
-                     path != FfnPath::kUnfused;
+  const bool fused = k == 1 && (src != nullptr || logits != nullptr) && path != FfnPath::kUnfused;
   // the single-launch FFN follows the dispatch as a programmatic dependent (PDL), fused combine or not
   const bool pdl = merged_ffn(dt);
   // every argument check precedes the first launch: an error return leaves no partial step behind
@@ -440,8 +441,8 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
     README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted,
                        ws_ffn, dev_status, reinterpret_cast<cudaStream_t>(stream), true, xready));
   } else {
-    README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted, ws_ffn,
-                                 ffn_ws_bytes(rows, d, dt), stream));
+    README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted,
+                                 dev_status, ws_ffn, ffn_ws_bytes(rows, d, dt), stream));
   }
   return readme_combine(y_sorted, dt, T, H, k, dest, topk_w, residual, y, dev_status, stream);
 }
@@ -541,8 +542,8 @@ readme_status readme_moe_stack(void* x, readme_dtype dt, int64_t T, int32_t H, c
 }
 
 readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T, int32_t H, int32_t d_perm,
-                                      const void* w_gate, const void* w_up, const void* w_down, void* y, void* ws,
-                                      size_t ws_bytes, readme_stream_t stream) {
+                                      const void* w_gate, const void* w_up, const void* w_down, void* y,
+                                      uint32_t* dev_status, void* ws, size_t ws_bytes, readme_stream_t stream) {
   README_TRY(check_rows(dt, H));
   README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
   README_CHECK_ARG(d_perm >= 8 && d_perm % 8 == 0, "d_perm must be a positive multiple of 8 (got %d)", d_perm);
@@ -562,7 +563,7 @@ readme_status readme_permanent_expert(const void* x, readme_dtype dt, int64_t T,
   README_TRY(launch_set_offsets(offs, static_cast<int32_t>(T), st));
   void* ws_ffn = static_cast<char*>(ws) + 256;
   // y <- y + F_perm(x): the down projection adds the residual y in its epilogue, in place (identity rows)
-  return run_ffn(x, dt, T, H, 1, d_perm, 1, offs, w_gate, w_up, w_down, nullptr, y, y, ws_ffn, nullptr, st);
+  return run_ffn(x, dt, T, H, 1, d_perm, 1, offs, w_gate, w_up, w_down, nullptr, y, y, ws_ffn, dev_status, st);
 }
 
 size_t readme_permanent_expert_workspace_bytes(int64_t T, int32_t H, int32_t d_perm, readme_dtype dt) {

@@ -59,17 +59,12 @@ struct __align__(8) SmemT {
   int tile_start2[kMaxSeg + 1];  // merged a6+a7 kernel: the down tiles' prefix
   int mt_start[kMaxSeg + 1];     // merged kernel: first m-tile id of each segment (readiness counters)
   uint32_t xok[kXokWords];       // merged kernel, pdl == 2: bit per m-tile, this CTA's A rows seen ready
-  // merged kernel, dynamic tile fetch: the leader's producer publishes each next tile id to both CTAs
-  int tq[4];
-  uint64_t tq_full[4];   // per CTA: the id in tq[slot] is valid (1 arrival: the leader's producer)
-  uint64_t tq_empty[4];  // leader only: every consumer warp of the pair has read tq[slot] (10 arrivals)
 };
 using Smem = SmemT<kStages, kStageA>;
 using SmemD = SmemT<kStagesD, kStageAD>;
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 constexpr size_t kSmemBytesD = sizeof(SmemD) + 1024;
 static_assert(kSmemBytesD <= 232448 && kSmemBytes <= 232448, "shared memory");
-constexpr int kTQ = 4;
 
 struct Tile {
   int g, m0, rows, n0;
@@ -374,16 +369,21 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 // a gate/up tile with a release add on ready[m-tile] (after a generic->async proxy fence, since the down
 // tile reads h with TMA), and the down producer acquires ready[m-tile] == NT1 * 8 before loading. Down
 // tiles come after every gate/up tile in every pair's sequence, so a wait only ever depends on tiles that
-// are earlier in some pair's sequence (all pairs are co-resident: one CTA per SM, grid <= #SMs; a bounded
-// poll flags README_DEV_SCHED_TIMEOUT instead of hanging if that ever fails). This removes the gate/up
-// kernel's tail, the down kernel's prologue and the down kernel's last-round imbalance.
+// are earlier in some pair's sequence. That needs every pair of the grid co-resident: the launcher sizes
+// the grid with cudaOccupancyMaxActiveClusters. If co-residency still fails (an SM-holding kernel from
+// another stream or process, MPS), the bounded poll gives up: the waiting thread sets
+// README_DEV_SCHED_TIMEOUT in dev_status and the launch's abort word, and from then on every epilogue of
+// the launch skips its stores — each output element is either its correct value or left as it was, never
+// a value computed from unready rows (tests/test_gpu_parity.py::test_ffn_sm_starved_*).
 struct LayerArgs {
   int H, d, E, nseg;
   const int32_t* offsets;
   __nv_bfloat16* h;          // [rows, d]
   __nv_bfloat16* y;          // [rows, H] (y_sorted) or [T, H] (scatter)
   uint32_t* ready;           // [#m-tiles] zeroed before the launch
-  uint32_t* dev_status;
+  uint32_t* abort;           // one word of the zeroed readiness region: nonzero once a readiness wait gave up
+  uint32_t* dev_status;      // nullable
+  uint32_t spin_limit;       // polls before a readiness wait gives up
   Fuse fz;
   const int32_t* expert_slot;  // nullable: expert e's weights live at slot expert_slot[e] of the weight pools
   // kFuse == 2 (expert parallelism over peer memory): received row r came from rank p = v / vrows as its
@@ -396,12 +396,10 @@ struct LayerArgs {
   int pdl;  // launched as a programmatic dependent of the dispatch: 1 = griddepcontrol.wait before reading
             // x_sorted; 2 = per-row readiness flags (xready) instead, so gate/up tiles start while the
             // dispatch is still writing later experts' rows (the wait moves to the kernel's end)
-  int dyn;  // dynamic tile fetch: tiles after each pair's first come from an atomic counter (ready[sched])
-  int sched;
   const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
-  int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (README_FFN_ASKIP)
-  int order;               // lab: 1 = gate/up tiles N-tile fastest (README_FFN_ORDER)
+  int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (knob ffn_askip)
+  int order;               // lab: 1 = gate/up tiles N-tile fastest (knob ffn_order)
 };
 
 struct LTile {
@@ -409,9 +407,12 @@ struct LTile {
   bool m256;
 };
 
+constexpr int kBN1 = 128;  // h columns per gate/up tile ([gate 64 | up 64] rows per CTA)
+constexpr int kBN2 = 256;  // output columns per down tile (128 W_down rows per CTA)
+
 template <int kMT, class SM>
 __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
-                                             int& gcur2, int bn1, int bn2, bool nfast = false) {
+                                             int& gcur2, bool nfast = false) {
   LTile tl;
   int local, g, NT;
   if (t < T1) {
@@ -431,7 +432,7 @@ __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int 
   const int cnt = s.seg_off[g + 1] - s.seg_off[g];
   const int mt_g = (cnt + kMT - 1) / kMT;
   // m-tile fastest (default: consecutive pairs share a weight tile) or, for gate/up tiles with nfast (lab
-  // knob README_FFN_ORDER=1), N-tile fastest (consecutive pairs share an A tile)
+  // knob ffn_order = 1), N-tile fastest (consecutive pairs share an A tile)
   const bool nf = nfast && tl.mode == 0;
   const int nt = nf ? local % NT : local / mt_g, mt = nf ? local / NT : local % mt_g;
   tl.g = g;
@@ -439,7 +440,7 @@ __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int 
   tl.m0 = s.seg_off[g] + mt * kMT;
   tl.rows = min(kMT, cnt - mt * kMT);
   tl.m256 = tl.rows > 128;
-  tl.n0 = nt * (tl.mode == 0 ? bn1 : bn2);
+  tl.n0 = nt * (tl.mode == 0 ? kBN1 : kBN2);
   return tl;
 }
 
@@ -448,11 +449,19 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// A readiness wait gave up (lane 0 of the waiting warp): report it and stop every later store of the launch.
+__device__ __forceinline__ void sched_give_up(const LayerArgs& la) {
+  if (la.dev_status) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+  atomicExch(la.abort, 1u);
+  __threadfence();
+}
 
-// kNB = B rows each CTA stages per K step: 128 (default; a gate/up tile covers 128 h columns, a down tile
-// 256 output columns) or 64 (small batches: twice as many, half-width tiles, so every SM streams its
-// share of the touched experts' weights — decode is weight-bandwidth bound).
-template <int kFuse, int kNB, int kMT>
+template <int kFuse, int kMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
@@ -468,9 +477,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const bool leader = cta == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
-  constexpr int kBN1 = kNB, kBN2 = 2 * kNB;  // h columns per gate/up tile, output columns per down tile
-  constexpr int kN = 2 * kNB;               // MMA N (both CTAs' B halves)
-  static_assert(kNB == 128 || kNB == 64, "kNB");
+  constexpr int kN = 256;  // MMA N (both CTAs' 128-row B halves)
   const int NT1 = (d + kBN1 - 1) / kBN1, NT2 = (H + kBN2 - 1) / kBN2;
   const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
   const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
@@ -508,10 +515,6 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       tc::mbar_init(&s.tfull[i], 1);
       tc::mbar_init(&s.tempty[i], 8);
     }
-    for (int i = 0; i < kTQ; ++i) {
-      tc::mbar_init(&s.tq_full[i], 1);
-      tc::mbar_init(&s.tq_empty[i], 10);  // leader MMA warp + 4 + 4 epilogue warps + the peer's producer
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc::fence_before();
@@ -527,9 +530,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
       int g1 = 0, g2 = 0;
-      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
-      const int nr = tl.n0 + (kNB / 2) * static_cast<int>(cta);
+      const int nr = tl.n0 + 64 * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
       for (int kb = 0; kb < kbs; ++kb) {
         tc::tma_prefetch_3d(&tmG, kb * kBK, nr, e);
@@ -539,40 +542,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (la.pdl == 1) tc::pdl_wait();
   }
   if (la.trace && tid == 0) trace_min(la.trace, 2);
-  // Tile sequence of this pair. Static: pair, pair + npairs, ... Dynamic (la.dyn): the first tile is still
-  // `pair`; each later one is npairs + atomicAdd(counter), fetched by the leader's producer when it moves on
-  // and published through a 4-deep queue to the pair's other warps — per-pair work evens out (tiles differ
-  // in cost: M=128 tails, gate/up vs down) while the global order (and the down tiles' readiness
-  // dependencies) stays the same. A consumer warp reads entry j and releases it on the leader.
-  const bool dyn = la.dyn != 0;
-  auto consume = [&](int j) -> int {
-    if (!dyn) return pair + j * npairs;
-    const int slot = j % kTQ;
-    tc::mbar_wait_cluster(&s.tq_full[slot], static_cast<uint32_t>(j / kTQ) & 1u);
-    const int t = *reinterpret_cast<volatile int*>(&s.tq[slot]);
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive_cluster(&s.tq_empty[slot], 0);
-    return t;
-  };
-  uint32_t fetched = 0;  // lane 0 of the leader's producer: the next tile's counter ticket, fetched one tile
-                         // ahead so the atomic's latency hides behind the current tile's loads
-  auto produce = [&](int j) -> int {  // the leader's producer warp
-    int t = pair + j * npairs;
-    if (dyn) {
-      if (j > 0) t = npairs + static_cast<int>(__shfl_sync(0xffffffffu, fetched, 0));
-      if (lane == 0) fetched = atomicAdd(la.ready + la.sched, 1u);
-      const int slot = j % kTQ;
-      tc::mbar_wait_cluster(&s.tq_empty[slot], (static_cast<uint32_t>(j / kTQ) & 1u) ^ 1u);
-      if (lane == 0) {
-        s.tq[slot] = t;
-        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(tc::mapa(&s.tq[slot], 1)), "r"(t) : "memory");
-        tc::mbar_arrive_cluster(&s.tq_full[slot], 0);  // release: the id stores are visible first
-        tc::mbar_arrive_cluster(&s.tq_full[slot], 1);
-      }
-      __syncwarp();
-    }
-    return t;
-  };
+  // Tile sequence of this pair (static): pair, pair + npairs, ...
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion counted on the leader's barrier). The whole warp walks the
@@ -581,18 +551,16 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint32_t phase = 0;
     int g1 = 0, g2 = 0;
     const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
-    for (int j = 0;; ++j) {
-      const int t = leader ? produce(j) : consume(j);
-      if (t >= ntiles) break;
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
+    for (int t = pair; t < ntiles; t += npairs) {
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
       // A tile of ≤ 64 rows: every row the second CTA would stage is past the tile's end, so it skips its A
       // load (its MMA rows read stale shared memory; row m of the product depends on A row m only and rows
-      // past tl.rows are never stored). README_FFN_ASKIP=0 loads them anyway (A/B).
+      // past tl.rows are never stored). Knob ffn_askip = 0 loads them anyway (A/B).
       const bool a_skip = la.askip && !tl.m256 && tl.rows <= 64;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + kNB * 128) -
+      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128) -
                              (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
       if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
@@ -607,8 +575,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             for (int r = lo + lane; r < hi; r += kWarp) ok = ok && ld_acquire_u32(la.xready + r) != 0u;
             if (__all_sync(0xffffffffu, ok)) break;
             __nanosleep(64);
-            if (++spins == (1u << 25)) {
-              if (la.dev_status && lane == 0) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+            if (++spins >= la.spin_limit) {
+              if (lane == 0) sched_give_up(la);
               break;
             }
           }
@@ -627,8 +595,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         uint32_t spins = 0;
         while (ld_acquire_u32(rp) < ready_target) {
           __nanosleep(128);
-          if (++spins == (1u << 25)) {
-            if (la.dev_status && lane == 0) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
+          if (++spins >= la.spin_limit) {
+            if (lane == 0) sched_give_up(la);
             break;
           }
         }
@@ -637,7 +605,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       }
       const int KB = tl.mode == 0 ? KB1 : KB2;
       const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
-      const int nrg = tl.n0 + (kNB / 2) * static_cast<int>(cta), nrd = tl.n0 + kNB * static_cast<int>(cta);
+      const int nrg = tl.n0 + 64 * static_cast<int>(cta), nrd = tl.n0 + 128 * static_cast<int>(cta);
       for (int kb = 0; kb < KB; ++kb) {
         tc::mbar_wait(&s.empty[stage], phase ^ 1);
         if (tc::elect_one()) {
@@ -646,12 +614,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
           if (!(a_skip && cta == 1)) tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
-          if (tl.mode == 0) {  // kNB/2 rows of W_gate then the same rows of W_up (box height kNB/2)
+          if (tl.mode == 0) {  // 64 rows of W_gate then the same rows of W_up
             tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nrg, e);
-            tc::tma_load_3d_2sm(&tmU, s.b[stage] + (kNB / 2) * 128, fb, k0, nrg, e);
-          } else {  // kNB rows of W_down in boxes of 64
+            tc::tma_load_3d_2sm(&tmU, s.b[stage] + 64 * 128, fb, k0, nrg, e);
+          } else {  // 128 rows of W_down in boxes of 64
             tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
-            if constexpr (kNB == 128) tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
+            tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
           }
         }
         __syncwarp();
@@ -670,11 +638,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
-      int g1 = 0, g2 = 0;
-      for (int i = 0;; ++i) {
-        const int t = consume(i);
-        if (t >= ntiles) break;
-        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
+      int g1 = 0, g2 = 0, i = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++i) {
+        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -709,15 +675,16 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
     uint8_t* stg = s.stg[q];
-    int g1 = 0, g2 = 0;
-    for (int i = 0;; ++i) {
-      const int t = consume(i);
-      if (t >= ntiles) break;
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, kBN1, kBN2, la.order != 0);
+    int g1 = 0, g2 = 0, i = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++i) {
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
       tc::fence_after();
+      // a readiness wait of this launch gave up: this tile may have been computed from unready rows, so it
+      // (and every later tile) stores nothing
+      const bool aborted = __shfl_sync(0xffffffffu, lane == 0 ? ld_volatile_u32(la.abort) : 0u, 0) != 0u;
       const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256);
       // Accumulator columns of this warp's 32 rows: all kN (M=256), or half of them (M=128, "2x2" layout:
       // lanes 64-127 hold columns [kN/2, kN) at TMEM columns [0, kN/2)).
@@ -731,27 +698,26 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         ncols = kN / 2;
         acc_off = (q >> 1) * (kN / 2);
       }
-      const bool valid = row_in_tile < tl.rows;
+      const bool valid = row_in_tile < tl.rows && !aborted;
       const int64_t r = tl.m0 + row_in_tile;
       if (tl.mode == 0) {
-        // windows of kNB columns: [gate kNB/2 | up kNB/2] of h columns n0 + (window) * kNB/2 + [0, kNB/2)
-        constexpr int kHalf = kNB / 2;
+        // windows of 128 columns: [gate 64 | up 64] of h columns n0 + (window) * 64 + [0, 64)
         __nv_bfloat16* orow = la.h + r * d;
-        for (int w = 0; w < ncols / kNB; ++w) {
-          const uint32_t wbase = tacc + static_cast<uint32_t>(w * kNB);
-          const int hcol0 = tl.n0 + (acc_off + w * kNB) / 2;
+        for (int w = 0; w < ncols / 128; ++w) {
+          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
+          const int hcol0 = tl.n0 + (acc_off + w * 128) / 2;
 #pragma unroll 1
-          for (int c = 0; c < kHalf; c += 32) {
+          for (int c = 0; c < 64; c += 32) {
             uint32_t gr[32], ur[32];
             tc::tmem_ld32(wbase + c, gr);
-            tc::tmem_ld32(wbase + kHalf + c, ur);
+            tc::tmem_ld32(wbase + 64 + c, ur);
             tc::tmem_wait_ld();
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
             stage_row_bf16x32(stg, lane, c / 8, v);
           }
-          const int lim = (d - hcol0) * 2 < kHalf * 2 ? (d - hcol0) * 2 : kHalf * 2;
+          const int lim = (d - hcol0) * 2 < 128 ? (d - hcol0) * 2 : 128;
           stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, lim, false);
         }
       } else {
@@ -804,7 +770,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       if (lane == 0) {
         tc::mbar_arrive_cluster_relaxed(&s.tempty[acc], 0);
         if (tl.mode == 0) {
-          // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release)
+          // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release);
+          // an aborted tile still publishes, so its down tiles stop waiting (they store nothing either)
           asm volatile("fence.proxy.async.global;" ::: "memory");
           asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + s.mt_start[tl.g] + tl.mt)
                        : "memory");
@@ -823,430 +790,54 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
 }
 
-// ---------------------------------------------------------------------------------------------------
-// Wide-N single-launch expert FFN (README_FFN_WIDE=1; measured slower, kept for A/B). A CTA pair computes a 256-row x 2-half tile: for every
-// K stage each CTA stages its 128 A rows ONCE and B rows for TWO 256-column halves, and issues two M=256
-// N=256 MMAs (one per half) into two TMEM accumulators (columns [0,256) and [256,512)). Staged bytes per
-// FLOP drop by a quarter against the double-buffered 256-column tile (48 KB per 1024 MMA cycles instead of
-// 32 KB per 512): that kernel is bound by L2->SM throughput (~11.5 TB/s measured, the LTS cap), so the
-// wide tile runs closer to the tensor-pipe bound. Gate/up half h covers h columns n0 + 128h + [0,128)
-// ([gate 64 | up 64] per CTA, as in the narrow kernel); down half h covers output columns n0 + 256h +
-// [0,256). A half that lies entirely past N is skipped (d = 5504 = 21.5 x 256).
-// The accumulators are single-buffered across tiles; the epilogue drains accumulator 0 first and releases
-// it, and the MMA issuer starts the next tile on accumulator 0 while accumulator 1 is still draining,
-// catching accumulator 1 up over the stages it kept (ring depth permitting): the epilogue stays hidden.
-constexpr int kWStages = 4;
-constexpr int kWStageB = 2 * 128 * 128;  // two halves x 128 rows x 128 B per CTA
-
-struct __align__(8) WSmem {
-  uint8_t a[kWStages][kStageA];
-  uint8_t b[kWStages][kWStageB];
-  uint64_t full[kWStages];
-  uint64_t empty[kWStages];
-  uint64_t tfull;
-  uint64_t tempty[2];
-  uint32_t tmem_base;
-  alignas(16) uint8_t stg[4][32 * 128];
-  int seg_off[kMaxSeg + 1];
-  int tile_start[kMaxSeg + 1];
-  int tile_start2[kMaxSeg + 1];
-  int mt_start[kMaxSeg + 1];
+// Per-device kernel attributes (max dynamic shared memory) and the co-residency limit of the single-launch
+// kernels (CTA pairs that fit at once: the persistent grid never exceeds it).
+struct DevInfo {
+  cudaError_t err = cudaSuccess;
+  int max_pairs[2] = {0, 0};  // [kMT == 128, kMT == 256]
 };
-constexpr size_t kWSmemBytes = sizeof(WSmem) + 1024;
-static_assert(kWSmemBytes <= 232448, "wide kernel shared memory");
 
-__device__ __forceinline__ LTile decode_wtile(const WSmem& s, int t, int nseg, int T1, int& gcur1, int& gcur2,
-                                             int bn1, int bn2) {
-  LTile tl;
-  int local, g;
-  if (t < T1) {
-    while (gcur1 + 1 < nseg && s.tile_start[gcur1 + 1] <= t) ++gcur1;
-    g = gcur1;
-    local = t - s.tile_start[g];
-    tl.mode = 0;
-  } else {
-    const int t2 = t - T1;
-    while (gcur2 + 1 < nseg && s.tile_start2[gcur2 + 1] <= t2) ++gcur2;
-    g = gcur2;
-    local = t2 - s.tile_start2[g];
-    tl.mode = 1;
-  }
-  const int cnt = s.seg_off[g + 1] - s.seg_off[g];
-  const int mt_g = (cnt + 255) / 256;
-  const int nt = local / mt_g, mt = local % mt_g;
-  tl.g = g;
-  tl.mt = mt;
-  tl.m0 = s.seg_off[g] + mt * 256;
-  tl.rows = min(256, cnt - mt * 256);
-  tl.m256 = tl.rows > 128;
-  tl.n0 = nt * (tl.mode == 0 ? bn1 : bn2);
-  return tl;
-}
-
-template <int kFuse>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-ffn_wide_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
-                const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                const __grid_constant__ CUtensorMap tmD, LayerArgs la) {
-  extern __shared__ uint8_t smem_raw[];
-  WSmem& s = *reinterpret_cast<WSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
-  const uint32_t cta = tc::cluster_ctarank();
-  const bool leader = cta == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
-  constexpr int kHW1 = 128, kHW2 = 256;            // columns per half: gate/up (h columns), down
-  constexpr int kBN1 = 2 * kHW1, kBN2 = 2 * kHW2;  // columns per tile
-  const int NT1 = (d + kBN1 - 1) / kBN1, NT2 = (H + kBN2 - 1) / kBN2;
-  const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
-  const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
-
-  for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = la.offsets[i];
-  if (warp == 0 && lane == 0) {
-    tc::prefetch_tmap(&tmX);
-    tc::prefetch_tmap(&tmG);
-    tc::prefetch_tmap(&tmU);
-    tc::prefetch_tmap(&tmH);
-    tc::prefetch_tmap(&tmD);
-  }
-  if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
-  __syncthreads();
-  if (tid == 0) {
-    int a1 = 0, a2 = 0, am = 0;
-    for (int g = 0; g < nseg; ++g) {
-      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + 255) / 256;
-      s.tile_start[g] = a1;
-      s.tile_start2[g] = a2;
-      s.mt_start[g] = am;
-      a1 += mt_g * NT1;
-      a2 += mt_g * NT2;
-      am += mt_g;
+const DevInfo& dev_info() {
+  static std::once_flag once[64];
+  static DevInfo info[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  std::call_once(once[dev], [&] {
+    DevInfo& di = info[dev];
+    const void* fns[3] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
+                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
+                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>)};
+    for (int i = 0; i < 3 && di.err == cudaSuccess; ++i)
+      di.err = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    const void* lfns[2][3] = {{reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128>),
+                               reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128>),
+                               reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128>)},
+                              {reinterpret_cast<const void*>(ffn_layer2_kernel<0, 256>),
+                               reinterpret_cast<const void*>(ffn_layer2_kernel<1, 256>),
+                               reinterpret_cast<const void*>(ffn_layer2_kernel<2, 256>)}};
+    const size_t lsmem[2] = {kSmemBytesD, kSmemBytes};
+    for (int v = 0; v < 2; ++v) {
+      int mp = 1 << 30;
+      for (int i = 0; i < 3 && di.err == cudaSuccess; ++i) {
+        di.err = cudaFuncSetAttribute(lfns[v][i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem[v]));
+        if (di.err != cudaSuccess) break;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * (num_sms() / 2));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = lsmem[v];
+        int n = 0;
+        di.err = cudaOccupancyMaxActiveClusters(&n, lfns[v][i], &cfg);
+        if (di.err == cudaSuccess && n < mp) mp = n;
+      }
+      di.max_pairs[v] = mp;
     }
-    s.tile_start[nseg] = a1;
-    s.tile_start2[nseg] = a2;
-    s.mt_start[nseg] = am;
-    for (int i = 0; i < kWStages; ++i) {
-      tc::mbar_init(&s.full[i], 1);
-      tc::mbar_init(&s.empty[i], 1);
-    }
-    tc::mbar_init(&s.tfull, 1);
-    tc::mbar_init(&s.tempty[0], 8);
-    tc::mbar_init(&s.tempty[1], 8);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc::fence_before();
-  __syncthreads();
-  tc::cluster_sync();
-  tc::fence_after();
-  const int T1 = s.tile_start[nseg];
-  const int ntiles = T1 + s.tile_start2[nseg];
-  const uint32_t tmem_base = s.tmem_base;
-  if (la.pdl) {  // see ffn_layer2_kernel: warm L2 with the first weight tile, then wait for the dispatch
-    if (warp == 0 && lane == 0 && pair < T1) {
-      int g1 = 0, g2 = 0;
-      const LTile tl = decode_wtile(s, pair, nseg, T1, g1, g2, kBN1, kBN2);
-      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
-      const int kbs = KB1 < kPrefetchK / 2 ? KB1 : kPrefetchK / 2;
-      for (int h = 0; h < 2; ++h) {
-        const int nr = tl.n0 + h * kHW1 + 64 * static_cast<int>(cta);
-        if (nr >= d) break;
-        for (int kb = 0; kb < kbs; ++kb) {
-          tc::tma_prefetch_3d(&tmG, kb * kBK, nr, e);
-          tc::tma_prefetch_3d(&tmU, kb * kBK, nr, e);
-        }
-      }
-    }
-    tc::pdl_wait();
-  }
-
-  if (warp == 0) {
-    // ===== TMA producer (both CTAs; completion counted on the leader's barrier) =====
-    int stage = 0;
-    uint32_t phase = 0;
-    int g1 = 0, g2 = 0;
-    for (int t = pair; t < ntiles; t += npairs) {
-      const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
-      const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
-      const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
-      const int a_rows = tl.m256 ? 128 : 64;
-      const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + (two ? 2 : 1) * 128 * 128);
-      if (tl.mode == 1) {
-        if (lane == 0) {
-          const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
-          uint32_t spins = 0;
-          while (ld_acquire_u32(rp) < ready_target) {
-            __nanosleep(128);
-            if (++spins == (1u << 25)) {
-              if (la.dev_status) atomicOr(la.dev_status, README_DEV_SCHED_TIMEOUT);
-              break;
-            }
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        __syncwarp();
-      }
-      const int KB = tl.mode == 0 ? KB1 : KB2;
-      for (int kb = 0; kb < KB; ++kb) {
-        tc::mbar_wait(&s.empty[stage], phase ^ 1);
-        if (lane == 0) {
-          const uint32_t fb = tc::mapa(&s.full[stage], 0);
-          const int k0 = kb * kBK;
-          if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
-          const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
-          tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
-          if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
-          for (int h = 0; h < (two ? 2 : 1); ++h) {
-            uint8_t* bh = s.b[stage] + h * (128 * 128);
-            if (tl.mode == 0) {  // 64 rows of W_gate then the same 64 rows of W_up
-              const int nr = tl.n0 + h * kHW1 + 64 * static_cast<int>(cta);
-              tc::tma_load_3d_2sm(&tmG, bh, fb, k0, nr, e);
-              tc::tma_load_3d_2sm(&tmU, bh + 64 * 128, fb, k0, nr, e);
-            } else {  // 128 rows of W_down
-              const int nr = tl.n0 + h * kHW2 + 128 * static_cast<int>(cta);
-              tc::tma_load_3d_2sm(&tmD, bh, fb, k0, nr, e);
-              tc::tma_load_3d_2sm(&tmD, bh + 64 * 128, fb, k0, nr + 64, e);
-            }
-          }
-        }
-        if (++stage == kWStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader) {
-      // ===== MMA issuer (leader CTA): the whole warp walks the loop, one elected lane issues =====
-      constexpr uint32_t idesc256 = tc::idesc_bf16(256, 256);
-      constexpr uint32_t idesc128 = tc::idesc_bf16(128, 256);
-      const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
-      int stage = 0;
-      uint32_t phase = 0;
-      int g1 = 0, g2 = 0, i = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
-        const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
-        const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
-        const uint32_t par = (static_cast<uint32_t>(i) & 1u) ^ 1u;  // accumulators released by tile i-1
-        const int KB = tl.mode == 0 ? KB1 : KB2;
-        // half-1 MMAs still owed (accumulator 1 not yet drained) for the consecutive stages
-        // [pend0, pend0 + npend) of this tile, which began at k-block first_pend_kb
-        int pend0 = 0, npend = 0, first_pend_kb = 0;
-        bool acc1_free = !two;
-        tc::mbar_wait_cluster(&s.tempty[0], par);
-        tc::fence_after();
-        auto issue = [&](int st, int h, bool first_k) {
-          const uint64_t ad = adesc0 + static_cast<uint64_t>(st * (kStageA >> 4));
-          const uint64_t bd = bdesc0 + static_cast<uint64_t>(st * (kWStageB >> 4) + h * ((128 * 128) >> 4));
-          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(h * 256);
-          if (tc::elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < kBK / kUK; ++kk)
-              tc::mma_f16<2>(d_tmem, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2), idesc,
-                             (!first_k || kk != 0) ? 1u : 0u);
-          }
-          __syncwarp();
-        };
-        auto release = [&](int st) {
-          if (tc::elect_one()) tc::commit_2sm_mc(&s.empty[st], 0x3);
-          __syncwarp();
-        };
-        auto catch_up = [&]() {  // accumulator 1, oldest owed stage first
-          for (int j = 0; j < npend; ++j) {
-            const int st = (pend0 + j) % kWStages;
-            issue(st, 1, first_pend_kb + j == 0);
-            release(st);
-          }
-          npend = 0;
-        };
-        for (int kb = 0; kb < KB; ++kb) {
-          if (!acc1_free && npend == kWStages) {  // the ring is exhausted: wait for the drain
-            tc::mbar_wait_cluster(&s.tempty[1], par);
-            tc::fence_after();
-            acc1_free = true;
-          }
-          if (!acc1_free && tc::mbar_test_cluster(&s.tempty[1], par)) {
-            tc::fence_after();
-            acc1_free = true;
-          }
-          if (acc1_free && npend) catch_up();
-          tc::mbar_wait_cluster(&s.full[stage], phase);
-          tc::fence_after();
-          issue(stage, 0, kb == 0);
-          if (!two) {
-            release(stage);
-          } else if (acc1_free) {
-            issue(stage, 1, kb == 0);
-            release(stage);
-          } else {
-            if (npend == 0) {
-              pend0 = stage;
-              first_pend_kb = kb;
-            }
-            ++npend;
-          }
-          if (++stage == kWStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        if (npend) {  // short tile: accumulator 1 never freed while its stages streamed
-          tc::mbar_wait_cluster(&s.tempty[1], par);
-          tc::fence_after();
-          catch_up();
-        } else if (!two) {
-          tc::mbar_wait_cluster(&s.tempty[1], par);  // keep accumulator 1's phase in step with the tiles
-        }
-        if (tc::elect_one()) tc::commit_2sm_mc(&s.tfull, 0x3);
-        __syncwarp();
-      }
-    }
-  } else {
-    // ===== epilogue: warps 2..5 of both CTAs =====
-    const int q = warp & 3;
-    uint8_t* stg = s.stg[q];
-    int g1 = 0, g2 = 0, i = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const LTile tl = decode_wtile(s, t, nseg, T1, g1, g2, kBN1, kBN2);
-      const bool two = tl.n0 + (tl.mode == 0 ? kHW1 : kHW2) < (tl.mode == 0 ? d : H);
-      tc::mbar_wait_cluster(&s.tfull, static_cast<uint32_t>(i) & 1u);
-      tc::fence_after();
-      int row_in_tile, ncols, acc_off;
-      if (tl.m256) {
-        row_in_tile = static_cast<int>(cta) * 128 + q * 32 + lane;
-        ncols = 256;
-        acc_off = 0;
-      } else {
-        row_in_tile = static_cast<int>(cta) * 64 + (q & 1) * 32 + lane;
-        ncols = 128;
-        acc_off = (q >> 1) * 128;
-      }
-      const bool valid = row_in_tile < tl.rows;
-      const int64_t r = tl.m0 + row_in_tile;
-      // output row pointers (down tiles)
-      int64_t orow_idx = r;
-      bool valid_row = valid;
-      __nv_bfloat16* orow = nullptr;
-      const __nv_bfloat16* rrow = nullptr;
-      if (tl.mode == 1) {
-        if constexpr (kFuse == 2) {
-          const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
-          valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
-          const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
-          const int64_t iv = valid_row ? v - p * la.vrows : 0;
-          __nv_bfloat16* py = la.peer_y[0];
-          const __nv_bfloat16* pr = la.peer_res[0];
-#pragma unroll
-          for (int j = 1; j < kMaxPeers; ++j)
-            if (p == j) {
-              py = la.peer_y[j];
-              pr = la.peer_res[j];
-            }
-          orow = py + iv * H;
-          rrow = pr ? pr + iv * H : nullptr;
-        } else {
-          if constexpr (kFuse == 1) {
-            orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
-            valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
-          }
-          orow = la.y + orow_idx * H;
-          rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
-        }
-      }
-      for (int h = 0; h < 2; ++h) {
-        if (h == 0 || two) {
-          const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(h * 256);
-          if (tl.mode == 0) {
-            __nv_bfloat16* hrow = la.h + r * d;
-            for (int w = 0; w < ncols / 128; ++w) {
-              const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
-              const int hcol0 = tl.n0 + h * kHW1 + (acc_off + w * 128) / 2;
-#pragma unroll 1
-              for (int c = 0; c < 64; c += 32) {
-                uint32_t gr[32], ur[32];
-                tc::tmem_ld32(wbase + c, gr);
-                tc::tmem_ld32(wbase + 64 + c, ur);
-                tc::tmem_wait_ld();
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
-                stage_row_bf16x32(stg, lane, c / 8, v);
-              }
-              stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(hrow + hcol0) : 0ull, (d - hcol0) * 2, false);
-            }
-          } else {
-#pragma unroll 1
-            for (int c0 = 0; c0 < ncols; c0 += 64) {
-              const int col0 = tl.n0 + h * kHW2 + acc_off + c0;
-#pragma unroll 1
-              for (int c = 0; c < 64; c += 32) {
-                uint32_t vr[32];
-                tc::tmem_ld32(tacc + static_cast<uint32_t>(c0 + c), vr);
-                tc::tmem_wait_ld();
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-                if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
-                stage_row_bf16x32(stg, lane, c / 8, v);
-              }
-              stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2,
-                          false);
-            }
-          }
-        }
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster_relaxed(&s.tempty[h], 0);  // accumulator h drained
-      }
-      if (lane == 0 && tl.mode == 0) {
-        // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release)
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + s.mt_start[tl.g] + tl.mt)
-                     : "memory");
-      }
-    }
-  }
-
-  if constexpr (kFuse == 2) __threadfence_system();
-  tc::fence_before();
-  __syncthreads();
-  tc::cluster_sync();
-  tc::fence_after();
-  if (warp == 1) tc::tmem_dealloc<2>(tmem_base, kTmemCols);
+  });
+  return info[dev];
 }
 
 readme_status set_smem_attr() {
-  static std::once_flag once[64];
-  static cudaError_t err[64];
-  int dev = 0;
-  README_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) dev = 0;
-  std::call_once(once[dev], [&] {
-    const void* fns[9] = {reinterpret_cast<const void*>(ffn_gemm2_kernel<0, 0>),
-                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 0>),
-                          reinterpret_cast<const void*>(ffn_gemm2_kernel<1, 1>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128, 256>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128, 256>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128, 256>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<0, 64, 256>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<1, 64, 256>),
-                          reinterpret_cast<const void*>(ffn_layer2_kernel<2, 64, 256>)};
-    err[dev] = cudaSuccess;
-    for (int i = 0; i < 9 && err[dev] == cudaSuccess; ++i)
-      err[dev] = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    const void* dfns[3] = {reinterpret_cast<const void*>(ffn_layer2_kernel<0, 128, 128>),
-                           reinterpret_cast<const void*>(ffn_layer2_kernel<1, 128, 128>),
-                           reinterpret_cast<const void*>(ffn_layer2_kernel<2, 128, 128>)};
-    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
-      err[dev] = cudaFuncSetAttribute(dfns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytesD));
-    const void* wfns[3] = {reinterpret_cast<const void*>(ffn_wide_kernel<0>),
-                           reinterpret_cast<const void*>(ffn_wide_kernel<1>),
-                           reinterpret_cast<const void*>(ffn_wide_kernel<2>)};
-    for (int i = 0; i < 3 && err[dev] == cudaSuccess; ++i)
-      err[dev] = cudaFuncSetAttribute(wfns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWSmemBytes));
-  });
-  if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(ffn_gemm2_kernel)");
+  const DevInfo& di = dev_info();
+  if (di.err != cudaSuccess) return cuda_fail(di.err, "cudaFuncSetAttribute / cudaOccupancyMaxActiveClusters (expert FFN)");
   return README_OK;
 }
 
@@ -1275,11 +866,10 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   }
   if (mode == 1) mB1 = mB0;
   const int64_t mt_ub = nseg + (rows + 255) / 256;
-  const int pairs = num_sms() / 2;
+  const int pairs = num_sms() / 2;  // no inter-CTA waits here: the grid need not be co-resident
   const int64_t tiles = mt_ub * ((N + (mode == 0 ? 127 : 255)) / (mode == 0 ? 128 : 256));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  const char* lab = getenv("README_LAB");
-  const Fuse fz{src, static_cast<int>(rows), residual, lab ? atoi(lab) : 0};
+  const Fuse fz{src, static_cast<int>(rows), residual, knob(Knob::kFfnLab)};
   if (mode == 0)
     ffn_gemm2_kernel<0, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   else if (src == nullptr && residual == nullptr)
@@ -1290,10 +880,24 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   return README_OK;
 }
 
-// [readiness counters: <= kMaxSeg + #m-tiles + 1][x_sorted row flags: rows] (the flags are used when the
-// gather dispatch precedes the FFN, pdl == 2); one memset zeroes both
-size_t ffn_layer_xready_offset(int64_t rows) {  // counters sized for 128-row m-tiles (either kMT)
-  return align_up(static_cast<size_t>(kMaxSeg + (rows + 127) / 128 + 1) * sizeof(uint32_t), 256);
+readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
+                                  int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
+                                  const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st) {
+  return launch_gemm_2cta(0, xs, rows, H, d, E, nseg, offsets, wg, wu, h, nullptr, nullptr, st);
+}
+
+readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
+                               const int32_t* offsets, const __nv_bfloat16* wd, __nv_bfloat16* out,
+                               const int32_t* src, const __nv_bfloat16* residual, cudaStream_t st) {
+  return launch_gemm_2cta(1, h, rows, d, H, E, nseg, offsets, wd, nullptr, out, src, residual, st);
+}
+
+// Readiness region of the single-launch kernel: [down-tile counters: kMaxSeg + #128-row m-tiles][abort word]
+// [pad][x_sorted row flags: rows] (the flags are used when the gather dispatch precedes the FFN, pdl == 2);
+// one memset (or the route launch) zeroes all of it before every launch.
+int64_t ffn_layer_abort_index(int64_t rows) { return kMaxSeg + (rows + 127) / 128 + 1; }
+size_t ffn_layer_xready_offset(int64_t rows) {
+  return align_up(static_cast<size_t>(ffn_layer_abort_index(rows) + 1) * sizeof(uint32_t), 256);
 }
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
   (void)nseg;
@@ -1314,19 +918,10 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   }
   readme_status rs = set_smem_attr();
   if (rs != README_OK) return rs;
-  // Tile width: full width by default; README_FFN_NB=64 selects half-width tiles (twice as many tiles: more
-  // SMs share a small batch's weight stream, but measured slower at decode sizes — profiles/SUMMARY.md).
-  int nb = 128;
-  if (const char* v = getenv("README_FFN_NB")) nb = atoi(v) == 64 ? 64 : 128;
-  // README_FFN_WIDE=1 selects the wide-N tile (two 256-column halves per K stage, 25 % fewer staged bytes
-  // per FLOP); measured 15 % slower than the double-buffered 256-column tile at config 2 (more DRAM
-  // re-reads, single-buffered accumulators), so it is not the default (profiles/SUMMARY.md)
-  bool wide = false;
-  if (const char* v = getenv("README_FFN_WIDE")) wide = nb == 128 && atoi(v) != 0;
   CUtensorMap mX, mG, mU, mH, mD;
   const int32_t EW = expert_slot ? n_slots : E;  // outer extent of the weight tensors
-  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, nb / 2) &&
-            tc::make_map_3d(&mU, wu, H, d, EW, kBK, nb / 2) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
+  bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, 64) &&
+            tc::make_map_3d(&mU, wu, H, d, EW, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
             tc::make_map_3d(&mD, wd, d, H, EW, kBK, 64);
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
@@ -1335,28 +930,40 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   // with pdl the caller zeroed `ready` before the dispatch (a memset here would sit between the two kernels)
   if (!pdl) README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
   // 128-row m-tiles with the 8-stage ring for decode-sized launches (weight streaming: more bytes in flight,
-  // no B reuse to lose); README_FFN_MT=128|256 overrides (A/B measurement)
+  // no B reuse to lose); knob ffn_mt = 128 | 256 overrides (A/B measurement)
   int mt = rows <= kDecodeRows ? 128 : 256;
-  if (const char* v = getenv("README_FFN_MT")) mt = atoi(v) == 128 ? 128 : 256;
-  if (wide || nb == 64) mt = 256;
+  if (const int v = knob(Knob::kFfnMt)) mt = v == 128 ? 128 : 256;
   const int64_t mt_ub = nseg + (rows + mt - 1) / mt;
-  int pairs = num_sms() / 2;
-  // README_FFN_PAIRS=n: at most n CTA pairs (measurement of placement-limited grids, e.g. 66 pairs = the
-  // 132 SMs that 4-CTA clusters place on)
-  if (const char* v = getenv("README_FFN_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(v)));
-  const int64_t tiles = wide ? mt_ub * ((d + 255) / 256 + (H + 511) / 512)
-                             : mt_ub * ((d + nb - 1) / nb + (H + 2 * nb - 1) / (2 * nb));
+  // Persistent grid: never more pairs than can be co-resident (down tiles wait on other pairs' gate/up
+  // tiles); knob ffn_pairs = n caps it further (measurement of placement-limited grids)
+  int pairs = std::min(num_sms() / 2, dev_info().max_pairs[mt == 256 ? 1 : 0]);
+  if (const int v = knob(Knob::kFfnPairs)) pairs = std::max(1, std::min(pairs, v));
+  if (pairs < 1) {
+    set_error("expert FFN: no CTA pair of this kernel fits on the device");
+    return README_ERR_UNSUPPORTED;
+  }
+  const int64_t tiles = mt_ub * ((d + kBN1 - 1) / kBN1 + (H + kBN2 - 1) / kBN2);
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  // README_FFN_DYNAMIC=1: dynamic tile fetch (counter = the spare readiness slot after the last m-tile).
-  // Measured 1-2 % slower than the static round-robin schedule at config 2 (profiles/SUMMARY.md), so off.
-  int dyn = 0;
-  if (const char* v = getenv("README_FFN_DYNAMIC")) dyn = atoi(v) != 0;
-  LayerArgs la{H, d, E, nseg, offsets, h, y, ready, dev_status, Fuse{src, static_cast<int>(rows), residual, 0},
-               expert_slot, {}, {}, 0, 0, pdl ? (xready && !wide ? 2 : 1) : 0, dyn,
-               static_cast<int>(nseg + (rows + 127) / 128), xready, g_trace_buf};
-  la.askip = 1;
-  if (const char* v = getenv("README_FFN_ASKIP")) la.askip = atoi(v) != 0;
-  if (const char* v = getenv("README_FFN_ORDER")) la.order = atoi(v);
+  LayerArgs la{};
+  la.H = H;
+  la.d = d;
+  la.E = E;
+  la.nseg = nseg;
+  la.offsets = offsets;
+  la.h = h;
+  la.y = y;
+  la.ready = ready;
+  la.abort = ready + ffn_layer_abort_index(rows);
+  la.dev_status = dev_status;
+  const int spin = knob(Knob::kFfnSpin);
+  la.spin_limit = spin <= 0 ? 1u : (spin >= 31 ? (1u << 31) : (1u << spin));
+  la.fz = Fuse{src, static_cast<int>(rows), residual, 0};
+  la.expert_slot = expert_slot;
+  la.pdl = pdl ? (xready ? 2 : 1) : 0;
+  la.xready = xready;
+  la.trace = g_trace_buf;
+  la.askip = knob(Knob::kFfnAskip) != 0;
+  la.order = knob(Knob::kFfnOrder);
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
@@ -1373,39 +980,25 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = wide ? kWSmemBytes : (mt == 128 ? kSmemBytesD : kSmemBytes);
+  cfg.dynamicSmemBytes = mt == 128 ? kSmemBytesD : kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-#define README_LAYER_LAUNCH(F, NB) \
-  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, NB, 256>, mX, mG, mU, mH, mD, la))
-#define README_LAYER_LAUNCH_D(F) \
-  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, 128, 128>, mX, mG, mU, mH, mD, la))
-#define README_WIDE_LAUNCH(F) \
-  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_wide_kernel<F>, mX, mG, mU, mH, mD, la))
-  if (wide) {
-    if (fuse == 2) README_WIDE_LAUNCH(2);
-    else if (fuse == 1) README_WIDE_LAUNCH(1);
-    else README_WIDE_LAUNCH(0);
-  } else if (nb == 64) {
-    if (fuse == 2) README_LAYER_LAUNCH(2, 64);
-    else if (fuse == 1) README_LAYER_LAUNCH(1, 64);
-    else README_LAYER_LAUNCH(0, 64);
-  } else if (mt == 128) {
-    if (fuse == 2) README_LAYER_LAUNCH_D(2);
-    else if (fuse == 1) README_LAYER_LAUNCH_D(1);
-    else README_LAYER_LAUNCH_D(0);
-  } else {
+#define README_LAYER_LAUNCH(F, MT) \
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, MT>, mX, mG, mU, mH, mD, la))
+  if (mt == 128) {
     if (fuse == 2) README_LAYER_LAUNCH(2, 128);
     else if (fuse == 1) README_LAYER_LAUNCH(1, 128);
     else README_LAYER_LAUNCH(0, 128);
+  } else {
+    if (fuse == 2) README_LAYER_LAUNCH(2, 256);
+    else if (fuse == 1) README_LAYER_LAUNCH(1, 256);
+    else README_LAYER_LAUNCH(0, 256);
   }
 #undef README_LAYER_LAUNCH
-#undef README_LAYER_LAUNCH_D
-#undef README_WIDE_LAUNCH
   README_CUDA(cudaGetLastError());
   return README_OK;
 }

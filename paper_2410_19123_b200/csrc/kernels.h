@@ -4,6 +4,13 @@
 
 namespace readme {
 
+// knobs.cpp: lab/test switches, read from the environment once, overridable by readme_debug_set_knob.
+enum class Knob : int {
+  kRoute, kRouteCluster, kRouteTile, kDispatch, kDispatchBulk, kCombineBulk, kPermUnrollD, kPermUnrollC,
+  kFfnKernel, kFfnMt, kFfnPairs, kFfnAskip, kFfnOrder, kFfnLab, kFfnSwap, kFfnSpin, kCount
+};
+int knob(Knob k);
+
 // route.cu
 size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
@@ -30,6 +37,7 @@ readme_status launch_dispatch_rmsnorm_gather(const void* x, readme_dtype dt, int
 readme_status launch_invert_perm(const int32_t* dest, int64_t n, int32_t* src, cudaStream_t st);  // src = dest^-1
 readme_status launch_set_offsets(int32_t* offs, int32_t T, cudaStream_t st);  // {0, T}
 readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st);  // measurement only
+readme_status launch_debug_hold_sms(int32_t n_ctas, int64_t ns, cudaStream_t st);  // test only
 readme_status launch_finalize_dispatch(const void* x, size_t row_bytes, int64_t T, int32_t k, int32_t E,
                                        const int32_t* topk_idx, const int32_t* offsets, int32_t* dest, int32_t* src,
                                        void* x_sorted, cudaStream_t st);

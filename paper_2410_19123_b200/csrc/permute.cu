@@ -453,18 +453,15 @@ void set_dispatch_carveout() {
 // 128-bit loads in flight per lane: 4 in the scatter dispatch (contiguous reads, scattered row writes),
 // 8 in the k = 1 gather combine (scattered row reads) — measured on one box, 3 runs each at 65536 rows:
 // dispatch 0.834 vs 0.79 of the copy peak with 4 vs 8, combine 0.89 vs 0.92 (README_PERM_UNROLL_D /
-// README_PERM_UNROLL_C = 4 | 8 override for A/B measurement)
-int perm_unroll(bool gather) {
-  const char* v = getenv(gather ? "README_PERM_UNROLL_C" : "README_PERM_UNROLL_D");
-  if (v) return atoi(v) == 8 ? 8 : 4;
-  return gather ? 8 : 4;
-}
+// knobs perm_unroll_c / perm_unroll_d = 4 | 8 override for A/B measurement)
+int perm_unroll(bool gather) { return knob(gather ? Knob::kPermUnrollC : Knob::kPermUnrollD) == 4 ? 4 : 8; }
 
 // Bulk-copy row moves (scatter dispatch; k = 1 combine without residual) for >= 4096 rows whose 16-row
-// ring fits in shared memory; README_DISPATCH_BULK / README_COMBINE_BULK = 0|1 override (A/B measurement).
-bool use_bulk_moves(int64_t rows, size_t row_bytes, const char* env) {
+// ring fits in shared memory; knobs dispatch_bulk / combine_bulk = 0|1 override (A/B measurement).
+bool use_bulk_moves(int64_t rows, size_t row_bytes, Knob which) {
   if (row_bytes % 16 != 0 || static_cast<size_t>(kBulkCopiers) * kBulkSlots * row_bytes > kBulkMaxSmem) return false;
-  if (const char* v = getenv(env)) return atoi(v) != 0;
+  const int v = knob(which);
+  if (v >= 0) return v != 0;
   return rows >= 4096;
 }
 
@@ -501,7 +498,7 @@ readme_status launch_dispatch(const void* x, size_t row_bytes, int64_t T, int32_
                               void* x_sorted, uint32_t* dev_status, cudaStream_t st) {
   const int64_t nslots = T * k;
   if (nslots == 0) return README_OK;
-  if (use_bulk_moves(nslots, row_bytes, "README_DISPATCH_BULK"))
+  if (use_bulk_moves(nslots, row_bytes, Knob::kDispatchBulk))
     return launch_move_rows_bulk<false>(x, row_bytes, nslots, k, dest, x_sorted, dev_status, st);
   if (perm_unroll(false) == 8)
     dispatch_kernel<8><<<grid_for_rows(nslots), kPermThreads, 0, st>>>(
@@ -531,6 +528,24 @@ readme_status launch_dispatch_gather(const void* x, size_t row_bytes, int64_t ro
 __global__ void debug_mark_kernel(uint64_t* slot) { *slot = globaltimer_ns(); }
 readme_status launch_debug_mark(uint64_t* slot, cudaStream_t st) {
   debug_mark_kernel<<<1, 1, 0, st>>>(slot);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
+// Test only: occupy whole SMs for `ns` nanoseconds (one CTA per SM: each takes the maximum shared memory),
+// so a kernel launched behind it on another stream finds only the remaining SMs.
+constexpr int kHoldSmem = 227 * 1024;
+__global__ void debug_hold_kernel(int64_t ns) {
+  extern __shared__ uint8_t hold_smem[];
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < static_cast<uint64_t>(ns)) __nanosleep(1000);
+    hold_smem[0] = 1;
+  }
+}
+readme_status launch_debug_hold_sms(int32_t n_ctas, int64_t ns, cudaStream_t st) {
+  README_CUDA(cudaFuncSetAttribute(debug_hold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHoldSmem));
+  debug_hold_kernel<<<n_ctas, 32, kHoldSmem, st>>>(ns);
   README_CUDA(cudaGetLastError());
   return README_OK;
 }
@@ -599,7 +614,7 @@ readme_status launch_combine(const void* y_sorted, readme_dtype dt, int64_t T, i
                              const int32_t* dest, const float* topk_w, const void* residual, void* y,
                              uint32_t* dev_status, cudaStream_t st) {
   if (T == 0) return README_OK;
-  if (k == 1 && residual == nullptr && use_bulk_moves(T, static_cast<size_t>(H) * dt_size(dt), "README_COMBINE_BULK"))
+  if (k == 1 && residual == nullptr && use_bulk_moves(T, static_cast<size_t>(H) * dt_size(dt), Knob::kCombineBulk))
     return launch_move_rows_bulk<true>(y_sorted, static_cast<size_t>(H) * dt_size(dt), T, 1, dest, y, dev_status, st);
   const int grid = grid_for_rows(T);
   if (k == 1 && residual == nullptr) {

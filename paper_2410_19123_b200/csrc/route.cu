@@ -47,7 +47,7 @@ RouteGeom route_geom(int64_t T, int32_t E, int32_t k) {
   // so lookback chains stay short; README_ROUTE_TILE overrides (A/B measurement)
   int cap = 256;
   while (cap > 32 && (T + cap - 1) / cap < 148) cap >>= 1;
-  if (const char* v = getenv("README_ROUTE_TILE")) cap = atoi(v) > 0 ? atoi(v) : cap;
+  if (const int v = knob(Knob::kRouteTile)) cap = v > 0 ? v : cap;
   if (tt > cap) tt = cap;
   if (tt < 1) tt = 1;
   RouteGeom g;
@@ -619,12 +619,12 @@ int max_route_cluster() {
   return cache[dev];
 }
 
-// Which route implementation a batch takes: README_ROUTE=lookback|cluster overrides (A/B measurement).
+// Which route implementation a batch takes: knob route = 1 (cluster) | 2 (lookback) overrides (A/B
+// measurement).
 bool use_cluster_route(int64_t T, int32_t k) {
-  if (const char* v = getenv("README_ROUTE")) {
-    if (strcmp(v, "lookback") == 0) return false;
-    if (strcmp(v, "cluster") == 0) return true;
-  }
+  const int v = knob(Knob::kRoute);
+  if (v == 2) return false;
+  if (v == 1) return true;
   return T * k <= kClusterMaxSlots;
 }
 
@@ -640,8 +640,7 @@ ClusterGeom cluster_geom(int64_t T, int32_t E, int32_t k) {
   const int cmax = max_route_cluster();
   int C = 1;
   while (C < cmax && C < subtiles) C <<= 1;  // one sub-tile per CTA while the cluster can grow
-  if (const char* v = getenv("README_ROUTE_CLUSTER")) {  // A/B measurement: force the cluster size
-    const int f = atoi(v);
+  if (const int f = knob(Knob::kRouteCluster)) {  // A/B measurement: force the cluster size
     if (f == 1 || f == 2 || f == 4 || f == 8 || (f == 16 && cmax == 16)) C = f;
   }
   g.C = C;

@@ -35,7 +35,8 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_ep_signal", "readme_ep_wait", "readme_ep_publish_counts", "readme_ep_plan", "readme_ep_dispatch",
            "readme_ep_expert_ffn",
            "readme_set_device", "readme_status_string", "readme_last_error",
-           "readme_version", "readme_debug_trace", "readme_debug_mark")
+           "readme_version", "readme_debug_trace", "readme_debug_mark", "readme_debug_set_knob",
+           "readme_debug_get_knob", "readme_debug_reset_knob", "readme_debug_hold_sms")
 
 
 class ReadmeError(RuntimeError):
@@ -56,7 +57,7 @@ _SIGS = {
     "readme_dispatch": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
     "readme_expert_ffn_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, ctypes.c_int]),
     "readme_expert_ffn": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
-                                         _vp, _sz, _vp]),
+                                         _vp, _vp, _sz, _vp]),
     "readme_expert_gate_up": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
                                              _vp]),
     "readme_expert_down": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
@@ -79,8 +80,8 @@ _SIGS = {
     "readme_scheduler_queued": (_i64, [_vp, _i32]),
     "readme_scheduler_next_batch": (_i64, [_vp, _i64, _vp, _vp]),
     "readme_permanent_expert_workspace_bytes": (_sz, [_i64, _i32, _i32, ctypes.c_int]),
-    "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz,
-                                               _vp]),
+    "readme_permanent_expert": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                               _sz, _vp]),
     "readme_router_workspace_bytes": (_sz, [_i64, _i32]),
     "readme_router_step_workspace_bytes": (_sz, [_i64, _i32]),
     "readme_router_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, ctypes.c_float, _vp, _vp, _vp,
@@ -113,6 +114,10 @@ _SIGS = {
     "readme_version": (ctypes.c_int, []),
     "readme_debug_trace": (None, [_vp]),
     "readme_debug_mark": (ctypes.c_int, [_i32, _vp]),
+    "readme_debug_set_knob": (ctypes.c_int, [ctypes.c_char_p, _i32]),
+    "readme_debug_get_knob": (ctypes.c_int, [ctypes.c_char_p, _vp]),
+    "readme_debug_reset_knob": (ctypes.c_int, [ctypes.c_char_p]),
+    "readme_debug_hold_sms": (ctypes.c_int, [_i32, _i64, _vp]),
 }
 
 
@@ -232,8 +237,9 @@ def expert_ffn_workspace_bytes(rows: int, H: int, E: int, d: int, dtype: torch.d
 
 def expert_ffn(x_sorted: torch.Tensor, offsets: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor,
                w_down: torch.Tensor, n_src: int = 1, out: torch.Tensor | None = None,
-               ws: torch.Tensor | None = None) -> torch.Tensor:
-    """a6-a7: grouped SwiGLU expert FFN over expert-contiguous rows (readme_expert_ffn)."""
+               ws: torch.Tensor | None = None, dev_status: torch.Tensor | None = None) -> torch.Tensor:
+    """a6-a7: grouped SwiGLU expert FFN over expert-contiguous rows (readme_expert_ffn). dev_status: optional
+    uint32/int32 device word that README_DEV_SCHED_TIMEOUT is OR-ed into."""
     rows, H = x_sorted.shape
     E, d, H2 = w_gate.shape
     if H2 != H or tuple(w_up.shape) != (E, d, H) or tuple(w_down.shape) != (E, H, d):
@@ -247,7 +253,7 @@ def expert_ffn(x_sorted: torch.Tensor, offsets: torch.Tensor, w_gate: torch.Tens
     st = _prep(x_sorted, offsets, w_gate, w_up, w_down, out, ws)
     _check("readme_expert_ffn", lib().readme_expert_ffn(
         _ptr(x_sorted), _dt(x_sorted), rows, H, E, d, n_src, _ptr(offsets), _ptr(w_gate), _ptr(w_up),
-        _ptr(w_down), _ptr(out), _ptr(ws), ws.numel(), st))
+        _ptr(w_down), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
     return out
 
 
@@ -426,7 +432,8 @@ class ExpertScheduler:
 
 
 def permanent_expert(x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor,
-                     y: torch.Tensor, ws: torch.Tensor | None = None) -> torch.Tensor:
+                     y: torch.Tensor, ws: torch.Tensor | None = None,
+                     dev_status: torch.Tensor | None = None) -> torch.Tensor:
     """y += F_perm(x) for every token (the permanent expert; readme_permanent_expert)."""
     T, H = x.shape
     dp = w_gate.shape[0]
@@ -435,7 +442,8 @@ def permanent_expert(x: torch.Tensor, w_gate: torch.Tensor, w_up: torch.Tensor, 
         ws = torch.empty(need, dtype=torch.uint8, device=x.device)
     st = _prep(x, w_gate, w_up, w_down, y, ws)
     _check("readme_permanent_expert", lib().readme_permanent_expert(
-        _ptr(x), _dt(x), T, H, dp, _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(y), _ptr(ws), ws.numel(), st))
+        _ptr(x), _dt(x), T, H, dp, _ptr(w_gate), _ptr(w_up), _ptr(w_down), _ptr(y),
+        _ptr(dev_status), _ptr(ws), ws.numel(), st))
     return y
 
 
@@ -670,3 +678,43 @@ def ep_expert_ffn(x_recv: torch.Tensor, seg_offsets, w_gate, w_up, w_down, row_m
     _check("readme_ep_expert_ffn", lib().readme_ep_expert_ffn(
         _ptr(x_recv), _dt(x_recv), rows_cap, H, El, d, G, _ptr(seg_offsets), _ptr(w_gate), _ptr(w_up),
         _ptr(w_down), _ptr(row_map), _ptrs(peer_out), res, vrows, _ptr(dev_status), _ptr(ws), ws.numel(), st))
+
+
+# ---- lab / test switches (readme_debug_set_knob) ---------------------------------------------
+
+def set_knob(name: str, value: int) -> None:
+    _check("readme_debug_set_knob", lib().readme_debug_set_knob(name.encode(), int(value)))
+
+
+def get_knob(name: str) -> int:
+    v = ctypes.c_int32(0)
+    _check("readme_debug_get_knob", lib().readme_debug_get_knob(name.encode(), ctypes.byref(v)))
+    return int(v.value)
+
+
+def reset_knob(name: str) -> None:
+    _check("readme_debug_reset_knob", lib().readme_debug_reset_knob(name.encode()))
+
+
+class knobs:
+    """Context manager: `with rd.knobs(ffn_mt=128, route=2): ...` sets the switches, restores them after."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = get_knob(k)
+            set_knob(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_knob(k, v)
+
+
+def debug_hold_sms(n_ctas: int, ns: int, stream: torch.cuda.Stream) -> None:
+    """Test only: occupy n_ctas SMs for ns nanoseconds on `stream` (readme_debug_hold_sms)."""
+    lib().readme_set_device(stream.device.index)
+    _check("readme_debug_hold_sms", lib().readme_debug_hold_sms(int(n_ctas), int(ns), ctypes.c_void_p(stream.cuda_stream)))

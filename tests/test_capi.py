@@ -71,13 +71,13 @@ def test_route_workspace_too_small(lib):
 def test_ffn_rejects_bad_shapes(lib):
     d = ctypes.c_void_p(16)
     # H not a multiple of 8
-    assert lib.readme_expert_ffn(d, 1, 10, 12, 8, 64, 1, d, d, d, d, d, d, 1 << 30, None) == 1
+    assert lib.readme_expert_ffn(d, 1, 10, 12, 8, 64, 1, d, d, d, d, d, None, d, 1 << 30, None) == 1
     # d not a multiple of 8
-    assert lib.readme_expert_ffn(d, 1, 10, 64, 8, 60, 1, d, d, d, d, d, d, 1 << 30, None) == 1
+    assert lib.readme_expert_ffn(d, 1, 10, 64, 8, 60, 1, d, d, d, d, d, None, d, 1 << 30, None) == 1
     # unknown dtype
-    assert lib.readme_expert_ffn(d, 7, 10, 64, 8, 64, 1, d, d, d, d, d, d, 1 << 30, None) == 2
+    assert lib.readme_expert_ffn(d, 7, 10, 64, 8, 64, 1, d, d, d, d, d, None, d, 1 << 30, None) == 2
     # misaligned pointer
-    assert lib.readme_expert_ffn(ctypes.c_void_p(18), 1, 10, 64, 8, 64, 1, d, d, d, d, d, d, 1 << 30, None) == 1
+    assert lib.readme_expert_ffn(ctypes.c_void_p(18), 1, 10, 64, 8, 64, 1, d, d, d, d, d, None, d, 1 << 30, None) == 1
 
 
 def test_no_cpu_fallback_in_binding():
@@ -85,3 +85,16 @@ def test_no_cpu_fallback_in_binding():
     from paper_2410_19123_b200 import readme
     with pytest.raises(ValueError, match="CUDA"):
         readme.route(torch.zeros(4, 8), 1)
+
+
+def test_knobs_set_get_reset(lib):
+    """Lab switches: read once from the environment, overridable, unknown names rejected synchronously."""
+    v = ctypes.c_int32(-99)
+    assert lib.readme_debug_get_knob(b"ffn_mt", ctypes.byref(v)) == 0 and v.value == 0
+    assert lib.readme_debug_set_knob(b"ffn_mt", 128) == 0
+    assert lib.readme_debug_get_knob(b"ffn_mt", ctypes.byref(v)) == 0 and v.value == 128
+    assert lib.readme_debug_reset_knob(b"ffn_mt") == 0
+    assert lib.readme_debug_get_knob(b"ffn_mt", ctypes.byref(v)) == 0 and v.value == 0
+    assert lib.readme_debug_set_knob(b"no_such_knob", 1) == 1
+    assert b"unknown knob" in lib.readme_last_error()
+    assert lib.readme_debug_get_knob(b"ffn_spin", ctypes.byref(v)) == 0 and v.value == 25

@@ -5,6 +5,8 @@ seeded inputs. Rules (BASELINE.json north_star):
   FP outputs: per-token inf-norm relative error <= 2e-2 (bf16) / <= 1e-4 (fp32); topk_w fp32 rule,
   and exactly 1.0f for k=1.
 Sizes span several tiles and ragged tails; full-size config 2 is checked on sampled tokens."""
+import time
+
 import numpy as np
 import pytest
 import torch
@@ -24,6 +26,23 @@ def rd():
     build.build()
     readme.lib()
     return readme
+
+
+@pytest.fixture
+def knob(rd):
+    """knob(name, value): set a library lab switch (readme_debug_set_knob) for this test only."""
+    touched = []
+
+    def set_(name, value):
+        touched.append(name)
+        rd.set_knob(name, int(value))
+
+    yield set_
+    for n in touched:
+        rd.reset_knob(n)
+
+
+ROUTE_IMPL = {"cluster": 1, "lookback": 2}
 
 
 def _np(t):
@@ -65,10 +84,10 @@ ROUTE_CASES = [
 
 @pytest.mark.parametrize("impl", ["cluster", "lookback"])
 @pytest.mark.parametrize("T,E,k,kind,ldt", ROUTE_CASES)
-def test_route_bit_exact(rd, monkeypatch, impl, T, E, k, kind, ldt):
+def test_route_bit_exact(rd, knob, impl, T, E, k, kind, ldt):
     # both route implementations: the single-launch cluster route (default up to 256K slots) and the
     # multi-CTA decoupled-lookback route (larger batches)
-    monkeypatch.setenv("README_ROUTE", impl)
+    knob("route", ROUTE_IMPL[impl])
     lg = synth.router_logits(T, E, seed=T + E) if kind == "normal" else synth.near_tie_logits(T, E, seed=T + E)
     lg_t = synth.to_torch(lg, ldt)
     ref = oracle.route(lg_t, k)  # the oracle sees exactly the bits the GPU sees
@@ -78,11 +97,11 @@ def test_route_bit_exact(rd, monkeypatch, impl, T, E, k, kind, ldt):
 
 
 @pytest.mark.parametrize("impl", [None, "cluster"])
-def test_route_large_batch(rd, monkeypatch, impl):
+def test_route_large_batch(rd, knob, impl):
     # 300K slots: past the cluster route's default range (lookback), and forced through the cluster route
     # (each of the 16 CTAs walks ~19 sub-tiles, carrying its running per-expert counts)
     if impl:
-        monkeypatch.setenv("README_ROUTE", impl)
+        knob("route", ROUTE_IMPL[impl])
     lg = synth.router_logits(150001, 8, seed=5)
     ref = oracle.route(lg, 2)
     plan = rd.route(torch.from_numpy(lg).to(DEV), 2)
@@ -150,9 +169,9 @@ def test_dispatch_bit_exact(rd, T, H, k, dt):
 
 
 @pytest.mark.parametrize("bulk", ["0", "1"])
-def test_dispatch_bad_index_flagged(rd, monkeypatch, bulk):
+def test_dispatch_bad_index_flagged(rd, knob, bulk):
     """An out-of-range dest entry is flagged in dev_status and skipped; every other row still lands."""
-    monkeypatch.setenv("README_DISPATCH_BULK", bulk)
+    knob("dispatch_bulk", bulk)
     T, H = 6000, 256
     x = synth.to_torch(synth.tokens(T, H, seed=5), "bf16").to(DEV)
     dest = torch.from_numpy(np.random.default_rng(6).permutation(T).astype(np.int32)).to(DEV)
@@ -171,9 +190,9 @@ def test_dispatch_bad_index_flagged(rd, monkeypatch, bulk):
 
 
 @pytest.mark.parametrize("bulk", ["0", "1"])
-def test_combine_k1_bad_index_flagged(rd, monkeypatch, bulk):
+def test_combine_k1_bad_index_flagged(rd, knob, bulk):
     """k = 1 gather combine: an out-of-range dest entry is flagged and its output row left untouched."""
-    monkeypatch.setenv("README_COMBINE_BULK", bulk)
+    knob("combine_bulk", bulk)
     T, H = 6000, 256
     ys = synth.to_torch(synth.tokens(T, H, seed=7), "bf16").to(DEV)
     dest = torch.from_numpy(np.random.default_rng(8).permutation(T).astype(np.int32)).to(DEV)
@@ -228,16 +247,18 @@ def _ffn_case(T, H, d, E, k, dt, seed, skew=None):
     return x, lg, wg, wu, wd
 
 
-def _set_kernel(monkeypatch, kernel):
-    """merged / merged-nb64 / merged-nb128 (single launch, tile width forced) / split / 1cta."""
-    if kernel.startswith("merged-nb"):  # the double-buffered 256-column tile at a forced width
-        monkeypatch.setenv("README_FFN_NB", kernel[len("merged-nb"):])
-        monkeypatch.setenv("README_FFN_WIDE", "0")
+FFN_KERNEL = {"merged": 0, "split": 1, "unfused": 2}
+
+
+def _set_kernel(knob, kernel):
+    """merged (single launch, 256-row m-tiles above 1024 rows) / merged-mt128 / split (two launches)."""
+    if kernel == "merged-mt128":
+        knob("ffn_mt", 128)
         kernel = "merged"
-    monkeypatch.setenv("README_FFN_KERNEL", kernel)
+    knob("ffn_kernel", FFN_KERNEL[kernel])
 
 
-KERNELS = ["merged", "merged-nb64", "merged-nb128", "split", "1cta"]
+KERNELS = ["merged", "merged-mt128", "split"]
 
 
 @pytest.mark.parametrize("T,H,d,E,k,skew", [
@@ -250,8 +271,8 @@ KERNELS = ["merged", "merged-nb64", "merged-nb128", "split", "1cta"]
     (1024, 256, 128, 4, 1, None),      # counts ~256 -> exact and near-exact tiles
 ])
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_expert_ffn_bf16_teacher_forced(rd, monkeypatch, kernel, T, H, d, E, k, skew):
-    _set_kernel(monkeypatch, kernel)
+def test_expert_ffn_bf16_teacher_forced(rd, knob, kernel, T, H, d, E, k, skew):
+    _set_kernel(knob, kernel)
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + H, skew=skew)
     plan = rd.route(torch.from_numpy(lg).to(DEV), k)
     xs = rd.dispatch(x.to(DEV), plan.dest, k)
@@ -293,9 +314,9 @@ def test_gate_up_and_down_separately(rd, dt):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
+def test_expert_ffn_tile_edges(rd, knob, kernel):
     """Segment sizes on every tile boundary: empty, 1 row, 64/128/256 +- 1 (M=128 vs M=256 tails)."""
-    _set_kernel(monkeypatch, kernel)
+    _set_kernel(knob, kernel)
     counts = [0, 1, 63, 64, 65, 127, 128, 129, 255, 256, 257, 383, 384, 385, 511, 512]
     E, H, d = len(counts), 128, 136
     off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
@@ -307,35 +328,27 @@ def test_expert_ffn_tile_edges(rd, monkeypatch, kernel):
     assert rel_err(_np(ys), ref) <= BF16_TOL
 
 
+# variants of the single-launch FFN that compute every output element from the same K-ordered MMAs:
+# (m-tile rows, second CTA skips A loads of <= 64-row tiles, max CTA pairs, gate/up N-tile-fastest order)
+FFN_VARIANTS = [(256, 1, 0, 0), (128, 1, 0, 0), (128, 0, 0, 0), (256, 0, 0, 0), (256, 1, 3, 0), (128, 1, 1, 0),
+                (256, 1, 0, 1), (128, 1, 0, 1)]
+
+
 @pytest.mark.parametrize("T,d,skew", [(256, 5504, "zipf"), (2000, 264, None), (40, 136, "empty")])
-def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
-    """The half-width tiles (decode) and the full-width tiles compute every output element from the same
-    K-ordered MMAs: bitwise equal results, with and without the fused residual scatter."""
+def test_ffn_variants_bitwise_equal(rd, knob, T, d, skew):
+    """128-row vs 256-row m-tiles, with and without the A-load skip, on 3 and 1 CTA pairs (every pair walks
+    a long tile list; the down tiles wait on gate/up tiles of the same few pairs) and in N-tile-fastest
+    order: bitwise equal results, with and without the fused residual scatter."""
     H, E = 4096 if d == 5504 else 256, 8
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=T + d, skew=skew)
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    # half-width, 256-column, wide-N tiles, the 256-column tile with dynamic tile fetch, 128-row vs
-    # 256-row m-tiles, and the second CTA loading its (unused) A rows of tiles of <= 64 rows or not
-    for cfg in (("64", "0", "0", "256", "1"), ("128", "0", "0", "256", "1"),
-                ("128", "1", "0", "256", "1"), ("128", "0", "1", "256", "1"),
-                ("128", "0", "0", "128", "1"), ("128", "0", "1", "128", "1"),
-                ("128", "0", "0", "128", "0"), ("128", "0", "0", "256", "0"),
-                ("128", "0", "0", "256", "1", "3"), ("128", "0", "0", "128", "1", "1"),
-                ("128", "0", "0", "256", "1", "1000", "1"), ("128", "0", "1", "128", "1", "1000", "1")):
-        # optional 6th field: at most that many CTA pairs (every pair walks a long tile list; the down tiles
-        # wait on gate/up tiles of the same few pairs); 7th: gate/up tiles in N-tile-fastest order
-        pairs = cfg[5] if len(cfg) > 5 else "1000"
-        order = cfg[6] if len(cfg) > 6 else "0"
-        nb, wide, dyn, mt, askip = cfg[:5]
-        monkeypatch.setenv("README_FFN_ORDER", order)
-        monkeypatch.setenv("README_FFN_PAIRS", pairs)
-        monkeypatch.setenv("README_FFN_ASKIP", askip)
-        monkeypatch.setenv("README_FFN_NB", nb)
-        monkeypatch.setenv("README_FFN_WIDE", wide)
-        monkeypatch.setenv("README_FFN_DYNAMIC", dyn)
-        monkeypatch.setenv("README_FFN_MT", mt)
+    for mt, askip, pairs, order in FFN_VARIANTS:
+        knob("ffn_mt", mt)
+        knob("ffn_askip", askip)
+        knob("ffn_pairs", pairs)
+        knob("ffn_order", order)
         y, _ = rd.moe_layer(x, wg, wu, wd, logits=lg, residual=x)
         plan = rd.route(lg, 1)
         ys = rd.expert_ffn(rd.dispatch(x, plan.dest, 1), plan.offsets, wg, wu, wd)
@@ -343,6 +356,71 @@ def test_tile_widths_bitwise_equal(rd, monkeypatch, T, d, skew):
     torch.cuda.synchronize()
     for o in outs[1:]:
         assert torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1])
+
+
+# ---- co-residency of the single-launch FFN (its down tiles wait on other CTA pairs' gate/up tiles) ------
+
+def _starve_setup(rd, T=8192, H=1024, d=1024, E=8):
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=601)
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    plan = rd.route(torch.from_numpy(lg).to(DEV), 1)
+    xs = rd.dispatch(x.to(DEV), plan.dest, 1)
+    ref = rd.expert_ffn(xs, plan.offsets, *W)  # uncontended launch
+    torch.cuda.synchronize()
+    n_hold = torch.cuda.get_device_properties(0).multi_processor_count - 8
+    return x.to(DEV), lg, plan, xs, W, ref, n_hold
+
+
+def test_ffn_sm_starved_recovers(rd):
+    """140 of 148 SMs held by another stream's kernel for 0.3 s while the FFN launches: the few pairs that
+    fit wait for the rest (bounded polls, far below the give-up limit) and the result is bitwise the
+    uncontended one, dev_status clean."""
+    x, lg, plan, xs, W, ref, n_hold = _starve_setup(rd)
+    hold, work = torch.cuda.Stream(), torch.cuda.Stream()
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    out = torch.full_like(ref, 7.0)
+    torch.cuda.synchronize()
+    rd.debug_hold_sms(n_hold, 300_000_000, hold)
+    time.sleep(0.05)
+    with torch.cuda.stream(work):
+        rd.expert_ffn(xs, plan.offsets, *W, out=out, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert torch.equal(out, ref)
+    # the whole layer (gather dispatch with row flags, FFN behind it with PDL) under the same starvation
+    y0, _ = rd.moe_layer(x, *W, logits=torch.from_numpy(lg).to(DEV), residual=x)
+    torch.cuda.synchronize()
+    y1 = torch.full_like(y0, 7.0)
+    plan1 = rd.new_plan(x.shape[0], 8, 1, DEV)
+    torch.cuda.synchronize()
+    rd.debug_hold_sms(n_hold, 300_000_000, hold)
+    time.sleep(0.05)
+    with torch.cuda.stream(work):
+        rd.moe_layer(x, *W, logits=torch.from_numpy(lg).to(DEV), residual=x, plan=plan1, out=y1)
+    torch.cuda.synchronize()
+    assert int(plan1.dev_status.item()) == 0
+    assert torch.equal(y1, y0)
+
+
+def test_ffn_sm_starved_gives_up_without_wrong_values(rd, knob):
+    """The same starvation held for 2 s with the poll limit cut to 2^12: a readiness wait gives up, the
+    launch reports README_DEV_SCHED_TIMEOUT, and every output element is either untouched (the sentinel)
+    or exactly the uncontended value — never one computed from unready rows."""
+    x, lg, plan, xs, W, ref, n_hold = _starve_setup(rd)
+    knob("ffn_spin", 12)
+    hold, work = torch.cuda.Stream(), torch.cuda.Stream()
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    out = torch.full_like(ref, 7.0)
+    torch.cuda.synchronize()
+    rd.debug_hold_sms(n_hold, 2_000_000_000, hold)
+    time.sleep(0.05)
+    with torch.cuda.stream(work):
+        rd.expert_ffn(xs, plan.offsets, *W, out=out, dev_status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & rd.README_DEV_SCHED_TIMEOUT
+    touched = out != 7.0
+    assert torch.equal(out[touched], ref[touched])
+    assert int(touched.sum().item()) < out.numel()  # the give-up really stopped stores
 
 
 def test_expert_ffn_segments_n_src(rd):
@@ -360,20 +438,20 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("path", ["fused", "gather", "scatter", "lookback", "split", "unfused", "1cta"])
+@pytest.mark.parametrize("path", ["fused", "gather", "scatter", "lookback", "split", "unfused"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
                                            ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
                                            ("bf16", 3000, 1024, 1376, 8, 1)])
-def test_moe_layer_end_to_end(rd, monkeypatch, path, dt, T, H, d, E, k):
+def test_moe_layer_end_to_end(rd, knob, path, dt, T, H, d, E, k):
     # fused: cluster route -> gather dispatch with per-row flags -> single-launch FFN waiting per tile;
     # lookback: multi-CTA route -> finalize fused into the dispatch -> FFN behind a whole-grid PDL wait
     # gather / scatter force the dispatch form (by default gather from 2048 rows up)
     if path == "lookback":
-        monkeypatch.setenv("README_ROUTE", "lookback")
+        knob("route", 2)
     elif path in ("gather", "scatter"):
-        monkeypatch.setenv("README_DISPATCH", path)
+        knob("dispatch", 2 if path == "gather" else 1)
     elif path != "fused":
-        monkeypatch.setenv("README_FFN_KERNEL", path)
+        knob("ffn_kernel", FFN_KERNEL[path])
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
     res = synth.to_torch(synth.residual(T, H, seed=12), dt)
     y, plan = rd.moe_layer(x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV), k=k,
@@ -483,7 +561,7 @@ def test_build_experts_bit_exact(rd):
 
 
 @pytest.mark.parametrize("with_residual", [False, True])
-def test_fused_scatter_vs_unfused(rd, monkeypatch, with_residual):
+def test_fused_scatter_vs_unfused(rd, knob, with_residual):
     """k=1: the combine fused into GEMM2's epilogue (y[src[r]] = res + acc, one rounding) equals the unfused
     sequence bit for bit without a residual; with one, the unfused path rounds twice (y_sorted, then
     res + y_sorted), so both are checked against the oracle instead."""
@@ -494,7 +572,7 @@ def test_fused_scatter_vs_unfused(rd, monkeypatch, with_residual):
     lgt = torch.from_numpy(lg).to(DEV)
     r_dev = res.to(DEV) if res is not None else None
     y1, _ = rd.moe_layer(x.to(DEV), *W, logits=lgt, residual=r_dev)
-    monkeypatch.setenv("README_FFN_KERNEL", "unfused")
+    knob("ffn_kernel", 2)
     y2, _ = rd.moe_layer(x.to(DEV), *W, logits=lgt, residual=r_dev)
     torch.cuda.synchronize()
     if not with_residual:
@@ -716,13 +794,13 @@ def test_dispatch_rmsnorm(rd, dt, k):
 
 @pytest.mark.parametrize("path", ["fused", "gather", "split"])
 @pytest.mark.parametrize("dt,k,L", [("bf16", 1, 4), ("bf16", 2, 3), ("f32", 1, 3)])
-def test_moe_stack_end_to_end(rd, monkeypatch, path, dt, k, L):
+def test_moe_stack_end_to_end(rd, knob, path, dt, k, L):
     # fused: gather-form pre-norm dispatch with row flags + single-launch FFN (k = 1, bf16); split: the
     # scatter dispatch + two-launch FFN
     if path == "split":
-        monkeypatch.setenv("README_FFN_KERNEL", "split")
+        knob("ffn_kernel", 1)
     elif path == "gather":
-        monkeypatch.setenv("README_DISPATCH", "gather")
+        knob("dispatch", 2)
     T, H, d, E = 600, 256, 256, 8
     x = synth.to_torch(synth.tokens(T, H, seed=161), dt)
     ids = synth.assignments_markov(2, T // 2, E, 0.672, seed=162)
