@@ -400,19 +400,28 @@ struct LayerArgs {
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
   int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (knob ffn_askip)
   int order;               // lab: 1 = gate/up tiles N-tile fastest (knob ffn_order)
+  int swap_rows;           // segment tails of <= swap_rows rows run as swap-AB tiles (knob ffn_swap; 0 = none)
 };
 
 struct LTile {
   int mode, g, mt, m0, rows, n0;
-  bool m256;
+  bool m256;  // M = 256 pair MMA (each CTA 128 A rows), else M = 128 (64 rows per CTA)
+  bool swap;  // swap-AB tail tile: weights are the MMA's M side, the tile's rows its N side
 };
 
 constexpr int kBN1 = 128;  // h columns per gate/up tile ([gate 64 | up 64] rows per CTA)
 constexpr int kBN2 = 256;  // output columns per down tile (128 W_down rows per CTA)
 
+// Tile list of the single-launch kernel: [every gate/up tile][every down tile]; inside each phase segment ->
+// N tile -> m-tile (m fastest: the 4-5 pairs working on one expert's m-tiles read the same weight tile at the
+// same time, so L2 serves it once). A segment's last m-tile of <= swap_rows rows runs swap-AB in place (it
+// stays next to the full m-tiles that share its weight tile: moving the cheap tails to the end of each phase
+// for a longest-first schedule re-read their weights from DRAM and measured 9 % slower at config 2).
+// Down tiles come after every gate/up tile, so every wait is on a tile earlier in the global order
+// (deadlock-free whenever the grid is co-resident).
 template <int kMT, class SM>
-__device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int& gcur1,
-                                             int& gcur2, bool nfast = false) {
+__device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int swap_rows,
+                                             int& gcur1, int& gcur2, bool nfast = false) {
   LTile tl;
   int local, g, NT;
   if (t < T1) {
@@ -431,8 +440,7 @@ __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int 
   }
   const int cnt = s.seg_off[g + 1] - s.seg_off[g];
   const int mt_g = (cnt + kMT - 1) / kMT;
-  // m-tile fastest (default: consecutive pairs share a weight tile) or, for gate/up tiles with nfast (lab
-  // knob ffn_order = 1), N-tile fastest (consecutive pairs share an A tile)
+  // m-tile fastest (default) or, for gate/up tiles with nfast (lab knob ffn_order = 1), N-tile fastest
   const bool nf = nfast && tl.mode == 0;
   const int nt = nf ? local % NT : local / mt_g, mt = nf ? local / NT : local % mt_g;
   tl.g = g;
@@ -440,6 +448,7 @@ __device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int 
   tl.m0 = s.seg_off[g] + mt * kMT;
   tl.rows = min(kMT, cnt - mt * kMT);
   tl.m256 = tl.rows > 128;
+  tl.swap = tl.rows <= swap_rows;  // only a segment's last m-tile can be that short
   tl.n0 = nt * (tl.mode == 0 ? kBN1 : kBN2);
   return tl;
 }
@@ -461,11 +470,84 @@ __device__ __forceinline__ void sched_give_up(const LayerArgs& la) {
   __threadfence();
 }
 
+// Epilogue of a swap-AB tile (a segment tail of <= 64 rows): this CTA's TMEM lane = weight row (gate/up: 4 x
+// [16 gate | the same 16 up] neurons, one group per epilogue warp; down: 128 output columns), column j = the
+// tile's row m0 + j. Processed 32 columns at a time. Same fp32 values and roundings as the normal epilogue.
+template <int kFuse>
+__device__ __forceinline__ void swap_epilogue(const LayerArgs& la, const LTile& tl, uint32_t tacc, uint32_t cta,
+                                              int q, int lane, bool store) {
+  const int H = la.H, d = la.d;
+  for (int c = 0; c < tl.rows; c += 32) {  // warp-uniform
+    uint32_t r[32];
+    tc::tmem_ld32(tacc + static_cast<uint32_t>(c), r);
+    tc::tmem_wait_ld();
+    if (tl.mode == 0) {
+      // lanes 0-15 hold gate, 16-31 up of neurons n; lanes 0-15 finish columns c..c+15, lanes 16-31 c+16..c+31
+      const bool lo = lane < 16;
+      const int neuron = tl.n0 + 64 * static_cast<int>(cta) + 16 * q + (lane & 15);
+      const bool ok = store && neuron < d;
+      __nv_bfloat16* hcol = la.h + neuron;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float send = __uint_as_float(lo ? r[16 + j] : r[j]);
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+        const float g = lo ? __uint_as_float(r[j]) : recv, u = lo ? recv : __uint_as_float(r[16 + j]);
+        const int tok = c + (lo ? j : 16 + j);
+        if (ok && tok < tl.rows) hcol[static_cast<int64_t>(tl.m0 + tok) * d] = __float2bfloat16_rn(tc::silu(g) * u);
+      }
+    } else {
+      const int col = tl.n0 + 128 * static_cast<int>(cta) + 32 * q + lane;
+      const bool ok = store && col < H;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int tok = c + j;
+        if (tok >= tl.rows) break;  // warp-uniform
+        const int64_t rr = tl.m0 + tok;
+        __nv_bfloat16* orow;
+        const __nv_bfloat16* rrow = nullptr;
+        bool vrow = true;
+        if constexpr (kFuse == 2) {
+          const int64_t v = static_cast<int64_t>(__ldg(la.fz.src + rr));
+          vrow = v >= 0 && v < la.vrows * la.npeer;
+          const int p = vrow ? static_cast<int>(v / la.vrows) : 0;
+          const int64_t i = vrow ? v - p * la.vrows : 0;
+          __nv_bfloat16* py = la.peer_y[0];
+          const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+          for (int jj = 1; jj < kMaxPeers; ++jj)
+            if (p == jj) {
+              py = la.peer_y[jj];
+              pr = la.peer_res[jj];
+            }
+          orow = py + i * H;
+          rrow = pr ? pr + i * H : nullptr;
+        } else {
+          int64_t oi = rr;
+          if constexpr (kFuse == 1) {
+            oi = la.fz.src ? static_cast<int64_t>(__ldg(la.fz.src + rr)) : rr;
+            vrow = oi >= 0 && oi < la.fz.rows;
+            if (!vrow) oi = 0;
+            rrow = la.fz.residual ? la.fz.residual + oi * H : nullptr;
+          }
+          orow = la.y + oi * H;
+        }
+        float val = __uint_as_float(r[j]);
+        if (ok && vrow) {
+          if (rrow) val += __bfloat162float(rrow[col]);
+          orow[col] = __float2bfloat16_rn(val);
+        }
+      }
+    }
+  }
+}
+
 template <int kFuse, int kMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                  const __grid_constant__ CUtensorMap tmD, LayerArgs la) {
+                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX16,
+                  const __grid_constant__ CUtensorMap tmH16, const __grid_constant__ CUtensorMap tmG16,
+                  const __grid_constant__ CUtensorMap tmU16, LayerArgs la) {
   extern __shared__ uint8_t smem_raw[];
   using SM = typename std::conditional<kMT == 256, Smem, SmemD>::type;
   constexpr int kS = kMT == 256 ? kStages : kStagesD;     // ring stages
@@ -490,6 +572,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     tc::prefetch_tmap(&tmU);
     tc::prefetch_tmap(&tmH);
     tc::prefetch_tmap(&tmD);
+    if (la.swap_rows > 0) {
+      tc::prefetch_tmap(&tmX16);
+      tc::prefetch_tmap(&tmH16);
+      tc::prefetch_tmap(&tmG16);
+      tc::prefetch_tmap(&tmU16);
+    }
   }
   if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
   __syncthreads();
@@ -530,7 +618,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
       int g1 = 0, g2 = 0;
-      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int nr = tl.n0 + 64 * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
@@ -552,16 +640,21 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     int g1 = 0, g2 = 0;
     const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
     for (int t = pair; t < ntiles; t += npairs) {
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
-      const int a_rows = tl.m256 ? 128 : 64;
+      // Activation rows this CTA stages per K step: 128 (M = 256), 64 (M = 128) or, for a swap-AB tile, half
+      // of its N = rows rounded up to 16 (in 16-row boxes)
+      const int nsw = tl.swap ? ((tl.rows + 15) & ~15) : 0;
+      const int a_rows = tl.swap ? nsw / 2 : (tl.m256 ? 128 : 64);
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
+      const int nact = (a_rows + 15) / 16;  // swap tiles: 16-row activation boxes
       // A tile of ≤ 64 rows: every row the second CTA would stage is past the tile's end, so it skips its A
       // load (its MMA rows read stale shared memory; row m of the product depends on A row m only and rows
       // past tl.rows are never stored). Knob ffn_askip = 0 loads them anyway (A/B).
-      const bool a_skip = la.askip && !tl.m256 && tl.rows <= 64;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128) -
-                             (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
+      const bool a_skip = la.askip && !tl.swap && !tl.m256 && tl.rows <= 64;
+      const uint32_t bytes = tl.swap ? 2u * static_cast<uint32_t>(nact * 16 * 128 + 128 * 128)
+                                     : 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128) -
+                                           (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
       if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
         // padding: their products are never stored, so they are not waited for)
@@ -612,6 +705,23 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
           const int k0 = kb * kBK;
           if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
+          if (tl.swap) {
+            // swap-AB tile: the activations are the MMA's B side (nsw/2 rows here, 16-row boxes); the weights
+            // its A side. Gate/up weight rows go in as 4 x [16 gate | the same 16 up] so each epilogue warp's
+            // 32 TMEM lanes hold both factors of its 16 neurons.
+            const CUtensorMap* mA16 = tl.mode == 0 ? &tmX16 : &tmH16;
+            for (int i = 0; i < nact; ++i) tc::tma_load_2d_2sm(mA16, s.a[stage] + i * 2048, fb, k0, a_row0 + 16 * i);
+            if (tl.mode == 0) {
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                tc::tma_load_3d_2sm(&tmG16, s.b[stage] + (32 * q4) * 128, fb, k0, nrg + 16 * q4, e);
+                tc::tma_load_3d_2sm(&tmU16, s.b[stage] + (32 * q4 + 16) * 128, fb, k0, nrg + 16 * q4, e);
+              }
+            } else {
+              tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
+              tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
+            }
+          } else {
           if (!(a_skip && cta == 1)) tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
           if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
           if (tl.mode == 0) {  // 64 rows of W_gate then the same rows of W_up
@@ -620,6 +730,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           } else {  // 128 rows of W_down in boxes of 64
             tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
             tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
+          }
           }
         }
         __syncwarp();
@@ -638,10 +749,13 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
-      int g1 = 0, g2 = 0, i = 0;
+      int g1 = 0, g2 = 0;
+      int i = 0;
       for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
-        const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
+        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
+        // swap-AB tile: M = 256 weight rows (128 per CTA, from the B slots), N = rows rounded up to 16 (from the
+        // A slots): operands exchanged, accumulator lane = weight row, column = the tile's row
+        const uint32_t idesc = tl.swap ? tc::idesc_bf16(256, (tl.rows + 15) & ~15) : (tl.m256 ? idesc256 : idesc128);
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
         tc::mbar_wait_cluster(&s.tempty[acc], (use & 1u) ^ 1u);
@@ -652,8 +766,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           tc::mbar_wait_cluster(&s.full[stage], phase);
           tc::fence_after();
           // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
-          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (kSA >> 4));
-          const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
+          const uint64_t sa = adesc0 + static_cast<uint64_t>(stage * (kSA >> 4));
+          const uint64_t sb = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
+          const uint64_t ad = tl.swap ? sb : sa, bd = tl.swap ? sa : sb;
           if (tc::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / kUK; ++kk)
@@ -675,9 +790,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
     uint8_t* stg = s.stg[q];
-    int g1 = 0, g2 = 0, i = 0;
+    int g1 = 0, g2 = 0;
+    int i = 0;
     for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, g1, g2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -700,7 +816,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       }
       const bool valid = row_in_tile < tl.rows && !aborted;
       const int64_t r = tl.m0 + row_in_tile;
-      if (tl.mode == 0) {
+      if (tl.swap) {
+        swap_epilogue<kFuse>(la, tl, tacc, cta, q, lane, !aborted);
+      } else if (tl.mode == 0) {
         // windows of 128 columns: [gate 64 | up 64] of h columns n0 + (window) * 64 + [0, 64)
         __nv_bfloat16* orow = la.h + r * d;
         for (int w = 0; w < ncols / 128; ++w) {
@@ -923,16 +1041,26 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   bool ok = tc::make_map_2d(&mX, xs, H, rows, kBK, 64) && tc::make_map_3d(&mG, wg, H, d, EW, kBK, 64) &&
             tc::make_map_3d(&mU, wu, H, d, EW, kBK, 64) && tc::make_map_2d(&mH, h, d, rows, kBK, 64) &&
             tc::make_map_3d(&mD, wd, d, H, EW, kBK, 64);
+  // 128-row m-tiles with the 8-stage ring for decode-sized launches (weight streaming: more bytes in flight,
+  // no B reuse to lose); knob ffn_mt = 128 | 256 overrides (A/B measurement)
+  int mt = rows <= kDecodeRows ? 128 : 256;
+  if (const int v = knob(Knob::kFfnMt)) mt = v == 128 ? 128 : 256;
+  // Segment tails of <= swap_rows rows run as swap-AB tiles (16-row boxes for their activation rows and for the
+  // [16 gate | 16 up] weight interleave). Default: tails of <= 64 rows of 256-row m-tile launches (A/B,
+  // scripts/ffn_lab.py: +2.5 % at 4096 rows, +0.2..0.8 % at 8192-16384); none at decode sizes (-4 % at
+  // 256-1024 rows: the tiles there are weight-bandwidth bound either way). Knob ffn_swap = n >= 0 forces it.
+  const int kswap = knob(Knob::kFfnSwap);
+  const int swap_rows = (kswap < 0 ? (mt == 256 ? 64 : 0) : std::min(64, kswap)) & ~15;
+  CUtensorMap mX16 = mX, mH16 = mH, mG16 = mG, mU16 = mU;
+  if (ok && swap_rows > 0)
+    ok = tc::make_map_2d(&mX16, xs, H, rows, kBK, 16) && tc::make_map_2d(&mH16, h, d, rows, kBK, 16) &&
+         tc::make_map_3d(&mG16, wg, H, d, EW, kBK, 16) && tc::make_map_3d(&mU16, wu, H, d, EW, kBK, 16);
   if (!ok) {
     set_error("cuTensorMapEncodeTiled failed (driver entry point missing or bad shape/alignment)");
     return README_ERR_CUDA;
   }
   // with pdl the caller zeroed `ready` before the dispatch (a memset here would sit between the two kernels)
   if (!pdl) README_CUDA(cudaMemsetAsync(ready, 0, ffn_layer_ready_bytes(rows, nseg), st));
-  // 128-row m-tiles with the 8-stage ring for decode-sized launches (weight streaming: more bytes in flight,
-  // no B reuse to lose); knob ffn_mt = 128 | 256 overrides (A/B measurement)
-  int mt = rows <= kDecodeRows ? 128 : 256;
-  if (const int v = knob(Knob::kFfnMt)) mt = v == 128 ? 128 : 256;
   const int64_t mt_ub = nseg + (rows + mt - 1) / mt;
   // Persistent grid: never more pairs than can be co-resident (down tiles wait on other pairs' gate/up
   // tiles); knob ffn_pairs = n caps it further (measurement of placement-limited grids)
@@ -964,6 +1092,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   la.trace = g_trace_buf;
   la.askip = knob(Knob::kFfnAskip) != 0;
   la.order = knob(Knob::kFfnOrder);
+  la.swap_rows = swap_rows;
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {
@@ -988,7 +1117,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
 #define README_LAYER_LAUNCH(F, MT) \
-  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, MT>, mX, mG, mU, mH, mD, la))
+  README_CUDA(cudaLaunchKernelEx(&cfg, ffn_layer2_kernel<F, MT>, mX, mG, mU, mH, mD, mX16, mH16, mG16, mU16, la))
   if (mt == 128) {
     if (fuse == 2) README_LAYER_LAUNCH(2, 128);
     else if (fuse == 1) README_LAYER_LAUNCH(1, 128);

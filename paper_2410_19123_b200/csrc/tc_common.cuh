@@ -50,14 +50,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-// Wait with cluster-scope acquire (arrivals come from the peer CTA).
+// Wait on a barrier that the peer CTA of the pair also arrives on (TMA complete_tx of both CTAs, multicast
+// tcgen05.commit, remote epilogue arrivals). CTA-scope acquire is enough: what these barriers order is
+// async-proxy data (TMA into shared memory, TMEM through tcgen05 fences), not generic loads of the peer's
+// memory. A cluster-scope acquire made ptxas emit an L1 invalidate (CCTL.IVALL) after every successful
+// wait — 46 % of the MMA warp's stall samples in the v1 capture of this round (profiles/SUMMARY.md).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(a), "r"(parity)

@@ -1,6 +1,7 @@
-"""Expert FFN alone (readme_expert_ffn, one ffn_layer2 launch) at several batch sizes under env variants
-(e.g. README_FFN_MT=128|256), CUDA-graph replays, L2 flushed before each. Measurement only.
-Usage: python scripts/ffn_lab.py VAR=a,b [T1 T2 ...]"""
+"""Expert FFN alone (readme_expert_ffn, one ffn_layer2 launch) at several batch sizes under library knob
+variants (readme_debug_set_knob; e.g. ffn_swap=0,64 or ffn_mt=128,256), CUDA-graph replays, L2 flushed
+before each, variants alternated round by round on the same box. Measurement only.
+Usage: python scripts/ffn_lab.py KNOB=a,b [T1 T2 ...]"""
 import json
 import os
 import sys
@@ -12,7 +13,7 @@ import synth  # noqa: E402
 from paper_2410_19123_b200 import readme as rd  # noqa: E402
 
 var, vals = sys.argv[1].split("=")
-vals = vals.split(",")
+vals = [int(v) for v in vals.split(",")]
 Ts = [int(t) for t in sys.argv[2:]] or [256, 512, 1024, 2048, 4096, 8192]
 H, E, d = 4096, 8, 5504
 g = torch.Generator(device="cuda").manual_seed(1)
@@ -23,29 +24,35 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 res = {}
 for T in Ts:
     x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
-    plan = rd.route(torch.from_numpy(synth.router_logits(T, E, seed=T)).cuda(), 1)
+    # the bench's routing logits at T = 8192 (config 2 counts), else seeded by T
+    seed = synth.MASTER_SEED + 2 if T == 8192 else T
+    plan = rd.route(torch.from_numpy(synth.router_logits(T, E, seed=seed)).cuda(), 1)
     xs = rd.dispatch(x, plan.dest, 1)
     ys = torch.empty_like(xs)
     ws = torch.empty(rd.expert_ffn_workspace_bytes(T, H, E, d, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    graphs = {}
     for v in vals:
-        os.environ[var] = v
+        rd.set_knob(var, v)
         fn = lambda: rd.expert_ffn(xs, plan.offsets, wg, wu, wd, out=ys, ws=ws)
         fn()
         torch.cuda.synchronize()
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
             fn()
-        ms = []
-        for _ in range(12):
+        graphs[v] = gr
+    rd.reset_knob(var)
+    ms = {v: [] for v in vals}
+    for _ in range(15):
+        for v in vals:
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            gr.replay()
+            graphs[v].replay()
             b.record()
             torch.cuda.synchronize()
-            ms.append(a.elapsed_time(b))
-        ms.sort()
-        t = sum(ms[2:-2]) / len(ms[2:-2])
+            ms[v].append(a.elapsed_time(b))
+    for v in vals:
+        m = sorted(ms[v])[3:-3]
+        t = sum(m) / len(m)
         res.setdefault(T, {})[v] = {"us": round(t * 1e3, 1), "TFLOPs": round(6 * T * H * d / (t * 1e-3) / 1e12, 1)}
-    os.environ.pop(var, None)
-print(json.dumps({"var": var, "results": res}))
+print(json.dumps({"knob": var, "counts_T8192": plan.counts.tolist() if Ts[-1] == 8192 else None, "results": res}))

@@ -251,14 +251,18 @@ FFN_KERNEL = {"merged": 0, "split": 1, "unfused": 2}
 
 
 def _set_kernel(knob, kernel):
-    """merged (single launch, 256-row m-tiles above 1024 rows) / merged-mt128 / split (two launches)."""
+    """merged (single launch, 256-row m-tiles above 1024 rows) / merged-mt128 / merged-swap (segment tails of
+    <= 64 rows as swap-AB tiles) / merged-noswap / split (two launches)."""
     if kernel == "merged-mt128":
         knob("ffn_mt", 128)
-        kernel = "merged"
-    knob("ffn_kernel", FFN_KERNEL[kernel])
+    elif kernel == "merged-swap":
+        knob("ffn_swap", 64)
+    elif kernel == "merged-noswap":
+        knob("ffn_swap", 0)
+    knob("ffn_kernel", FFN_KERNEL["split" if kernel == "split" else "merged"])
 
 
-KERNELS = ["merged", "merged-mt128", "split"]
+KERNELS = ["merged", "merged-mt128", "merged-swap", "merged-noswap", "split"]
 
 
 @pytest.mark.parametrize("T,H,d,E,k,skew", [
@@ -329,22 +333,26 @@ def test_expert_ffn_tile_edges(rd, knob, kernel):
 
 
 # variants of the single-launch FFN that compute every output element from the same K-ordered MMAs:
-# (m-tile rows, second CTA skips A loads of <= 64-row tiles, max CTA pairs, gate/up N-tile-fastest order)
-FFN_VARIANTS = [(256, 1, 0, 0), (128, 1, 0, 0), (128, 0, 0, 0), (256, 0, 0, 0), (256, 1, 3, 0), (128, 1, 1, 0),
-                (256, 1, 0, 1), (128, 1, 0, 1)]
+# (m-tile rows, second CTA skips A loads of <= 64-row tiles, max CTA pairs, gate/up N-tile-fastest order,
+# segment tails of <= n rows as swap-AB tiles)
+FFN_VARIANTS = [(256, 1, 0, 0, 0), (128, 1, 0, 0, 0), (128, 0, 0, 0, 0), (256, 0, 0, 0, 0), (256, 1, 3, 0, 0),
+                (128, 1, 1, 0, 0), (256, 1, 0, 1, 0), (128, 1, 0, 1, 0), (256, 1, 0, 0, 64), (128, 1, 0, 0, 64),
+                (256, 1, 0, 0, 32), (256, 1, 3, 0, 64), (128, 1, 1, 0, 48), (256, 0, 0, 1, 16)]
 
 
 @pytest.mark.parametrize("T,d,skew", [(256, 5504, "zipf"), (2000, 264, None), (40, 136, "empty")])
 def test_ffn_variants_bitwise_equal(rd, knob, T, d, skew):
     """128-row vs 256-row m-tiles, with and without the A-load skip, on 3 and 1 CTA pairs (every pair walks
-    a long tile list; the down tiles wait on gate/up tiles of the same few pairs) and in N-tile-fastest
-    order: bitwise equal results, with and without the fused residual scatter."""
+    a long tile list; the down tiles wait on gate/up tiles of the same few pairs), in N-tile-fastest order,
+    and with segment tails as swap-AB tiles (operands exchanged: weights on the MMA's M side): bitwise equal
+    results, with and without the fused residual scatter."""
     H, E = 4096 if d == 5504 else 256, 8
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "bf16", seed=T + d, skew=skew)
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    for mt, askip, pairs, order in FFN_VARIANTS:
+    for mt, askip, pairs, order, swap in FFN_VARIANTS:
+        knob("ffn_swap", swap)
         knob("ffn_mt", mt)
         knob("ffn_askip", askip)
         knob("ffn_pairs", pairs)

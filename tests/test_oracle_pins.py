@@ -457,3 +457,72 @@ def test_router_zero_head_gives_zero_logits():
     W["w_head"] = torch.zeros_like(W["w_head"])
     out = router.forward(synth.token_ids(12, vocab=300, seed=164), np.array([0, 12]), W)
     assert np.all(out == 0.0)
+
+
+# ---- closed forms for the router block (Q15) and the pre-norm stack (Q10) ---------------------------------
+# tests/golden/router_and_stack_closed_forms.json holds the hand derivations; the recipes below build the
+# weights those derivations describe (eps = 0 so every RMSNorm of a one-hot row is sqrt(512) times it).
+
+def _zero_router(vocab, n_heads_out):
+    D = 512
+    z = lambda *s: np.zeros(s, np.float64)
+    return {"emb": np.eye(vocab, D), "norm1": np.ones(D), "w_qkv": z(3 * D, D), "w_o": z(D, D),
+            "norm2": np.ones(D), "w_gate": z(D, D), "w_up": z(D, D), "w_down": z(D, D), "norm_f": np.ones(D),
+            "w_head": z(n_heads_out, D)}
+
+
+def _attention_case():
+    r = math.sqrt(512.0)
+    W = _zero_router(2, 3)
+    a = math.sqrt(math.sqrt(128.0) * math.log(3.0)) / r
+    W["w_qkv"][0, 1] = a            # W_q, head 0 dim 0 <- model dim 1 (token 1 only)
+    W["w_qkv"][512 + 0, 1] = a      # W_k, head 0 dim 0 <- model dim 1 (k_0 = 0)
+    W["w_qkv"][1024 + 0, 1] = 1.0 / r  # W_v, head 0 dim 0: v_1 = 1, v_0 = 0
+    W["w_o"][2, 0] = 1.0            # attention head-0 dim 0 -> model dim 2
+    W["w_head"][0, 2] = W["w_head"][1, 1] = W["w_head"][2, 0] = 1.0
+    return W
+
+
+def _mlp_case():
+    r = math.sqrt(512.0)
+    W = _zero_router(1, 2)
+    W["w_gate"][0, 0] = 2.0 / r
+    W["w_up"][0, 0] = 3.0 / r
+    W["w_down"][3, 0] = 1.0
+    W["norm_f"][:] = 2.0
+    W["w_head"][0, 3] = W["w_head"][1, 0] = 1.0
+    return W
+
+
+@pytest.mark.parametrize("evaluate", ["forward", "forward_incremental"])
+def test_router_attention_closed_form(evaluate):
+    """Q15 attention pinned by hand: the 1/sqrt(128) score scale (weights (1/4, 3/4) from scores (0, ln 3)),
+    the causal mask (token 0 sees only itself), RoPE's position invariance of q.k at equal positions, the
+    residual around attention and the final RMSNorm + head. Dropping the scale gives r(0.7071, 0.7071, 0)."""
+    from oracle import router
+    g = _gold("router_and_stack_closed_forms.json")["attention"]
+    out = getattr(router, evaluate)(np.array(g["ids"]), np.array([0, 2]), _attention_case(), eps=0.0)
+    np.testing.assert_allclose(out, np.array(g["logits"]), atol=g["tol_abs"], rtol=0)
+
+
+@pytest.mark.parametrize("evaluate", ["forward", "forward_incremental"])
+def test_router_mlp_head_closed_form(evaluate):
+    """Q15 MLP and gating head pinned by hand: silu(W_g m) * (W_u m) (P7(i)'s silu(2)*3), W_down, the residual
+    around the MLP, the final RMSNorm with its weight g_f = 2, and W_head's rows. ReLU for silu, gate and up
+    exchanged, or g_f dropped each move the logits by far more than the tolerance."""
+    from oracle import router
+    g = _gold("router_and_stack_closed_forms.json")["mlp_head"]
+    out = getattr(router, evaluate)(np.array(g["ids"]), np.array([0, 1]), _mlp_case(), eps=0.0)
+    np.testing.assert_allclose(out, np.array(g["logits"]), atol=g["tol_abs"], rtol=0)
+
+
+def test_moe_stack_prenorm_closed_form():
+    """Q10 pinned by hand: one pre-norm layer on P7(ii)'s identity expert maps x = (3, 5) to
+    x + F(x / sqrt(17)) = (3.356972, 6.133489); without the RMSNorm it would be (11.573167, 29.832679),
+    without the residual (0.356972, 1.133489)."""
+    g = _gold("router_and_stack_closed_forms.json")["prenorm_stack"]
+    I = np.eye(2)
+    wg, wu, wd = oracle.build_experts(I, I, I, np.array([[0, 1]], np.int32))
+    y, plan = oracle.moe_stack(np.array([g["x"]]), np.zeros((1, 1), np.float32), 1, [(wg, wu, wd)], eps=0.0)
+    np.testing.assert_allclose(y[0], g["y"], atol=g["tol_abs"], rtol=0)
+    assert plan["counts"].tolist() == [1]
