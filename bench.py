@@ -148,7 +148,7 @@ def cpu_baseline(cfg, inp, budget_s=15.0):
     lg = inp["logits"]
     idx = lg.argmax(axis=1)
     dense = [t.cpu() for t in inp["dense"]]
-    eg, eu, ed = (t.cpu() for t in inp["w"])
+    eg, eu, ed = oracle.build_experts(*dense, inp["S"])  # the oracle slices its own experts (never the GPU's)
     g = synth.rng(7, 7)
     threads = oracle.default_threads()
 

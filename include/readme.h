@@ -306,7 +306,9 @@ void readme_cache_stats(readme_expert_cache* c, int64_t* hits, int64_t* misses);
 readme_status readme_ep_alloc(size_t bytes, void** ptr); /* zero-filled device memory on the current device */
 readme_status readme_ep_free(void* ptr);
 readme_status readme_ipc_handle(const void* ptr, void* handle); /* handle: README_IPC_HANDLE_BYTES host bytes */
-readme_status readme_ipc_open(const void* handle, void** ptr);  /* a handle from another process */
+/* readme_ipc_open maps a handle from another process; a buffer on another GPU that this one cannot reach by
+ * peer access (cudaDeviceCanAccessPeer) is refused with README_ERR_UNSUPPORTED (nothing stays mapped). */
+readme_status readme_ipc_open(const void* handle, void** ptr);
 readme_status readme_ipc_close(void* ptr);
 /* Phase flags: peer_flags[q] -> rank q's uint64 [G] flag array for this phase; epoch -> this rank's uint64
  * counter for the phase (device memory, zero-initialised, private to the rank). readme_ep_signal bumps

@@ -694,6 +694,27 @@ readme_status readme_ipc_open(const void* handle, void** ptr) {
   memcpy(&h, handle, sizeof(h));
   *ptr = nullptr;
   README_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  // The kernels load and store through this mapping directly: a buffer on another GPU must be reachable over
+  // NVLink / PCIe peer access from this one, else the mapping is refused (the caller falls back to NCCL).
+  int cur = -1;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e == cudaSuccess) e = cudaPointerGetAttributes(&at, *ptr);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(*ptr);
+    *ptr = nullptr;
+    return cuda_fail(e, "cudaPointerGetAttributes(ipc mapping)");
+  }
+  if (at.device != cur) {
+    int ok = 0;
+    e = cudaDeviceCanAccessPeer(&ok, cur, at.device);
+    if (e != cudaSuccess || !ok) {
+      cudaIpcCloseMemHandle(*ptr);
+      *ptr = nullptr;
+      set_error("device %d cannot access peer device %d (no P2P path): use the NCCL exchange", cur, at.device);
+      return README_ERR_UNSUPPORTED;
+    }
+  }
   return README_OK;
 }
 

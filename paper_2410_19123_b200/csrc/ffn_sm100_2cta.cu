@@ -39,8 +39,7 @@ constexpr int kPrefetchK = 32;      // K stages of the first weight tile warmed 
 constexpr int kXokWords = 64;       // m-tiles whose x readiness is cached in shared memory (2048)
 
 // Decode-sized launches use 128-row m-tiles only (M = 128 pair MMAs, 64 A rows per CTA): the A slot halves,
-// so the same ~192 KB ring holds 8 stages instead of 6 — a third more weight bytes in flight per SM.
-constexpr int kStagesD = 8;
+// so the ring holds more stages (more weight bytes in flight per SM).
 constexpr int kStageAD = 64 * 128;
 constexpr int64_t kDecodeRows = 1024;  // launches up to this many rows use the 128-row m-tile variant
 
@@ -56,15 +55,10 @@ struct __align__(8) SmemT {
   alignas(16) uint8_t stg[4][32 * 128];  // epilogue staging, one 4 KB tile per epilogue warp
   int seg_off[kMaxSeg + 1];
   int tile_start[kMaxSeg + 1];
-  int tile_start2[kMaxSeg + 1];  // merged a6+a7 kernel: the down tiles' prefix
-  int mt_start[kMaxSeg + 1];     // merged kernel: first m-tile id of each segment (readiness counters)
-  uint32_t xok[kXokWords];       // merged kernel, pdl == 2: bit per m-tile, this CTA's A rows seen ready
 };
 using Smem = SmemT<kStages, kStageA>;
-using SmemD = SmemT<kStagesD, kStageAD>;
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
-constexpr size_t kSmemBytesD = sizeof(SmemD) + 1024;
-static_assert(kSmemBytesD <= 232448 && kSmemBytes <= 232448, "shared memory");
+static_assert(kSmemBytes <= 232448, "shared memory");
 
 struct Tile {
   int g, m0, rows, n0;
@@ -404,7 +398,7 @@ struct LayerArgs {
 };
 
 struct LTile {
-  int mode, g, mt, m0, rows, n0;
+  int mode, g, mt, mid, m0, rows, n0;  // mid = global m-tile id (readiness counter index)
   bool m256;  // M = 256 pair MMA (each CTA 128 A rows), else M = 128 (64 rows per CTA)
   bool swap;  // swap-AB tail tile: weights are the MMA's M side, the tile's rows its N side
 };
@@ -419,37 +413,47 @@ constexpr int kBN2 = 256;  // output columns per down tile (128 W_down rows per 
 // for a longest-first schedule re-read their weights from DRAM and measured 9 % slower at config 2).
 // Down tiles come after every gate/up tile, so every wait is on a tile earlier in the global order
 // (deadlock-free whenever the grid is co-resident).
-template <int kMT, class SM>
-__device__ __forceinline__ LTile decode_ltile(const SM& s, int t, int nseg, int T1, int NT1, int NT2, int swap_rows,
-                                             int& gcur1, int& gcur2, bool nfast = false) {
+// A role's tiles only move forward, so a cursor walks the segments (offsets read through the read-only
+// cache; no per-segment tables in shared memory, which holds one more ring stage instead).
+struct Cursor {
+  int phase = -1, g = 0, start = 0, mbase = 0;  // segment g's first tile index in its phase; its first m-tile id
+};
+
+template <int kMT>
+__device__ __forceinline__ LTile decode_ltile(const int32_t* __restrict__ offs, int t, int nseg, int T1, int NT1,
+                                             int NT2, int swap_rows, Cursor& c, bool nfast = false) {
   LTile tl;
-  int local, g, NT;
-  if (t < T1) {
-    while (gcur1 + 1 < nseg && s.tile_start[gcur1 + 1] <= t) ++gcur1;
-    g = gcur1;
-    local = t - s.tile_start[g];
-    tl.mode = 0;
-    NT = NT1;
-  } else {
-    const int t2 = t - T1;
-    while (gcur2 + 1 < nseg && s.tile_start2[gcur2 + 1] <= t2) ++gcur2;
-    g = gcur2;
-    local = t2 - s.tile_start2[g];
-    tl.mode = 1;
-    NT = NT2;
+  const int phase = t < T1 ? 0 : 1;
+  const int NT = phase ? NT2 : NT1;
+  if (c.phase != phase) {
+    c.phase = phase;
+    c.g = 0;
+    c.start = phase ? T1 : 0;
+    c.mbase = 0;
   }
-  const int cnt = s.seg_off[g + 1] - s.seg_off[g];
-  const int mt_g = (cnt + kMT - 1) / kMT;
+  int lo = __ldg(offs + c.g), hi = __ldg(offs + c.g + 1);
+  int mt_g = (hi - lo + kMT - 1) / kMT;
+  while (t >= c.start + mt_g * NT && c.g + 1 < nseg) {
+    c.start += mt_g * NT;
+    c.mbase += mt_g;
+    ++c.g;
+    lo = hi;
+    hi = __ldg(offs + c.g + 1);
+    mt_g = (hi - lo + kMT - 1) / kMT;
+  }
+  const int local = t - c.start;
   // m-tile fastest (default) or, for gate/up tiles with nfast (lab knob ffn_order = 1), N-tile fastest
-  const bool nf = nfast && tl.mode == 0;
+  const bool nf = nfast && phase == 0;
   const int nt = nf ? local % NT : local / mt_g, mt = nf ? local / NT : local % mt_g;
-  tl.g = g;
+  tl.mode = phase;
+  tl.g = c.g;
   tl.mt = mt;
-  tl.m0 = s.seg_off[g] + mt * kMT;
-  tl.rows = min(kMT, cnt - mt * kMT);
+  tl.mid = c.mbase + mt;
+  tl.m0 = lo + mt * kMT;
+  tl.rows = min(kMT, hi - lo - mt * kMT);
   tl.m256 = tl.rows > 128;
   tl.swap = tl.rows <= swap_rows;  // only a segment's last m-tile can be that short
-  tl.n0 = nt * (tl.mode == 0 ? kBN1 : kBN2);
+  tl.n0 = nt * (phase == 0 ? kBN1 : kBN2);
   return tl;
 }
 
@@ -541,6 +545,45 @@ __device__ __forceinline__ void swap_epilogue(const LayerArgs& la, const LTile& 
   }
 }
 
+// Shared memory of the single-launch kernel: only the TMA ring, its barriers and the x-readiness cache (the
+// per-segment tables live in the cursor walk, the epilogue stores straight from registers), so the ring holds
+// 7 stages of 32 KB per CTA (256-row m-tiles) or 9 of 24 KB (128-row m-tiles): the v2 profile of this round
+// showed the MMA warp waiting on TMA data ~40 % of its time with 6 stages (profiles/SUMMARY.md).
+template <int S, int SA>
+struct __align__(8) SmemLT {
+  uint8_t a[S][SA];
+  uint8_t b[S][kStageB];
+  uint64_t full[S];
+  uint64_t empty[S];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  uint32_t xok[kXokWords];  // pdl == 2: bit per m-tile, this CTA's A rows seen ready
+};
+constexpr int kStagesL = 7;
+constexpr int kStagesLD = 9;
+using SmemL = SmemLT<kStagesL, kStageA>;
+using SmemLD = SmemLT<kStagesLD, kStageAD>;
+constexpr size_t kSmemBytesL = sizeof(SmemL) + 1024;
+constexpr size_t kSmemBytesLD = sizeof(SmemLD) + 1024;
+static_assert(kSmemBytesL <= 232448 && kSmemBytesLD <= 232448, "single-launch kernel shared memory");
+
+// 32 fp32 values of one row -> 32 bf16 (RNE) at dst, 16 B at a time, columns at or past ncols skipped
+// (ncols is a multiple of 8). Each thread writes whole 32-byte sectors of its own row.
+__device__ __forceinline__ void store_row_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int ncols) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (8 * j < ncols) {
+      uint4 w;
+      w.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
+      w.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
+      w.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
+      w.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
+      st_v4(reinterpret_cast<uint4*>(dst) + j, w);
+    }
+  }
+}
+
 template <int kFuse, int kMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
@@ -549,9 +592,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                   const __grid_constant__ CUtensorMap tmH16, const __grid_constant__ CUtensorMap tmG16,
                   const __grid_constant__ CUtensorMap tmU16, LayerArgs la) {
   extern __shared__ uint8_t smem_raw[];
-  using SM = typename std::conditional<kMT == 256, Smem, SmemD>::type;
-  constexpr int kS = kMT == 256 ? kStages : kStagesD;     // ring stages
-  constexpr int kSA = kMT == 256 ? kStageA : kStageAD;    // A bytes per stage per CTA
+  using SM = typename std::conditional<kMT == 256, SmemL, SmemLD>::type;
+  constexpr int kS = kMT == 256 ? kStagesL : kStagesLD;  // ring stages
+  constexpr int kSA = kMT == 256 ? kStageA : kStageAD;   // A bytes per stage per CTA
   static_assert(kMT == 256 || kMT == 128, "kMT");
   SM& s = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
@@ -559,12 +602,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const bool leader = cta == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int H = la.H, d = la.d, E = la.E, nseg = la.nseg;
+  const int32_t* __restrict__ offs = la.offsets;
   constexpr int kN = 256;  // MMA N (both CTAs' 128-row B halves)
   const int NT1 = (d + kBN1 - 1) / kBN1, NT2 = (H + kBN2 - 1) / kBN2;
   const int KB1 = (H + kBK - 1) / kBK, KB2 = (d + kBK - 1) / kBK;
   const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
 
-  for (int i = tid; i <= nseg; i += kThreads) s.seg_off[i] = la.offsets[i];
   for (int i = tid; i < kXokWords; i += kThreads) s.xok[i] = 0u;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmX);
@@ -580,21 +623,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     }
   }
   if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
-  __syncthreads();
+  // total m-tiles (every thread: nseg reads of the read-only offsets, no shared table)
+  int mtiles = 0;
+  for (int g = 0; g < nseg; ++g) mtiles += (__ldg(offs + g + 1) - __ldg(offs + g) + kMT - 1) / kMT;
   if (tid == 0) {
-    int a1 = 0, a2 = 0, am = 0;
-    for (int g = 0; g < nseg; ++g) {
-      const int mt_g = (s.seg_off[g + 1] - s.seg_off[g] + kMT - 1) / kMT;
-      s.tile_start[g] = a1;
-      s.tile_start2[g] = a2;
-      s.mt_start[g] = am;
-      a1 += mt_g * NT1;
-      a2 += mt_g * NT2;
-      am += mt_g;
-    }
-    s.tile_start[nseg] = a1;
-    s.tile_start2[nseg] = a2;
-    s.mt_start[nseg] = am;
     for (int i = 0; i < kS; ++i) {
       tc::mbar_init(&s.full[i], 1);
       tc::mbar_init(&s.empty[i], 1);
@@ -609,16 +641,16 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   __syncthreads();
   tc::cluster_sync();
   tc::fence_after();
-  const int T1 = s.tile_start[nseg];
-  const int ntiles = T1 + s.tile_start2[nseg];
+  const int T1 = mtiles * NT1;
+  const int ntiles = T1 + mtiles * NT2;
   const uint32_t tmem_base = s.tmem_base;
   // Launched with PDL behind the dispatch (la.pdl): everything above only read the routing offsets, which
   // the route kernel wrote before the dispatch began. Before waiting for the dispatch's x_sorted, start
   // pulling this pair's first gate/up weight tile into L2 — weights do not depend on the dispatch.
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
-      int g1 = 0, g2 = 0;
-      const LTile tl = decode_ltile<kMT>(s, pair, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
+      Cursor c;
+      const LTile tl = decode_ltile<kMT>(offs, pair, nseg, T1, NT1, NT2, la.swap_rows, c, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int nr = tl.n0 + 64 * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
@@ -634,13 +666,14 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion counted on the leader's barrier). The whole warp walks the
-    // loop so coordinates and addresses stay in uniform registers; one elected lane issues. =====
+    // loop so coordinates and addresses stay in uniform registers; one elected lane issues. Each tile kind
+    // gets its own K loop (no per-stage branching on the tile's shape). =====
     int stage = 0;
     uint32_t phase = 0;
-    int g1 = 0, g2 = 0;
+    Cursor cur;
     const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
     for (int t = pair; t < ntiles; t += npairs) {
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       // Activation rows this CTA stages per K step: 128 (M = 256), 64 (M = 128) or, for a swap-AB tile, half
       // of its N = rows rounded up to 16 (in 16-row boxes)
@@ -658,7 +691,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
         // padding: their products are never stored, so they are not waited for)
-        const int mid = s.mt_start[tl.g] + tl.mt;
+        const int mid = tl.mid;
         const bool cached = mid < kXokWords * 32 && (s.xok[mid >> 5] >> (mid & 31) & 1u);
         if (!cached) {
           const int lo = a_row0, hi = min(a_row0 + a_rows, tl.m0 + tl.rows);
@@ -684,7 +717,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       }
       if (tl.mode == 1) {
         // wait until every gate/up tile of this m-tile has published its h rows
-        const uint32_t* rp = la.ready + s.mt_start[tl.g] + tl.mt;
+        const uint32_t* rp = la.ready + tl.mid;
         uint32_t spins = 0;
         while (ld_acquire_u32(rp) < ready_target) {
           __nanosleep(128);
@@ -696,47 +729,60 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
       }
-      const int KB = tl.mode == 0 ? KB1 : KB2;
-      const CUtensorMap* mA = tl.mode == 0 ? &tmX : &tmH;
       const int nrg = tl.n0 + 64 * static_cast<int>(cta), nrd = tl.n0 + 128 * static_cast<int>(cta);
-      for (int kb = 0; kb < KB; ++kb) {
-        tc::mbar_wait(&s.empty[stage], phase ^ 1);
-        if (tc::elect_one()) {
-          const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
-          const int k0 = kb * kBK;
-          if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
-          if (tl.swap) {
-            // swap-AB tile: the activations are the MMA's B side (nsw/2 rows here, 16-row boxes); the weights
-            // its A side. Gate/up weight rows go in as 4 x [16 gate | the same 16 up] so each epilogue warp's
-            // 32 TMEM lanes hold both factors of its 16 neurons.
-            const CUtensorMap* mA16 = tl.mode == 0 ? &tmX16 : &tmH16;
-            for (int i = 0; i < nact; ++i) tc::tma_load_2d_2sm(mA16, s.a[stage] + i * 2048, fb, k0, a_row0 + 16 * i);
-            if (tl.mode == 0) {
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                tc::tma_load_3d_2sm(&tmG16, s.b[stage] + (32 * q4) * 128, fb, k0, nrg + 16 * q4, e);
-                tc::tma_load_3d_2sm(&tmU16, s.b[stage] + (32 * q4 + 16) * 128, fb, k0, nrg + 16 * q4, e);
-              }
-            } else {
-              tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
-              tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
-            }
-          } else {
-          if (!(a_skip && cta == 1)) tc::tma_load_2d_2sm(mA, s.a[stage], fb, k0, a_row0);
-          if (tl.m256) tc::tma_load_2d_2sm(mA, s.a[stage] + 64 * 128, fb, k0, a_row0 + 64);
-          if (tl.mode == 0) {  // 64 rows of W_gate then the same rows of W_up
-            tc::tma_load_3d_2sm(&tmG, s.b[stage], fb, k0, nrg, e);
-            tc::tma_load_3d_2sm(&tmU, s.b[stage] + 64 * 128, fb, k0, nrg, e);
-          } else {  // 128 rows of W_down in boxes of 64
-            tc::tma_load_3d_2sm(&tmD, s.b[stage], fb, k0, nrd, e);
-            tc::tma_load_3d_2sm(&tmD, s.b[stage] + 64 * 128, fb, k0, nrd + 64, e);
+      // one ring step per K block: wait for the slot, arm the leader's barrier, issue this tile kind's loads
+      auto kloop = [&](int KB, auto&& issue) {
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait(&s.empty[stage], phase ^ 1);
+          if (tc::elect_one()) {
+            const uint32_t fb = full0 + static_cast<uint32_t>(stage * 8);
+            if (leader) tc::mbar_expect_tx(&s.full[stage], bytes);
+            issue(s.a[stage], s.b[stage], fb, kb * kBK);
           }
+          __syncwarp();
+          if (++stage == kS) {
+            stage = 0;
+            phase ^= 1;
           }
         }
-        __syncwarp();
-        if (++stage == kS) {
-          stage = 0;
-          phase ^= 1;
+      };
+      if (tl.swap) {
+        // swap-AB tile: the activations are the MMA's B side (nsw/2 rows here, 16-row boxes); the weights its
+        // A side. Gate/up weight rows go in as 4 x [16 gate | the same 16 up] so each epilogue warp's 32 TMEM
+        // lanes hold both factors of its 16 neurons.
+        const CUtensorMap* mA16 = tl.mode == 0 ? &tmX16 : &tmH16;
+        if (tl.mode == 0) {
+          kloop(KB1, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            for (int i = 0; i < nact; ++i) tc::tma_load_2d_2sm(mA16, sa + i * 2048, fb, k0, a_row0 + 16 * i);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              tc::tma_load_3d_2sm(&tmG16, sb + (32 * q4) * 128, fb, k0, nrg + 16 * q4, e);
+              tc::tma_load_3d_2sm(&tmU16, sb + (32 * q4 + 16) * 128, fb, k0, nrg + 16 * q4, e);
+            }
+          });
+        } else {
+          kloop(KB2, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            for (int i = 0; i < nact; ++i) tc::tma_load_2d_2sm(mA16, sa + i * 2048, fb, k0, a_row0 + 16 * i);
+            tc::tma_load_3d_2sm(&tmD, sb, fb, k0, nrd, e);
+            tc::tma_load_3d_2sm(&tmD, sb + 64 * 128, fb, k0, nrd + 64, e);
+          });
+        }
+      } else {
+        const bool loadA = !(a_skip && cta == 1), A2 = tl.m256;
+        if (tl.mode == 0) {  // 64 rows of W_gate then the same rows of W_up
+          kloop(KB1, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            if (loadA) tc::tma_load_2d_2sm(&tmX, sa, fb, k0, a_row0);
+            if (A2) tc::tma_load_2d_2sm(&tmX, sa + 64 * 128, fb, k0, a_row0 + 64);
+            tc::tma_load_3d_2sm(&tmG, sb, fb, k0, nrg, e);
+            tc::tma_load_3d_2sm(&tmU, sb + 64 * 128, fb, k0, nrg, e);
+          });
+        } else {  // 128 rows of W_down in boxes of 64
+          kloop(KB2, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            if (loadA) tc::tma_load_2d_2sm(&tmH, sa, fb, k0, a_row0);
+            if (A2) tc::tma_load_2d_2sm(&tmH, sa + 64 * 128, fb, k0, a_row0 + 64);
+            tc::tma_load_3d_2sm(&tmD, sb, fb, k0, nrd, e);
+            tc::tma_load_3d_2sm(&tmD, sb + 64 * 128, fb, k0, nrd + 64, e);
+          });
         }
       }
     }
@@ -749,10 +795,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint64_t adesc0 = tc::sdesc_sw128(tc::smem_u32(s.a[0])), bdesc0 = tc::sdesc_sw128(tc::smem_u32(s.b[0]));
       int stage = 0;
       uint32_t phase = 0;
-      int g1 = 0, g2 = 0;
+      Cursor cur;
       int i = 0;
       for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
+        const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
         // swap-AB tile: M = 256 weight rows (128 per CTA, from the B slots), N = rows rounded up to 16 (from the
         // A slots): operands exchanged, accumulator lane = weight row, column = the tile's row
         const uint32_t idesc = tl.swap ? tc::idesc_bf16(256, (tl.rows + 15) & ~15) : (tl.m256 ? idesc256 : idesc128);
@@ -762,13 +808,13 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         tc::fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
         const int KB = tl.mode == 0 ? KB1 : KB2;
+        // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
+        const uint64_t a0 = tl.swap ? bdesc0 : adesc0, b0 = tl.swap ? adesc0 : bdesc0;
+        const uint32_t astep = tl.swap ? (kStageB >> 4) : (kSA >> 4), bstep = tl.swap ? (kSA >> 4) : (kStageB >> 4);
         for (int kb = 0; kb < KB; ++kb) {
           tc::mbar_wait_cluster(&s.full[stage], phase);
           tc::fence_after();
-          // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
-          const uint64_t sa = adesc0 + static_cast<uint64_t>(stage * (kSA >> 4));
-          const uint64_t sb = bdesc0 + static_cast<uint64_t>(stage * (kStageB >> 4));
-          const uint64_t ad = tl.swap ? sb : sa, bd = tl.swap ? sa : sb;
+          const uint64_t ad = a0 + static_cast<uint64_t>(stage * astep), bd = b0 + static_cast<uint64_t>(stage * bstep);
           if (tc::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / kUK; ++kk)
@@ -789,11 +835,10 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   } else {
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
-    uint8_t* stg = s.stg[q];
-    int g1 = 0, g2 = 0;
+    Cursor cur;
     int i = 0;
     for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const LTile tl = decode_ltile<kMT>(s, t, nseg, T1, NT1, NT2, la.swap_rows, g1, g2, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -833,10 +878,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
-            stage_row_bf16x32(stg, lane, c / 8, v);
+            if (valid) store_row_bf16x32(orow + hcol0 + c, v, d - (hcol0 + c));
           }
-          const int lim = (d - hcol0) * 2 < 128 ? (d - hcol0) * 2 : 128;
-          stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, lim, false);
         }
       } else {
         int64_t orow_idx = r;
@@ -847,7 +890,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
           valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
           const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
-          const int64_t i = valid_row ? v - p * la.vrows : 0;
+          const int64_t ii = valid_row ? v - p * la.vrows : 0;
           __nv_bfloat16* py = la.peer_y[0];
           const __nv_bfloat16* pr = la.peer_res[0];
 #pragma unroll
@@ -856,8 +899,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
               py = la.peer_y[j];
               pr = la.peer_res[j];
             }
-          orow = py + i * H;
-          rrow = pr ? pr + i * H : nullptr;
+          orow = py + ii * H;
+          rrow = pr ? pr + ii * H : nullptr;
         } else {
           if constexpr (kFuse == 1) {
             orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
@@ -867,20 +910,18 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < ncols; c0 += 64) {
-          const int col0 = tl.n0 + acc_off + c0;
-#pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
-            uint32_t vr[32];
-            tc::tmem_ld32(tacc + static_cast<uint32_t>(c0 + c), vr);
-            tc::tmem_wait_ld();
-            float v[32];
+        for (int c = 0; c < ncols; c += 32) {
+          const int col = tl.n0 + acc_off + c;
+          uint32_t vr[32];
+          tc::tmem_ld32(tacc + static_cast<uint32_t>(c), vr);
+          tc::tmem_wait_ld();
+          float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-            if (rrow && valid_row) add_bf16x32(rrow + col0 + c, v, H - (col0 + c));
-            stage_row_bf16x32(stg, lane, c / 8, v);
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+          if (valid_row) {
+            if (rrow) add_bf16x32(rrow + col, v, H - col);
+            store_row_bf16x32(orow + col, v, H - col);
           }
-          stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (H - col0) * 2, false);
         }
       }
       tc::fence_before();
@@ -891,8 +932,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           // publish this warp's share of the h tile to the down tiles (generic -> async proxy, then release);
           // an aborted tile still publishes, so its down tiles stop waiting (they store nothing either)
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + s.mt_start[tl.g] + tl.mt)
-                       : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.ready + tl.mid) : "memory");
         }
       }
     }
@@ -933,7 +973,7 @@ const DevInfo& dev_info() {
                               {reinterpret_cast<const void*>(ffn_layer2_kernel<0, 256>),
                                reinterpret_cast<const void*>(ffn_layer2_kernel<1, 256>),
                                reinterpret_cast<const void*>(ffn_layer2_kernel<2, 256>)}};
-    const size_t lsmem[2] = {kSmemBytesD, kSmemBytes};
+    const size_t lsmem[2] = {kSmemBytesLD, kSmemBytesL};
     for (int v = 0; v < 2; ++v) {
       int mp = 1 << 30;
       for (int i = 0; i < 3 && di.err == cudaSuccess; ++i) {
@@ -1109,7 +1149,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = mt == 128 ? kSmemBytesD : kSmemBytes;
+  cfg.dynamicSmemBytes = mt == 128 ? kSmemBytesLD : kSmemBytesL;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
