@@ -7,8 +7,9 @@ A step is one pass of the whole hot path (route -> dispatch ->
 (+SiLU) -> grouped down GEMM -> combine) over one batch of synthetic tokens, through the C ABI
 (libreadme_b200.so). N=1 runs BASELINE config 2 (one Llama-2-7B-shaped MoE layer, T=8192 prefill
 tokens, 8 experts of d=5504 neurons, top-1, bf16). N>1 (launched by torchrun) runs the expert-parallel
-layer (config 5 per rank: 8192 tokens per rank, experts sharded over ranks, NCCL all-to-all), weak
-scaling; value = all ranks' tokens / max-over-ranks time.
+layer (config 5: 65536 tokens in all, 65536/N per rank, experts sharded over ranks; all-to-alls fused into the
+kernels over peer memory, with the NCCL all-to-all path timed beside it), strong scaling; value = all ranks'
+tokens / max-over-ranks time.
 
 Rank 0 prints ONE JSON line. `--impl reference` times the CPU oracle (the tier's reference arm) on a
 bounded token sample of the same workload.
@@ -48,6 +49,7 @@ def parse():
     ap.add_argument("--ep", default="peer", choices=["peer", "nccl"],
                     help="N>1 expert parallelism: all-to-alls fused into the kernels over peer memory (default) "
                          "or NCCL all_to_all_single between the library's kernels")
+    ap.add_argument("--no-nccl-record", action="store_true", help="N>1: skip the NCCL all-to-all sub-record")
     ap.add_argument("--offload", action="store_true",
                     help="config 4 in the memory-constrained mode (NEXT-4): experts in pinned host memory")
     return ap.parse_args()
@@ -211,7 +213,9 @@ def run_reference(args):
         return
     import oracle
     import synth
-    cfg = dict(synth.CONFIGS[args.config])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg_id = 5 if world > 1 else args.config  # the same workload as this arm's N-GPU line
+    cfg = dict(synth.CONFIGS[cfg_id])
     T, H, D, d, E = cfg["T"], cfg["H"], cfg["D"], cfg["d"], cfg["E"]
     seed = synth.MASTER_SEED + 2
     wg, wu, wd = synth.dense_ffn_weights(D, H, d, seed=seed)
@@ -235,11 +239,12 @@ def run_reference(args):
     value = per_step * len(times) / tot
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"config{args.config}_{cfg['name']}", "T": T, "H": H, "E": E, "d": d,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"config{cfg_id}_{cfg['name']}", "T": T, "H": H, "E": E, "d": d,
                        "k": cfg["k"], "tokens_per_step_sampled": per_step},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": f"{per_step} random tokens per step of config {args.config}"},
+                             "sample": f"{per_step} random tokens per step of config {cfg_id}", "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -814,7 +819,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = dict(synth.CONFIGS[args.config if world == 1 else 5])
-    T = args.tokens or (cfg["T"] if world == 1 else 8192)
+    # N > 1: config 5 as BASELINE.json states it, 65536 tokens in all, strong scaling (65536 / N per rank)
+    T = args.tokens or (cfg["T"] if world == 1 else cfg["T"] // world)
     H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x L2
@@ -962,10 +968,11 @@ def main():
 
     pk, pk_src = peaks()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": (f"config{args.config}_{cfg['name']}" if world == 1 else "config5_expert_parallel"),
-                       "T_per_gpu": T, "H": H, "D": cfg["D"], "E": E, "d": d, "k": k,
+                       "T_per_gpu": T, "T_total": T * world, "H": H, "D": cfg["D"], "E": E, "d": d, "k": k,
                        "parallelism": "single" if world == 1 else f"ep{world}",
                        **({} if world == 1 else {"ep_exchange": "peer-memory stores fused into the dispatch kernel "
                                                  "and the down-GEMM epilogue" if ep_mode == "peer" else
@@ -1171,6 +1178,27 @@ def main():
         line["e2e"]["roofline"] = {"bound": "pcie", "copies_only_ms": c_ms, "frac": c_ms / p_ms,
                                    "note": "the step's H2D and D2H bytes copied concurrently, nothing else"}
         del xd2
+
+    if world > 1 and ep_mode == "peer" and not args.no_nccl_record:
+        # the north star's NCCL all-to-all, measured beside the fused path on the same ranks and tokens: route +
+        # one count exchange (host split sizes) + dispatch -> all_to_all_single -> grouped FFN ->
+        # all_to_all_single -> combine, eager (split sizes are host values), max over ranks
+        nl = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
+        for _ in range(args.warmup):
+            nl.step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        n_ms = timed(nl.step, args.steps)
+        dist.barrier()
+        nt = torch.tensor([float(sum(n_ms))], device=dev)
+        dist.all_reduce(nt, op=dist.ReduceOp.MAX)
+        n_per = float(nt.item()) / args.steps
+        line["nccl_exchange"] = {"value": T * world / (n_per * 1e-3), "unit": UNIT, "ms_per_step": n_per,
+                                 "vs_fused": ms_per_step / n_per,
+                                 "mode": "NCCL all_to_all_single between the library's dispatch / grouped FFN / "
+                                         "combine kernels, one count exchange per step, eager"}
+        del nl
+        torch.cuda.empty_cache()
 
     if world > 1 and not args.no_e2e:
         # e2e at N GPUs through the public API: every step each rank uploads its tokens and logits from

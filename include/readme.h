@@ -228,6 +228,21 @@ readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const i
                                     const readme_router_weights* w, float eps, float* logits, uint32_t* dev_status,
                                     void* ws, size_t ws_bytes, readme_stream_t stream);
 
+/* The router AND the routing plan in one call (NEXT-1 fusion: "fuse the gating head and
+ * top-k into route"): the block runs as in readme_router_forward, then ONE launch consumes its last hidden
+ * state and computes the final RMSNorm, the gating head (logits written to `logits`, bit-identical to
+ * readme_router_forward's), the top-k / weights, the per-expert histogram, the exclusive scan and the stable
+ * permutation (readme_route's a1-a4 on those logits, bit-identical to calling readme_route on them). Plan
+ * arrays as in readme_route (src required). k in [1, n_experts]. The one-launch form covers batches the
+ * single-launch route takes (T*k <= 256K slots); larger batches run the head kernel, then readme_route's
+ * multi-CTA form, with the same results. ws: readme_router_route_workspace_bytes(T, nseq, n_experts, k). */
+size_t readme_router_route_workspace_bytes(int64_t T, int32_t nseq, int32_t E, int32_t k);
+readme_status readme_router_forward_route(const int32_t* token_ids, int64_t T, const int32_t* seq_starts,
+                                          int32_t nseq, const readme_router_weights* w, float eps, int32_t k,
+                                          float* logits, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                                          int32_t* offsets, int32_t* dest, int32_t* src, uint32_t* dev_status,
+                                          void* ws, size_t ws_bytes, readme_stream_t stream);
+
 /* Incremental evaluation (decode; SURVEY §8(f) NEXT-1 "run once per request, incrementally only for new
  * tokens"): n new tokens, token i of request slot[i] at position pos[i] (0-based within its request). Each
  * token's RoPE'd key and value are appended to kv_cache[slot][pos] (bf16 [n_slots, max_len, 2, 512]: k then v

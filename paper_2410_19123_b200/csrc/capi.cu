@@ -647,6 +647,37 @@ readme_status readme_router_forward(const int32_t* token_ids, int64_t T, const i
                                reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t readme_router_route_workspace_bytes(int64_t T, int32_t nseq, int32_t E, int32_t k) {
+  return align_up(router_ws_bytes(T < 0 ? 0 : T, nseq < 1 ? 1 : nseq), 256) +
+         route_ws_bytes(T < 0 ? 0 : T, E < 1 ? 1 : E, k < 1 ? 1 : k);
+}
+
+readme_status readme_router_forward_route(const int32_t* token_ids, int64_t T, const int32_t* seq_starts,
+                                          int32_t nseq, const readme_router_weights* w, float eps, int32_t k,
+                                          float* logits, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                                          int32_t* offsets, int32_t* dest, int32_t* src, uint32_t* dev_status,
+                                          void* ws, size_t ws_bytes, readme_stream_t stream) {
+  README_CHECK_ARG(T >= 0 && T < (int64_t(1) << 31), "T out of range");
+  README_CHECK_ARG(nseq >= 1, "nseq must be >= 1");
+  RouterWeights rw;
+  README_TRY(check_router_weights(w, eps, &rw));
+  README_TRY(check_route_args(T, rw.n_experts, k));
+  README_CHECK_ARG(counts && offsets, "counts and offsets are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (T == 0) return launch_route(nullptr, README_F32, 0, rw.n_experts, k, nullptr, nullptr, counts, offsets, nullptr,
+                                  nullptr, dev_status, ws, st);
+  README_CHECK_ARG(token_ids && seq_starts && logits && topk_idx && topk_w && dest && src && ws && aligned16(ws),
+                   "null pointer argument (or unaligned workspace)");
+  const size_t need = readme_router_route_workspace_bytes(T, nseq, rw.n_experts, k);
+  if (ws_bytes < need) {
+    set_error("router+route workspace too small: %zu < %zu", ws_bytes, need);
+    return README_ERR_WORKSPACE;
+  }
+  const RoutePlanOut plan{k, topk_idx, counts, offsets, dest, src, topk_w,
+                          static_cast<char*>(ws) + align_up(router_ws_bytes(T, nseq), 256)};
+  return launch_router_forward(token_ids, T, seq_starts, nseq, rw, eps, logits, ws, dev_status, st, &plan);
+}
+
 readme_status readme_build_experts(const void* dense_w_gate, const void* dense_w_up, const void* dense_w_down,
                                    readme_dtype dt, int32_t D, int32_t H, int32_t E, int32_t d,
                                    const int32_t* neuron_idx, void* w_gate, void* w_up, void* w_down,

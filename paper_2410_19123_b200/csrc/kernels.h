@@ -12,11 +12,24 @@ enum class Knob : int {
 int knob(Knob k);
 
 // route.cu
+// The pre-gating router's gating head as the route's input (NEXT-1 fusion): logits = RMSNorm(h)*g . W^T are
+// computed inside the route launch (E <= 16 and the single-launch route; else by the head kernel first) and
+// written to `logits` [T, E] f32.
+struct RouteHead {
+  const __nv_bfloat16* h;  // [T, 512] the router block's output hidden state
+  const __nv_bfloat16* g;  // [512]
+  const __nv_bfloat16* w;  // [E, 512]
+  float eps;
+  float* logits;           // [T, E] out
+};
 size_t route_ws_bytes(int64_t T, int32_t E, int32_t k);
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
                            int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize = true,
-                           uint32_t* zero = nullptr, int64_t zero_words = 0);
+                           uint32_t* zero = nullptr, int64_t zero_words = 0, const RouteHead* head = nullptr);
+// router.cu: the separate gating-head kernel (logits [T, N] f32 from the hidden state)
+readme_status launch_router_head(const __nv_bfloat16* h2, int64_t T, const __nv_bfloat16* gf,
+                                 const __nv_bfloat16* whead, int N, float eps, float* logits, cudaStream_t st);
 // zero/zero_words: words the launch zeroes (the FFN's readiness region, so no memset node precedes it; a
 // memset on the multi-CTA path).
 // true when launch_route runs the single-launch cluster route for this batch: it then always finalizes
@@ -113,9 +126,17 @@ struct RouterWeights {
   const __nv_bfloat16 *emb, *g1, *wqkv, *wo, *g2, *wg, *wu, *wd, *gf, *whead;
 };
 size_t router_ws_bytes(int64_t T, int32_t nseq);
+// plan != null: instead of the head kernel, the routing plan is built by the route launch that consumes the
+// block's hidden state (head fused into a1-a4); logits are still written.
+struct RoutePlanOut {
+  int32_t k;
+  int32_t *topk_idx, *counts, *offsets, *dest, *src;
+  float* topk_w;
+  void* ws;  // route workspace (route_ws_bytes)
+};
 readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
                                     const RouterWeights& w, float eps, float* logits, void* ws,
-                                    uint32_t* dev_status, cudaStream_t st);
+                                    uint32_t* dev_status, cudaStream_t st, const RoutePlanOut* plan = nullptr);
 size_t router_step_ws_bytes(int64_t n, int32_t max_len);
 readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* slot, const int32_t* pos,
                                  __nv_bfloat16* kv, int32_t n_slots, int32_t max_len, const RouterWeights& w,

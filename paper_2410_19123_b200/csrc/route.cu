@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include "kernels.h"
+#include "router_head.cuh"
 
 namespace readme {
 
@@ -77,6 +78,10 @@ __device__ __forceinline__ bool beats(float v, int id, float bv, int bid) {
 // over the selected logits. Writes idx/w of the token's k slots and their expert ids to s_exp. For small E
 // this costs a few instructions per token, where a lane group per token (the E > 32 path) spends a warp
 // pass per 32/lpt tokens.
+template <int NE>
+__device__ __forceinline__ void topk_select(float (&v)[NE], int E, int k, int32_t* __restrict__ idx_out,
+                                            float* __restrict__ w_out, uint8_t* __restrict__ s_exp_out, bool& bad);
+
 template <int NE, typename LogitT>
 __device__ __forceinline__ void topk_one_token(const LogitT* __restrict__ row, int E, int k, bool vec,
                                                int32_t* __restrict__ idx_out, float* __restrict__ w_out,
@@ -109,6 +114,14 @@ __device__ __forceinline__ void topk_one_token(const LogitT* __restrict__ row, i
       for (int e = 0; e < NE; ++e) v[e] = e < E ? load_logit(row, e) : -INFINITY;
     }
   }
+  topk_select<NE>(v, E, k, idx_out, w_out, s_exp_out, bad);
+}
+
+// Top-k of one token's E <= NE logits held in registers (ties -> lower id, Q2), softmax weights over the
+// selected logits (Q1; k == 1 gives exactly 1.0f), non-finite logits flagged (Q3).
+template <int NE>
+__device__ __forceinline__ void topk_select(float (&v)[NE], int E, int k, int32_t* __restrict__ idx_out,
+                                            float* __restrict__ w_out, uint8_t* __restrict__ s_exp_out, bool& bad) {
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     if (e < E && !isfinite(v[e])) {
@@ -365,10 +378,20 @@ constexpr int kCWarps = kCThreads / kWarp;
 constexpr int kCMaxCluster = 16;
 constexpr int64_t kClusterMaxSlots = 256 * 1024;  // beyond: the multi-CTA lookback route
 constexpr int kCMaxSmem = (kMaxLogitFloats + kCWarps * README_MAX_EXPERTS) * 4;  // 64 KB
+// head mode (E <= 16): s_wcount, W_head in bf16 and the sub-tile's fp32 logits
+constexpr int kCHeadMaxE = 16;
+constexpr int kCMaxSmemHead = (kCWarps * kCHeadMaxE + kCThreads * kCHeadMaxE) * 4 + kCHeadMaxE * kRouterDim * 2;
 
 struct RouteExtra {
   uint32_t* zero;      // nullable: words zeroed by the launch (the FFN's readiness region)
   int64_t zero_words;
+  // head mode (non-null head_h, E <= 16): each sub-tile's logits are computed in the launch from the pre-gating
+  // router's last hidden state (router_head.cuh) into shared memory, written out to head_logits, then routed
+  const __nv_bfloat16* head_h;  // [T, 512]
+  const __nv_bfloat16* head_g;  // [512] final RMSNorm weight
+  const __nv_bfloat16* head_w;  // [E, 512] gating head
+  float head_eps;
+  float* head_logits;           // [T, E] out
 };
 
 struct ClusterGeom {
@@ -410,6 +433,12 @@ route_cluster_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k,
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
   for (int e = tid; e < E; e += kCThreads) s_run[e] = 0;
   if (tid == 0) s_bad = 0;
+  __nv_bfloat16* s_whead = reinterpret_cast<__nv_bfloat16*>(route_smem + sizeof(int) * kCWarps * E);
+  float* s_hl = reinterpret_cast<float*>(route_smem + sizeof(int) * kCWarps * E + sizeof(__nv_bfloat16) * E * kRouterDim);
+  if (NE > 0 && ex.head_h) {
+    for (int i = tid; i < E * kRouterDim; i += kCThreads) s_whead[i] = ex.head_w[i];
+    __syncthreads();
+  }
   const int64_t tok0 = static_cast<int64_t>(crank) * chunk;
   const int64_t tok1 = tok0 + chunk < T ? tok0 + chunk : T;
   const int tokens_per_warp_iter = kWarp / lpt;
@@ -423,9 +452,29 @@ route_cluster_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k,
     // ---- phase A: top-k per token: a thread per token (E <= 32), else logits -> smem and lane groups ----
     const LogitT* lsrc = logits + t0 * E;
     if constexpr (NE > 0) {
-      if (tid < nt)
+      if (ex.head_h) {
+        // the sub-tile's logits from the router's hidden state, one warp per token (bit-identical to the
+        // separate head kernel), kept in shared memory for the thread-per-token top-k below
+        for (int tok = warp; tok < nt; tok += kCWarps) {
+          const int64_t t = t0 + tok;
+          head_logits_warp(ex.head_h + t * kRouterDim, ex.head_g,
+                           [&](int n, int c) { return __bfloat162float(s_whead[n * kRouterDim + c]); }, E,
+                           ex.head_eps, lane, [&](int n, float v) {
+                             s_hl[tok * E + n] = v;
+                             ex.head_logits[t * E + n] = v;
+                           });
+        }
+        __syncthreads();
+        if (tid < nt) {
+          float v[NE];
+#pragma unroll
+          for (int e = 0; e < NE; ++e) v[e] = e < E ? s_hl[tid * E + e] : -INFINITY;
+          topk_select<NE>(v, E, k, topk_idx + (t0 + tid) * k, topk_w + (t0 + tid) * k, s_exp + tid * k, bad);
+        }
+      } else if (tid < nt) {
         topk_one_token<NE>(lsrc + static_cast<int64_t>(tid) * E, E, k, row_vec_ok(logits, E),
                            topk_idx + (t0 + tid) * k, topk_w + (t0 + tid) * k, s_exp + tid * k, bad);
+      }
     } else {
     for (int i = tid; i < nt * E; i += kCThreads) {
       float v = load_logit(lsrc, i);
@@ -593,7 +642,8 @@ int max_route_cluster() {
     bool ok16 = true;
     for (int ne : {0, 8, 16, 32}) {
       for (const void* f : {cluster_fn<float>(ne), cluster_fn<__nv_bfloat16>(ne)}) {
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kCMaxSmem);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kCMaxSmem > kCMaxSmemHead ? kCMaxSmem : kCMaxSmemHead);
         ok16 = ok16 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
       }
     }
@@ -663,19 +713,36 @@ size_t route_ws_bytes(int64_t T, int32_t E, int32_t k) {
 readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T, int32_t E, int32_t k,
                            int32_t* topk_idx, float* topk_w, int32_t* counts, int32_t* offsets, int32_t* dest,
                            int32_t* src, uint32_t* dev_status, void* ws, cudaStream_t st, bool finalize,
-                           uint32_t* zero, int64_t zero_words) {
+                           uint32_t* zero, int64_t zero_words, const RouteHead* head) {
   if (T == 0) {
     README_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st));
     README_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), st));
     return README_OK;
   }
+  if (head) {  // the logits come from the gating head; f32 from here on
+    logits = head->logits;
+    logits_dt = README_F32;
+  }
+  // the head runs inside the single-launch route (E <= 16); otherwise as its own kernel first
+  bool head_fused = head != nullptr && E <= kCHeadMaxE && use_cluster_route(T, k);
+  if (head && !head_fused)
+    README_TRY(launch_router_head(head->h, T, head->g, head->w, E, head->eps, head->logits, st));
   int lpt = 1;
   while (lpt < E && lpt < kWarp) lpt <<= 1;
   const int items = (E + lpt - 1) / lpt;
   if (use_cluster_route(T, k)) {
     // one cluster launch: a1-a4 including the finalize (dest = offsets + rank, src)
     const ClusterGeom cg = cluster_geom(T, E, k);
-    RouteExtra ex{zero, zero_words};
+    RouteExtra ex{zero, zero_words, nullptr, nullptr, nullptr, 0.f, nullptr};
+    size_t smem = cg.smem;
+    if (head_fused) {
+      ex.head_h = head->h;
+      ex.head_g = head->g;
+      ex.head_w = head->w;
+      ex.head_eps = head->eps;
+      ex.head_logits = head->logits;
+      smem += sizeof(__nv_bfloat16) * static_cast<size_t>(E) * kRouterDim + sizeof(float) * cg.tile_tokens * E;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -684,7 +751,7 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(static_cast<unsigned>(cg.C));
     cfg.blockDim = dim3(kCThreads);
-    cfg.dynamicSmemBytes = cg.smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
@@ -698,6 +765,7 @@ readme_status launch_route(const void* logits, readme_dtype logits_dt, int64_t T
     // result, finalized as the caller expects from the single-launch path
     cudaGetLastError();
     finalize = true;
+    if (head_fused) README_TRY(launch_router_head(head->h, T, head->g, head->w, E, head->eps, head->logits, st));
   }
   if (zero && zero_words > 0) README_CUDA(cudaMemsetAsync(zero, 0, sizeof(uint32_t) * zero_words, st));
   RouteGeom g = route_geom(T, E, k);

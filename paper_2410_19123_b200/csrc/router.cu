@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include "kernels.h"
+#include "router_head.cuh"
 
 namespace readme {
 
@@ -92,7 +93,8 @@ __global__ void rmsnorm512_kernel(const __nv_bfloat16* __restrict__ x, int64_t T
   }
 }
 
-// Gating head: logits[t] = (RMSNorm(h2[t]) * gf) . W_head^T, fp32. One warp per token, W_head in smem.
+// Gating head: logits[t] = (RMSNorm(h2[t]) * gf) . W_head^T, fp32. One warp per token, W_head in smem
+// (router_head.cuh; the fused head + route launch in route.cu computes the same bits).
 __global__ void router_head_kernel(const __nv_bfloat16* __restrict__ h2, int64_t T, const __nv_bfloat16* __restrict__ gf,
                                    const __nv_bfloat16* __restrict__ whead, int N, float eps, float* __restrict__ logits) {
   extern __shared__ float s_w[];  // [N][512]
@@ -101,24 +103,8 @@ __global__ void router_head_kernel(const __nv_bfloat16* __restrict__ h2, int64_t
   const int lane = threadIdx.x % kWarp;
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x / kWarp) + threadIdx.x / kWarp;
   if (t >= T) return;
-  float v[16];
-  float ss = 0.f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    v[i] = __bfloat162float(h2[t * kD + lane + 32 * i]);
-    ss = fmaf(v[i], v[i], ss);
-  }
-  ss = warp_sum(ss);
-  const float r = rsqrtf(ss / kD + eps);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] *= r * __bfloat162float(gf[lane + 32 * i]);
-  for (int n = 0; n < N; ++n) {
-    float acc = 0.f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc = fmaf(v[i], s_w[n * kD + lane + 32 * i], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) logits[t * N + n] = acc;
-  }
+  head_logits_warp(h2 + t * kD, gf, [&](int n, int c) { return s_w[n * kD + c]; }, N, eps, lane,
+                   [&](int n, float v) { logits[t * N + n] = v; });
 }
 
 // Causal attention with RoPE on the tensor cores (mma.sync m16n8k16 bf16 -> fp32), flash-attention style:
@@ -520,7 +506,7 @@ namespace {
 readme_status router_tail(int64_t T, const RouterWeights& w, float eps, float* logits, const int32_t* offs,
                           const __nv_bfloat16* h0, __nv_bfloat16* a, const __nv_bfloat16* att, __nv_bfloat16* h1,
                           __nv_bfloat16* h2, __nv_bfloat16* hff, uint32_t* ready, uint32_t* dev_status,
-                          cudaStream_t st) {
+                          cudaStream_t st, const RoutePlanOut* plan) {
   const int wpb = 8;
   const unsigned gblocks = static_cast<unsigned>((T + wpb - 1) / wpb);
   // h1 = h0 + att . Wo^T (the residual add fused into the GEMM epilogue)
@@ -531,10 +517,14 @@ readme_status router_tail(int64_t T, const RouterWeights& w, float eps, float* l
   // `ready` was zeroed by the embed launch (pdl = true: no memset node; the FFN waits on the RMSNorm grid)
   README_TRY(launch_ffn_layer_2cta(a, T, kD, 1, kD, 1, offs, w.wg, w.wu, w.wd, hff, h2, nullptr, h1, ready,
                                    dev_status, st, nullptr, 0, nullptr, true, nullptr));
-  router_head_kernel<<<gblocks, 32 * wpb, w.n_experts * kD * sizeof(float), st>>>(h2, T, w.gf, w.whead,
-                                                                                   w.n_experts, eps, logits);
-  README_CUDA(cudaGetLastError());
-  return README_OK;
+  if (plan) {
+    // NEXT-1 fusion: the final RMSNorm + gating head + top-k / histogram / scan / permutation in ONE route
+    // launch that consumes h2 (logits still written, bit-identical to the head kernel's)
+    const RouteHead head{h2, w.gf, w.whead, eps, logits};
+    return launch_route(logits, README_F32, T, w.n_experts, plan->k, plan->topk_idx, plan->topk_w, plan->counts,
+                        plan->offsets, plan->dest, plan->src, dev_status, plan->ws, st, true, nullptr, 0, &head);
+  }
+  return launch_router_head(h2, T, w.gf, w.whead, w.n_experts, eps, logits, st);
 }
 }  // namespace
 
@@ -544,9 +534,19 @@ size_t router_ws_bytes(int64_t T, int32_t nseq) {
   return 256 + 8 * act + 2 * tiles + 256 + act + ffn_layer_ready_bytes(T, 1) + 256;
 }
 
+readme_status launch_router_head(const __nv_bfloat16* h2, int64_t T, const __nv_bfloat16* gf,
+                                 const __nv_bfloat16* whead, int N, float eps, float* logits, cudaStream_t st) {
+  if (T == 0) return README_OK;
+  const int wpb = 8;
+  const unsigned gblocks = static_cast<unsigned>((T + wpb - 1) / wpb);
+  router_head_kernel<<<gblocks, 32 * wpb, N * kD * sizeof(float), st>>>(h2, T, gf, whead, N, eps, logits);
+  README_CUDA(cudaGetLastError());
+  return README_OK;
+}
+
 readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t* seq_starts, int32_t nseq,
                                     const RouterWeights& w, float eps, float* logits, void* ws,
-                                    uint32_t* dev_status, cudaStream_t st) {
+                                    uint32_t* dev_status, cudaStream_t st, const RoutePlanOut* plan) {
   if (T == 0) return README_OK;
   const size_t act = align_up(static_cast<size_t>(T) * kD * 2, 256);
   const size_t tiles_b = align_up(static_cast<size_t>(T / kQT + nseq + 1) * sizeof(int32_t), 256);
@@ -581,7 +581,7 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   dim3 ag(static_cast<unsigned>(max_tiles), kHeads);
   router_attention_kernel<<<ag, 128, 0, st>>>(qkv, seq_starts, tile_seq, tile_q0, ntiles, att);
   README_CUDA(cudaGetLastError());
-  return router_tail(T, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
+  return router_tail(T, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st, plan);
 }
 
 size_t router_step_ws_bytes(int64_t n, int32_t max_len) {
@@ -626,7 +626,7 @@ readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* s
   README_CUDA(cudaGetLastError());
   router_decode_merge_kernel<<<dim3(static_cast<unsigned>(n), kHeads), 128, 0, st>>>(part, nchunk, att);
   README_CUDA(cudaGetLastError());
-  return router_tail(n, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st);
+  return router_tail(n, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st, nullptr);
 }
 
 }  // namespace readme

@@ -27,7 +27,8 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_expert_ffn", "readme_expert_gate_up", "readme_expert_down", "readme_combine", "readme_moe_layer_workspace_bytes", "readme_moe_layer",
            "readme_build_experts", "readme_permanent_expert_workspace_bytes", "readme_permanent_expert",
            "readme_router_workspace_bytes", "readme_router_forward", "readme_router_step_workspace_bytes",
-           "readme_router_step", "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
+           "readme_router_step", "readme_router_route_workspace_bytes", "readme_router_forward_route",
+           "readme_dispatch_rmsnorm", "readme_moe_stack_workspace_bytes", "readme_moe_stack",
            "readme_scheduler_create", "readme_scheduler_destroy", "readme_scheduler_push", "readme_scheduler_queued",
            "readme_scheduler_next_batch", "readme_expert_ffn_slots", "readme_cache_create", "readme_cache_destroy",
            "readme_cache_set_future", "readme_cache_access", "readme_cache_lookup", "readme_cache_stats",
@@ -87,6 +88,9 @@ _SIGS = {
     "readme_router_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, ctypes.c_float, _vp, _vp, _vp,
                                           _sz, _vp]),
     "readme_router_forward": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _vp, _vp, _vp, _sz, _vp]),
+    "readme_router_route_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32]),
+    "readme_router_forward_route": (ctypes.c_int, [_vp, _i64, _vp, _i32, _vp, ctypes.c_float, _i32, _vp, _vp, _vp,
+                                                   _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "readme_expert_ffn_slots": (ctypes.c_int, [_vp, ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _vp,
                                                _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "readme_cache_create": (_vp, [_i32, _i32, ctypes.c_uint64]),
@@ -478,6 +482,34 @@ def router_forward(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: d
         _ptr(token_ids), T, _ptr(seq_starts), nseq, ctypes.cast(ctypes.pointer(w), ctypes.c_void_p),
         ctypes.c_float(eps), _ptr(out), _ptr(dev_status), _ptr(ws), ws.numel(), st))
     return out
+
+
+def router_forward_route(token_ids: torch.Tensor, seq_starts: torch.Tensor, weights: dict, k: int = 1,
+                         eps: float = 1e-5, plan: Plan | None = None, out: torch.Tensor | None = None,
+                         ws: torch.Tensor | None = None) -> tuple[torch.Tensor, Plan]:
+    """The router and the routing plan in one call (readme_router_forward_route): the block, then ONE route
+    launch that computes the final RMSNorm + gating head + a1-a4 from the block's hidden state. Returns
+    (logits [T, N] f32, plan)."""
+    T = token_ids.numel()
+    nseq = seq_starts.numel() - 1
+    N = weights["w_head"].shape[0]
+    dev = token_ids.device
+    out = out if out is not None else torch.empty((T, N), dtype=torch.float32, device=dev)
+    plan = plan if plan is not None else new_plan(T, N, k, dev)
+    need = int(lib().readme_router_route_workspace_bytes(T, nseq, N, k))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    st = _prep(token_ids, seq_starts, out, ws, *[weights[kk] for kk in ROUTER_KEYS], *plan_tensors(plan))
+    w = _RouterWeights(weights["emb"].shape[0], N, *[weights[kk].data_ptr() for kk in ROUTER_KEYS])
+    _check("readme_router_forward_route", lib().readme_router_forward_route(
+        _ptr(token_ids), T, _ptr(seq_starts), nseq, ctypes.cast(ctypes.pointer(w), ctypes.c_void_p),
+        ctypes.c_float(eps), k, _ptr(out), _ptr(plan.topk_idx), _ptr(plan.topk_w), _ptr(plan.counts),
+        _ptr(plan.offsets), _ptr(plan.dest), _ptr(plan.src), _ptr(plan.dev_status), _ptr(ws), ws.numel(), st))
+    return out, plan
+
+
+def plan_tensors(plan: Plan):
+    return (plan.topk_idx, plan.topk_w, plan.counts, plan.offsets, plan.dest, plan.src, plan.dev_status)
 
 
 def new_router_cache(n_slots: int, max_len: int, device) -> torch.Tensor:

@@ -141,3 +141,60 @@ def test_peer_ep_on_one_gpu_equals_single_layer(world, k, residual):
         p.join(timeout=60)
     for rank, ok, _ in res:
         assert ok is True, f"rank {rank}: {ok}"
+
+
+# ---- the NCCL branch: device all-to-alls on a real NCCL process group --------------------------------------
+
+def _nccl_worker(port, T, H, E, d, k, q):
+    """world_size 1 on NCCL (legal on one GPU): exercises the device all_to_all_single path of ep.exchange /
+    ep.plan_from_counts (no host staging) and the peer-memory path's flag phases under an NCCL group."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    layer = None
+    try:
+        import synth
+        from paper_2410_19123_b200 import ep
+        from paper_2410_19123_b200 import readme as rd
+        assert not ep._host_staged(None)
+        x = synth.to_torch(synth.tokens(T, H, seed=21), "bf16").to(dev)
+        lg = torch.from_numpy(synth.router_logits(T, E, seed=22)).to(dev)
+        W = [synth.to_torch(w, "bf16").to(dev) for w in synth.expert_weights(E, d, H, seed=23)]
+        y_full, _ = rd.moe_layer(x, *W, k=k, logits=lg)
+        nccl = ep.EPMoELayer(x, lg, *W, E, k)
+        y = nccl.step()
+        torch.cuda.synchronize()
+        ok = torch.equal(y, y_full)
+        ok = ok and nccl.ep.send_splits == [T * k] and nccl.ep.recv_splits == [T * k]
+        layer = ep.PeerEPLayer(T, H, E, k, *W, device=dev)
+        layer.x.copy_(x)
+        layer.route(lg)
+        y2 = layer.layer(residual=False)
+        torch.cuda.synchronize()
+        ok = ok and torch.equal(y2, y_full) and int(layer.dev_status.item()) == 0
+        q.put((bool(ok), None))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((traceback.format_exc(), None))
+    finally:
+        if layer is not None:
+            try:
+                layer.close()
+            except Exception:
+                pass
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_nccl_branch_world1_equals_single_layer(k):
+    """The NCCL exchange (device all_to_all_single with split sizes) and the peer-memory path both run under an
+    NCCL process group of one rank and reproduce the single-GPU layer bit for bit."""
+    T, H, E, d = 1000, 256, 8, 256
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_port(), T, H, E, d, k, q))
+    p.start()
+    ok, _ = q.get(timeout=300)
+    p.join(timeout=60)
+    assert ok is True, ok

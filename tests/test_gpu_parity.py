@@ -913,6 +913,44 @@ def test_router_forward_parity(rd):
     _check_plan(plan, oracle.route(lg.cpu(), 1), 1)
 
 
+@pytest.mark.parametrize("k,impl", [(1, None), (2, None), (1, "lookback")])
+def test_router_forward_route_fused(rd, knob, k, impl):
+    """NEXT-1 fusion: readme_router_forward_route computes the final RMSNorm + gating head + a1-a4 in ONE route
+    launch from the block's hidden state. Its logits are bit-identical to readme_router_forward's, its plan is
+    bit-identical to readme_route on those logits (and to the fp64 oracle's route of them), and its decisions
+    follow the fixed bf16 band vs the fp64 router oracle. impl = lookback forces the fallback (head kernel,
+    then the multi-CTA route): same results."""
+    from oracle import router
+    if impl:
+        knob("route", ROUTE_IMPL[impl])
+    vocab, N = 32000, 8
+    W = {kk: synth.to_torch(v, "bf16") for kk, v in synth.router_weights(vocab=vocab, n_experts=N, seed=195).items()}
+    Wd = {kk: v.to(DEV) for kk, v in W.items()}
+    lens = [1, 64, 100, 37, 300, 1500]
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(starts[-1])
+    ids = synth.token_ids(T, vocab=vocab, seed=196)
+    ids_d, st_d = torch.from_numpy(ids).to(DEV), torch.from_numpy(starts).to(DEV)
+    lg_sep = rd.router_forward(ids_d, st_d, Wd)
+    lg, plan = rd.router_forward_route(ids_d, st_d, Wd, k=k)
+    plan2 = rd.route(lg_sep, k)
+    torch.cuda.synchronize()
+    assert torch.equal(lg, lg_sep)
+    for name in ("topk_idx", "topk_w", "counts", "offsets", "dest", "src"):
+        assert torch.equal(getattr(plan, name), getattr(plan2, name)), name
+    assert int(plan.dev_status.item()) == 0
+    _check_plan(plan, oracle.route(lg.cpu(), k), k)
+    ref = router.forward(ids, starts, W)
+    got = _np(lg).astype(np.float64)
+    assert rel_err(got, ref) <= BF16_TOL
+    tol = BF16_TOL * np.abs(ref).max(axis=1)
+    top = np.sort(ref, axis=1)
+    gpu_ids = _np(plan.topk_idx)[:, 0]
+    clear = (top[:, -1] - top[:, -2]) > 2.0 * tol
+    assert np.array_equal(gpu_ids[clear], ref.argmax(axis=1)[clear])
+    assert np.all(ref[np.arange(T), gpu_ids] >= top[:, -1] - 2.0 * tol)
+
+
 def test_router_causal_on_gpu(rd):
     """Appending tokens to a sequence never changes the GPU logits of its prefix (bitwise: the kernels
     process each query row against keys <= it in a fixed order)."""
