@@ -117,6 +117,25 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# ---- L2 flush between timed steps ----------------------------------------------------------------------------
+
+class L2Flush:
+    """Between timed steps: write a 256 MiB buffer (2x L2), then read another 256 MiB, so a timed step starts
+    with none of its own data in L2 AND without the flush's dirty lines, whose write-back would otherwise
+    compete with the step's own DRAM stream (measured: ~126 MB of write-backs inside a decode step)."""
+
+    NOTE = "flushed between timed steps (256 MiB written, then 256 MiB read: no step data, no dirty lines)"
+
+    def __init__(self, dev):
+        import torch
+        self.w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+
+    def zero_(self):
+        self.w.zero_()
+        self.r.sum()
+
+
 # ---- workload -------------------------------------------------------------------------------------
 
 def make_inputs(cfg: dict, T: int, rank: int, device, E_local=None, expert_base=0):
@@ -274,7 +293,7 @@ def run_decode(args):
     H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
     inp = make_inputs(dict(synth.CONFIGS[2]), 512, 0, dev)
     eg, eu, ed = inp["w"]
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     pk, pk_src = peaks()
 
     def measure(ids):
@@ -460,7 +479,7 @@ def run_decode(args):
             "warmup": args.warmup, "ms_per_step": main_pt["ms"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "config3_decode_batching", "B": 256, "H": H, "D": cfg["D"], "E": E, "d": d,
-                       "k": k, "assignments": "Zipf(s=1) over experts", "l2": "flushed between timed steps"},
+                       "k": k, "assignments": "Zipf(s=1) over experts", "l2": L2Flush.NOTE},
             "roofline": {"bound": "hbm", "kernel": "expert FFN (ffn_layer2_kernel, one launch per step)",
                          "achieved": ffn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ffn_gbs / pk["hbm_gbs"],
                          "traffic": _traffic("decode_expert_ffn_bytes_per_launch"),
@@ -520,7 +539,7 @@ def run_tiny(args):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         fn()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     ms = []
     with Clocks(0) as clk:
         for _ in range(args.steps):
@@ -536,7 +555,7 @@ def run_tiny(args):
             "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config1_tiny", "T": T, "H": H, "E": E, "d": d, "k": k,
-                       "note": "latency-bound (12.6 MFLOP); graph replay", "l2": "flushed between steps"},
+                       "note": "latency-bound (12.6 MFLOP); graph replay", "l2": L2Flush.NOTE},
             "latency_us": t * 1e3, "gpu_launches": 4 * args.steps,  # route, dispatch, fp32 gate/up, fp32 down
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
@@ -562,7 +581,7 @@ def run_stack(args):
     x = torch.empty_like(x0)
     plan = rd.new_plan(T, E, k, dev)
     ws = torch.empty(rd.moe_stack_workspace_bytes(T, H, E, d, k, torch.bfloat16), dtype=torch.uint8, device=dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
 
     def step():
         x.copy_(x0)
@@ -642,7 +661,7 @@ def run_stack(args):
             "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "config4_stack32", "T": T, "L": L, "H": H, "E": E, "d": d, "k": k,
-                       "routing": "Markov locality p=0.672, routed once per step", "l2": "flushed between steps"},
+                       "routing": "Markov locality p=0.672, routed once per step", "l2": L2Flush.NOTE},
             "layer_tokens_per_s": T * L / (t * 1e-3),
             "router": {"ms": router_ms, "share_of_step_with_router": router_ms / (router_ms + t),
                        "note": "readme_router_forward over the same T tokens (4096-token sequences), run once per "
@@ -664,8 +683,8 @@ def run_offload(args):
     batches (T tokens each, u experts per batch as expert-aware batching yields them) runs through the L
     layers; the makespan of the queue is timed with CUDA events for fine-grained prefetching (next step's
     experts load on a separate stream while this step computes) vs on-demand loading, under the
-    Belady-inspired and LRU caches. Plus the paper's cache-hit table setup (Table tab:cache-hit): n_req
-    concurrent decode requests sharing one expert cache of k = 2..5 slots (per layer), Markov locality p=0.672."""
+    Belady-inspired and LRU caches. (The paper's cache-hit table, tab:cache-hit, needs its Chatbot-Arena trace:
+    out of scope.)"""
     import torch
 
     import synth
@@ -690,7 +709,7 @@ def run_offload(args):
         lgs.append(torch.from_numpy(synth.logits_for_assignments(ids, E, seed=seed + 200 + b)).to(dev))
         x0s.append(synth.to_torch(synth.tokens(T, H, seed=seed + 300 + b), "bf16").to(dev))
         touched.append(sorted(set(ids.tolist())))
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     expert_bytes = 3 * d * H * 2
     runs = []
     with Clocks(0) as clk:
@@ -751,21 +770,6 @@ def run_offload(args):
         if it >= 2:
             h2d.append(a.elapsed_time(b))
     h2d_GBps = expert_bytes / (float(np.median(h2d)) * 1e-3) / 1e9
-    # Table tab:cache-hit setup: n_req concurrent decode requests share one (per-layer) expert cache
-    n_req, n_tok = 8, 512
-    chains = synth.assignments_markov(n_req, n_tok, E, 0.672, seed=seed + 500).reshape(n_req, n_tok)
-    trace = chains.T.reshape(-1).astype(np.int64)  # decode step by step, request by request
-    table = {}
-    for k in (2, 3, 4, 5):
-        row = {}
-        for policy in ("random", "lru", "belady"):
-            c = rd.ExpertCache(k, policy, seed=1)
-            c.set_future(trace, np.arange(trace.size))
-            for t, key in enumerate(trace.tolist()):
-                c.access(key, t)
-            h, m = c.stats()
-            row[policy] = h / (h + m)
-        table[str(k)] = row
     best = max((r for r in runs if r["prefetch"]), key=lambda r: r["tokens_per_s"])
     line = {"metric": "memory-constrained MoE stack tokens/s (experts in host memory, NEXT-4)",
             "value": best["tokens_per_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -774,11 +778,8 @@ def run_offload(args):
             "config": {"workload": "config4_offload", "Q_batches": Q, "T": T, "L": L, "H": H, "E": E, "d": d,
                        "experts_per_batch": u, "host_expert_bytes": L * E * expert_bytes,
                        "routing": "expert-aware batches (u experts each), routed once per batch",
-                       "l2": "flushed between steps"},
+                       "l2": L2Flush.NOTE},
             "runs": runs, "resident_ms": resident_ms, "h2d_expert_GBps": h2d_GBps,
-            "cache_hit_table": {"setup": f"{n_req} concurrent decode requests x {n_tok} tokens, Markov p=0.672, "
-                                         f"E={E}, one layer's cache of k slots (PAPER.md Table tab:cache-hit)",
-                                "hit_ratio": table},
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
@@ -823,7 +824,7 @@ def main():
     T = args.tokens or (cfg["T"] if world == 1 else cfg["T"] // world)
     H, d, E, k = cfg["H"], cfg["d"], cfg["E"], cfg["k"]
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # 2x L2
+    flush = L2Flush(dev)
 
     def timed(fn, n):
         """n steps, L2 flushed before each (outside the events), CUDA events on the launching stream."""
@@ -978,7 +979,7 @@ def main():
                                                  "and the down-GEMM epilogue" if ep_mode == "peer" else
                                                  "NCCL all_to_all_single"}),
                        **({"ep_fallback": ep_fallback} if ep_fallback else {}),
-                       "l2": "flushed between timed steps (256 MiB write)"}}
+                       "l2": L2Flush.NOTE}}
     if world == 1:
         med = lambda a: float(np.median(a))
         line["step_mode"] = "cuda_graph_replay" if not args.eager else "eager"
@@ -1194,7 +1195,7 @@ def main():
         dist.all_reduce(nt, op=dist.ReduceOp.MAX)
         n_per = float(nt.item()) / args.steps
         line["nccl_exchange"] = {"value": T * world / (n_per * 1e-3), "unit": UNIT, "ms_per_step": n_per,
-                                 "vs_fused": ms_per_step / n_per,
+                                 "vs_fused": ms_per_step / n_per, "backend": dist.get_backend(),
                                  "mode": "NCCL all_to_all_single between the library's dispatch / grouped FFN / "
                                          "combine kernels, one count exchange per step, eager"}
         del nl

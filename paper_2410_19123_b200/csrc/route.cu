@@ -143,7 +143,7 @@ __device__ __forceinline__ void topk_select(float (&v)[NE], int E, int k, int32_
     }
     taken |= 1u << bid;
     if (j == 0) m = bv;
-    const float ej = expf(bv - m);
+    const float ej = isfinite(m) ? expf(bv - m) : (bv == m ? 1.0f : 0.0f);  // +-inf max: uniform over the tied maxima
     z += ej;
     idx_out[j] = bid;
     if (k > 1) w_out[j] = ej;  // normalised below
@@ -245,7 +245,7 @@ route_tile_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k, in
       }
       if (bid % lpt == gl) taken |= 1u << (bid / lpt);
       if (j == 0) m = bv;
-      const float ej = expf(bv - m);
+      const float ej = isfinite(m) ? expf(bv - m) : (bv == m ? 1.0f : 0.0f);  // +-inf max: uniform over the tied maxima
       z += ej;
       if (gl == 0 && tok_ok) {
         const int64_t s = (t0 + tok) * k + j;
@@ -517,7 +517,7 @@ route_cluster_kernel(const LogitT* __restrict__ logits, int64_t T, int E, int k,
         }
         if (bid % lpt == gl) taken |= 1u << (bid / lpt);
         if (j == 0) m = bv;
-        const float ej = expf(bv - m);
+        const float ej = isfinite(m) ? expf(bv - m) : (bv == m ? 1.0f : 0.0f);  // +-inf max: uniform over the tied maxima
         z += ej;
         if (gl == 0 && tok_ok) {
           const int64_t s = (t0 + tok) * k + j;

@@ -1,6 +1,7 @@
 """readme_dispatch alone (scatter form; LAB_OP=combine: readme_combine, k = 1 gather) at T rows x H = 4096
-bf16 under env variants (e.g. README_DISPATCH_BULK=0,1), CUDA-graph replays, L2 flushed before each;
-GB/s = 2 * rows * H * 2 / time. Measurement only. Usage: python scripts/dispatch_lab.py VAR=a,b [T1 T2 ...]"""
+bf16 under library knob variants (readme_debug_set_knob, e.g. dispatch_bulk=0,1), CUDA-graph replays, L2
+flushed before each; GB/s = 2 * rows * H * 2 / time. Measurement only.
+Usage: python scripts/dispatch_lab.py KNOB=a,b [T1 T2 ...]"""
 import json
 import os
 import sys
@@ -23,7 +24,7 @@ for T in Ts:
     xs = torch.empty_like(x)
     ref = None
     for v in vals:
-        os.environ[var] = v
+        rd.set_knob(var, int(v))
         if os.environ.get("LAB_OP") == "combine":
             fn = lambda: rd.combine(x, plan.dest, None, 1, out=xs)
         else:

@@ -21,6 +21,7 @@ wg = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wu = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wd = (torch.randn(E, H, d, device="cuda", generator=g) / 74).bfloat16()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_r = torch.zeros(64 << 20, dtype=torch.int32, device="cuda")  # read after the write: no dirty lines left
 res = {}
 for T in Ts:
     x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
@@ -45,6 +46,7 @@ for T in Ts:
     for _ in range(15):
         for v in vals:
             flush.zero_()
+            flush_r.sum()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             graphs[v].replay()

@@ -132,15 +132,26 @@ def test_route_T0(rd):
     assert plan.counts.tolist() == [0] * 8 and plan.offsets.tolist() == [0] * 9
 
 
-def test_route_nonfinite_flag(rd):
-    lg = synth.router_logits(600, 8)
+@pytest.mark.parametrize("E,impl", [(8, "cluster"), (8, "lookback"), (40, "cluster"), (40, "lookback")])
+def test_route_nonfinite_flag(rd, knob, E, impl):
+    """Q3: non-finite logits are flagged; ids stay in range and the k > 1 weights stay finite and sum to 1 even
+    for a +inf maximum (uniform over the tied +inf entries) or an all -inf row (uniform over the selection)."""
+    knob("route", ROUTE_IMPL[impl])
+    lg = synth.router_logits(600, E)
     lg[17, 3] = np.nan
     lg[400, 0] = np.inf
+    lg[401, 1] = lg[401, 5] = np.inf
+    lg[402, :] = -np.inf
     plan = rd.route(torch.from_numpy(lg).to(DEV), 2)
     torch.cuda.synchronize()
     assert int(plan.dev_status.item()) & rd.README_DEV_NONFINITE_LOGIT
+    w = _np(plan.topk_w)
     idx = _np(plan.topk_idx)
-    assert idx.min() >= 0 and idx.max() < 8
+    assert np.all(np.isfinite(w)) and np.allclose(w.sum(axis=1), 1.0, atol=1e-6)
+    assert idx.min() >= 0 and idx.max() < E
+    assert idx[400, 0] == 0 and w[400].tolist() == [1.0, 0.0]
+    assert idx[401].tolist() == [1, 5] and w[401].tolist() == [0.5, 0.5]
+    assert w[402].tolist() == [0.5, 0.5]
     # permutation still valid
     assert np.array_equal(np.sort(_np(plan.dest)), np.arange(1200))
 
