@@ -295,6 +295,7 @@ def run_decode(args):
     eg, eu, ed = inp["w"]
     flush = L2Flush(dev)
     pk, pk_src = peaks()
+    dev_flags = []  # dev_status of every timed decode step shape (all must be 0)
 
     def measure(ids):
         B = ids.shape[0]
@@ -328,6 +329,10 @@ def run_decode(args):
         U = int(len(np.unique(ids)))
         byts = U * 3.0 * H * d * 2 + 4.0 * B * H * 2
         t = float(np.mean(ms))
+        st_word = int(plan.dev_status.item())
+        dev_flags.append(st_word)
+        if st_word:
+            raise SystemExit(f"decode step B={B} set dev_status = {st_word:#x}: not reporting a number")
         return {"B": B, "unique_experts": U, "ms": t, "tokens_per_s": B / (t * 1e-3),
                 "GBps": byts / (t * 1e-3) / 1e9, "hbm_frac": byts / (t * 1e-3) / 1e9 / pk["hbm_gbs"]}
 
@@ -480,6 +485,7 @@ def run_decode(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "config3_decode_batching", "B": 256, "H": H, "D": cfg["D"], "E": E, "d": d,
                        "k": k, "assignments": "Zipf(s=1) over experts", "l2": L2Flush.NOTE},
+            "dev_status": max(dev_flags) if dev_flags else 0,
             "roofline": {"bound": "hbm", "kernel": "expert FFN (ffn_layer2_kernel, one launch per step)",
                          "achieved": ffn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ffn_gbs / pk["hbm_gbs"],
                          "traffic": _traffic("decode_expert_ffn_bytes_per_launch"),
