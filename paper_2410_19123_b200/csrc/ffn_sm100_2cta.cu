@@ -584,6 +584,78 @@ __device__ __forceinline__ void store_row_bf16x32(__nv_bfloat16* dst, const floa
   }
 }
 
+// Epilogue of one 128-lane accumulator slot of a non-swap tile (this warp's 32 rows): gate/up tiles store
+// h = silu(g) * u, down tiles store y (y_sorted, the fused combine y[src[r]] + residual, or the source rank's
+// row over peer memory). row_in_tile = this thread's row, ncols / acc_off = the accumulator columns it holds
+// (all 256 for M = 256, half for the M = 128 "2x2" layout). valid = the row exists and nothing aborted.
+template <int kFuse>
+__device__ __forceinline__ void drain_acc(const LayerArgs& la, const LTile& tl, uint32_t tacc, int row_in_tile,
+                                          int ncols, int acc_off, bool valid) {
+  const int H = la.H, d = la.d;
+  const int64_t r = tl.m0 + row_in_tile;
+  if (tl.mode == 0) {
+    // windows of 128 columns: [gate 64 | up 64] of h columns n0 + (window) * 64 + [0, 64)
+    __nv_bfloat16* orow = la.h + r * d;
+    for (int w = 0; w < ncols / 128; ++w) {
+      const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
+      const int hcol0 = tl.n0 + (acc_off + w * 128) / 2;
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t gr[32], ur[32];
+        tc::tmem_ld32(wbase + c, gr);
+        tc::tmem_ld32(wbase + 64 + c, ur);
+        tc::tmem_wait_ld();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+        if (valid) store_row_bf16x32(orow + hcol0 + c, v, d - (hcol0 + c));
+      }
+    }
+  } else {
+    int64_t orow_idx = r;
+    bool valid_row = valid;
+    __nv_bfloat16* orow;
+    const __nv_bfloat16* rrow = nullptr;
+    if constexpr (kFuse == 2) {
+      const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
+      valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
+      const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
+      const int64_t ii = valid_row ? v - p * la.vrows : 0;
+      __nv_bfloat16* py = la.peer_y[0];
+      const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+      for (int j = 1; j < kMaxPeers; ++j)
+        if (p == j) {
+          py = la.peer_y[j];
+          pr = la.peer_res[j];
+        }
+      orow = py + ii * H;
+      rrow = pr ? pr + ii * H : nullptr;
+    } else {
+      if constexpr (kFuse == 1) {
+        orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
+        valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
+      }
+      orow = la.y + orow_idx * H;
+      rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
+    }
+#pragma unroll 1
+    for (int c = 0; c < ncols; c += 32) {
+      const int col = tl.n0 + acc_off + c;
+      uint32_t vr[32];
+      tc::tmem_ld32(tacc + static_cast<uint32_t>(c), vr);
+      tc::tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+      if (valid_row) {
+        if (rrow) add_bf16x32(rrow + col, v, H - col);
+        store_row_bf16x32(orow + col, v, H - col);
+      }
+    }
+  }
+}
+
 template <int kFuse, int kMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
@@ -859,71 +931,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         ncols = kN / 2;
         acc_off = (q >> 1) * (kN / 2);
       }
-      const bool valid = row_in_tile < tl.rows && !aborted;
-      const int64_t r = tl.m0 + row_in_tile;
-      if (tl.swap) {
-        swap_epilogue<kFuse>(la, tl, tacc, cta, q, lane, !aborted);
-      } else if (tl.mode == 0) {
-        // windows of 128 columns: [gate 64 | up 64] of h columns n0 + (window) * 64 + [0, 64)
-        __nv_bfloat16* orow = la.h + r * d;
-        for (int w = 0; w < ncols / 128; ++w) {
-          const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
-          const int hcol0 = tl.n0 + (acc_off + w * 128) / 2;
-#pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
-            uint32_t gr[32], ur[32];
-            tc::tmem_ld32(wbase + c, gr);
-            tc::tmem_ld32(wbase + 64 + c, ur);
-            tc::tmem_wait_ld();
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
-            if (valid) store_row_bf16x32(orow + hcol0 + c, v, d - (hcol0 + c));
-          }
-        }
-      } else {
-        int64_t orow_idx = r;
-        bool valid_row = valid;
-        __nv_bfloat16* orow;
-        const __nv_bfloat16* rrow = nullptr;
-        if constexpr (kFuse == 2) {
-          const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
-          valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
-          const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
-          const int64_t ii = valid_row ? v - p * la.vrows : 0;
-          __nv_bfloat16* py = la.peer_y[0];
-          const __nv_bfloat16* pr = la.peer_res[0];
-#pragma unroll
-          for (int j = 1; j < kMaxPeers; ++j)
-            if (p == j) {
-              py = la.peer_y[j];
-              pr = la.peer_res[j];
-            }
-          orow = py + ii * H;
-          rrow = pr ? pr + ii * H : nullptr;
-        } else {
-          if constexpr (kFuse == 1) {
-            orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
-            valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
-          }
-          orow = la.y + orow_idx * H;
-          rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
-        }
-#pragma unroll 1
-        for (int c = 0; c < ncols; c += 32) {
-          const int col = tl.n0 + acc_off + c;
-          uint32_t vr[32];
-          tc::tmem_ld32(tacc + static_cast<uint32_t>(c), vr);
-          tc::tmem_wait_ld();
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-          if (valid_row) {
-            if (rrow) add_bf16x32(rrow + col, v, H - col);
-            store_row_bf16x32(orow + col, v, H - col);
-          }
-        }
-      }
+      if (tl.swap) swap_epilogue<kFuse>(la, tl, tacc, cta, q, lane, !aborted);
+      else drain_acc<kFuse>(la, tl, tacc, row_in_tile, ncols, acc_off, row_in_tile < tl.rows && !aborted);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -79,12 +79,12 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-// Non-blocking probe of a phase (cluster-scope acquire on success).
+// Non-blocking probe of a phase (CTA-scope acquire on success, as mbar_wait_cluster).
 __device__ __forceinline__ bool mbar_test_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(done)
       : "r"(smem_u32(bar)), "r"(parity)
