@@ -60,3 +60,25 @@ def test_bench_default_json_line_gpu():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["gpu_launches"] >= 3 * d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["dev_status"] == 0 and d["timed_output_check"]["ok"] is True
+    assert d["cpu_baseline"]["cpu_model"]
+
+
+@pytest.mark.gpu
+def test_bench_n2_line_on_one_gpu():
+    """The N > 1 path as the driver launches it (torchrun, 2 ranks), here sharing one GPU over gloo
+    (README_BENCH_BACKEND=gloo; numbers meaningless, a functional check): config 5's strong-scaling line with
+    65536 tokens in all, the fused peer-memory exchange, and the NCCL-exchange record beside it; one line."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29733", README_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29733", "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--no-e2e"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = _json_lines(p.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["workload"] == "config5_expert_parallel" and d["config"]["T_total"] == 65536
+    assert d["config"]["T_per_gpu"] == 32768 and "peer-memory" in d["config"]["ep_exchange"]
+    assert d["nccl_exchange"]["value"] > 0
