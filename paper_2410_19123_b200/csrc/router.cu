@@ -13,8 +13,11 @@
 // projections are dense contractions and run on the tcgen05 CTA-pair GEMM kernels of ffn_sm100_2cta.cu.
 #include <math.h>
 
+#include <mutex>
+
 #include "kernels.h"
 #include "router_head.cuh"
+#include "tc_common.cuh"
 
 namespace readme {
 
@@ -107,25 +110,6 @@ __global__ void router_head_kernel(const __nv_bfloat16* __restrict__ h2, int64_t
                    [&](int n, float v) { logits[t * N + n] = v; });
 }
 
-// Causal attention with RoPE on the tensor cores (mma.sync m16n8k16 bf16 -> fp32), flash-attention style:
-// one CTA (4 warps) per (sequence, head, 64-query tile); each warp owns 16 query rows, keeps Q as A
-// fragments, streams 64-key tiles (K with RoPE, V transposed) through shared memory, keeps S = Q K^T and
-// O in registers with an online softmax. ~17 GFLOP per 4096-token request (off the hot path).
-// qkv [T, 1536] bf16 (q | k | v, head h = columns h*128..), out [T, 512] bf16.
-constexpr int kQT = 64, kKT = 64;
-constexpr int kKS = kHd + 8;   // K smem row stride (bf16): conflict-free B-fragment loads
-constexpr int kVS = kKT + 8;   // V^T smem row stride (bf16)
-
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) { return pack_bf16x2(lo, hi); }
-
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
 // RoPE applied once per token, in place on the q and k parts of qkv (positions restart per sequence).
 // One warp per token; lane i handles angle pairs i and i + 32 (of 64) for all 4 heads of q and k.
 __global__ void router_rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t T, const int32_t* __restrict__ seq_starts,
@@ -159,163 +143,222 @@ __global__ void router_rope_kernel(__nv_bfloat16* __restrict__ qkv, int64_t T, c
   }
 }
 
-__global__ void __launch_bounds__(128)
-router_attention_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ seq_starts,
-                        const int32_t* __restrict__ tile_seq, const int32_t* __restrict__ tile_q0,
-                        const int32_t* __restrict__ ntiles, __nv_bfloat16* __restrict__ out) {
-  __shared__ __align__(16) __nv_bfloat16 sK[kKT * kKS];      // [key][dim] (also stages Q first)
-  __shared__ __align__(16) __nv_bfloat16 sVt[kHd * kVS];     // [dim][key]
+// ---- causal attention on tcgen05 / TMEM (the prefill path) ----------------------------------------------
+// One CTA (4 warps) per (128-query tile of a sequence, head). Q, K and V tiles come in with TMA (128-byte
+// swizzle, two 64-dim boxes per 128-row tile); per 128-key block: S = Q K^T on the tensor core into TMEM
+// (M = 128 queries, N = 128 keys, K = 128 dims); each thread owns one query row (its TMEM lane): causal mask,
+// online softmax in base 2, P (bf16) written to shared memory in the swizzled K-major layout; O_b = P V on
+// the tensor core into a second TMEM region (V is the MN-major B operand: its tile is used exactly as TMA
+// wrote it); the thread folds O_b into its fp32 row accumulator in registers with the softmax rescale. K/V
+// blocks are double-buffered (the next block's TMA runs under this block's work).
+constexpr int kAQ = 128;                 // queries per CTA
+constexpr int kAK = 128;                 // keys per block
+constexpr int kABox = 128 * 128;         // one 128-row x 64-dim swizzled box: 16 KB
+
+struct __align__(1024) AttnSmem {
+  uint8_t q[2][kABox];        // Q tile: dims [0,64) | [64,128)
+  uint8_t k[2][2][kABox];     // [slot][dim half]
+  uint8_t v[2][2][kABox];
+  uint8_t p[2][kABox];        // P tile: keys [0,64) | [64,128), rows = queries, K-major
+  uint64_t qbar, kvbar[2], sbar, pvbar;
+  uint32_t tmem_base;
+};
+constexpr size_t kAttnSmem = sizeof(AttnSmem) + 1024;
+static_assert(kAttnSmem <= 232448, "attention shared memory");
+
+// SW128 K-major descriptor as in tc_common.cuh, and the MN-major form for V: 64-element (128 B) rows along
+// N (dims), 8-row groups along K (keys) 1024 B apart (SBO), the second 64-dim half 16 KB away (LBO).
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(128, 1)
+router_attention_tc_kernel(const __grid_constant__ CUtensorMap tmQKV, const int32_t* __restrict__ seq_starts,
+                           const int32_t* __restrict__ tile_seq, const int32_t* __restrict__ tile_q0,
+                           const int32_t* __restrict__ ntiles, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t attn_raw[];
+  AttnSmem& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(attn_raw) + 1023) & ~uintptr_t(1023));
   const int tile = blockIdx.x, head = blockIdx.y;
   if (tile >= *ntiles) return;
   const int seq = tile_seq[tile];
   const int s0 = seq_starts[seq], s1 = seq_starts[seq + 1];
   const int q0 = tile_q0[tile];
-  const int nq = min(kQT, s1 - q0);
+  const int q_last = min(q0 + kAQ, s1) - 1;
+  const int nblk = (q_last - s0) / kAK + 1;  // key blocks [s0 + b*128, ...) up to the last query
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
-  const int ld = 3 * kD;
-  const float scale_log2 = rsqrtf(static_cast<float>(kHd)) * 1.4426950408889634f;  // softmax in base 2
+  const int qcol = head * kHd, kcol = kD + head * kHd, vcol = 2 * kD + head * kHd;
 
-  // ---- Q tile (RoPE already applied) -> smem -> A fragments (16 rows per warp, 8 k-chunks of 16 dims) ----
-  for (int i = tid; i < kQT * (kHd / 8); i += blockDim.x) {
-    const int rr = i / (kHd / 8), c8 = (i % (kHd / 8)) * 8;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (rr < nq) v = *reinterpret_cast<const uint4*>(&qkv[static_cast<int64_t>(q0 + rr) * ld + head * kHd + c8]);
-    *reinterpret_cast<uint4*>(&sK[rr * kKS + c8]) = v;
+  if (tid == 0) {
+    tc::prefetch_tmap(&tmQKV);
+    tc::mbar_init(&s.qbar, 1);
+    tc::mbar_init(&s.kvbar[0], 1);
+    tc::mbar_init(&s.kvbar[1], 1);
+    tc::mbar_init(&s.sbar, 1);
+    tc::mbar_init(&s.pvbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (warp == 0) tc::tmem_alloc<1>(&s.tmem_base, 256);
+  tc::fence_before();
   __syncthreads();
-  const int r_lo = warp * 16 + lane / 4;  // this thread's two rows: r_lo and r_lo + 8
-  const int cq = (lane % 4) * 2;
-  uint32_t qa[8][4];
-#pragma unroll
-  for (int kc = 0; kc < 8; ++kc) {
-    const int c = kc * 16 + cq;
-    qa[kc][0] = *reinterpret_cast<const uint32_t*>(&sK[r_lo * kKS + c]);
-    qa[kc][1] = *reinterpret_cast<const uint32_t*>(&sK[(r_lo + 8) * kKS + c]);
-    qa[kc][2] = *reinterpret_cast<const uint32_t*>(&sK[r_lo * kKS + c + 8]);
-    qa[kc][3] = *reinterpret_cast<const uint32_t*>(&sK[(r_lo + 8) * kKS + c + 8]);
+  tc::fence_after();
+  const uint32_t tmem = s.tmem_base;
+  auto load_kv = [&](int b) {  // thread 0: key block b into slot b & 1
+    const int sl = b & 1, k0 = s0 + b * kAK;
+    tc::mbar_expect_tx(&s.kvbar[sl], 4u * kABox);
+    tc::tma_load_2d(&tmQKV, s.k[sl][0], &s.kvbar[sl], kcol, k0);
+    tc::tma_load_2d(&tmQKV, s.k[sl][1], &s.kvbar[sl], kcol + 64, k0);
+    tc::tma_load_2d(&tmQKV, s.v[sl][0], &s.kvbar[sl], vcol, k0);
+    tc::tma_load_2d(&tmQKV, s.v[sl][1], &s.kvbar[sl], vcol + 64, k0);
+  };
+  if (tid == 0) {
+    tc::mbar_expect_tx(&s.qbar, 2u * kABox);
+    tc::tma_load_2d(&tmQKV, s.q[0], &s.qbar, qcol, q0);
+    tc::tma_load_2d(&tmQKV, s.q[1], &s.qbar, qcol + 64, q0);
+    load_kv(0);
+    if (nblk > 1) load_kv(1);
   }
-  float o[16][4];
-#pragma unroll
-  for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows r_lo, r_lo + 8
-  const int qrow0 = q0 + r_lo, qrow1 = qrow0 + 8;
+  constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128);
+  constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128) | (1u << 16);  // B (V) MN-major
+  const float scale_log2 = rsqrtf(static_cast<float>(kHd)) * 1.4426950408889634f;
+  const int qrow = q0 + warp * 32 + lane;  // this thread's query (TMEM lane 32 * warp + lane)
+  const uint32_t t_s = tmem + (static_cast<uint32_t>(warp * 32) << 16), t_o = t_s + 128u;
+  // O accumulates in TMEM columns [128, 256) across the key blocks (PV MMAs with accumulate); the row's
+  // exponent base m only moves when a block's max exceeds it by more than 2^8 (then O and l are rescaled in
+  // place), so most blocks need no O round trip (values stay within 2^8 of 1: exact enough in fp32 / bf16)
+  float m = -INFINITY, l = 0.f;
 
-  const int q_last = q0 + nq - 1;
-  for (int k0 = s0; k0 <= q_last; k0 += kKT) {
-    const int nk = min(kKT, s1 - k0);
-    __syncthreads();  // previous tile's smem reads are done
-    for (int i = tid; i < kKT * (kHd / 8); i += blockDim.x) {
-      const int kk = i / (kHd / 8), c8 = (i % (kHd / 8)) * 8;
-      uint4 kv4 = make_uint4(0u, 0u, 0u, 0u), vv4 = make_uint4(0u, 0u, 0u, 0u);
-      if (kk < nk) {
-        const int64_t row = k0 + kk;
-        kv4 = *reinterpret_cast<const uint4*>(&qkv[row * ld + kD + head * kHd + c8]);
-        vv4 = *reinterpret_cast<const uint4*>(&qkv[row * ld + 2 * kD + head * kHd + c8]);
-      }
-      *reinterpret_cast<uint4*>(&sK[kk * kKS + c8]) = kv4;
-      const __nv_bfloat16* vv = reinterpret_cast<const __nv_bfloat16*>(&vv4);
+  for (int b = 0; b < nblk; ++b) {
+    const int sl = b & 1, k0 = s0 + b * kAK;
+    if (tid == 0) {
+      if (b == 0) tc::mbar_wait(&s.qbar, 0);
+      tc::mbar_wait(&s.kvbar[sl], static_cast<uint32_t>(b >> 1) & 1u);
+      tc::fence_after();
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sVt[(c8 + j) * kVS + kk] = vv[j];
+      for (int kk = 0; kk < kHd / 16; ++kk) {  // S = Q K^T over the 128 dims (two 64-dim swizzled halves)
+        const uint64_t ad = tc::sdesc_sw128(tc::smem_u32(s.q[kk >> 2])) + static_cast<uint64_t>((kk & 3) * 2);
+        const uint64_t bd = tc::sdesc_sw128(tc::smem_u32(s.k[sl][kk >> 2])) + static_cast<uint64_t>((kk & 3) * 2);
+        tc::mma_f16<1>(tmem, ad, bd, idesc_s, kk != 0 ? 1u : 0u);
+      }
+      tc::commit(&s.sbar);
     }
+    __syncwarp();
+    tc::mbar_wait(&s.sbar, static_cast<uint32_t>(b) & 1u);
+    tc::fence_after();
+    // ---- this thread's query row over the block's 128 keys: masked max, then p = 2^(s - m) into P ----
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kAK; c += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(t_s + static_cast<uint32_t>(c), r);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int key = k0 + c + j;
+        if (key <= qrow && key < s1) mx = fmaxf(mx, __uint_as_float(r[j]) * scale_log2);
+      }
+    }
+    // move the base when the block's max exceeds it by more than 2^8 (also the row's first finite max);
+    // O is rescaled in TMEM by the warp (tcgen05.ld/st are warp-collective) when any lane's base moved
+    const bool up = mx > m + 8.f;
+    const float alpha = (up && m != -INFINITY) ? exp2f(m - mx) : 1.f;
+    if (up) {
+      l *= alpha;
+      m = mx;
+    }
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+      for (int c = 0; c < kHd; c += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(t_o + static_cast<uint32_t>(c), r);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+        tc::tmem_st32(t_o + static_cast<uint32_t>(c), r);
+      }
+      tc::tmem_wait_st();
+    }
+    float ps = 0.f;
+#pragma unroll
+    for (int c = 0; c < kAK; c += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(t_s + static_cast<uint32_t>(c), r);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int c8 = 0; c8 < 32; c8 += 8) {
+        float pf[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int key = k0 + c + c8 + j;
+          pf[j] = (key <= qrow && key < s1) ? exp2f(__uint_as_float(r[c8 + j]) * scale_log2 - m) : 0.f;
+          ps += pf[j];
+        }
+        uint4 w;
+        w.x = pack_bf16x2(pf[0], pf[1]);
+        w.y = pack_bf16x2(pf[2], pf[3]);
+        w.z = pack_bf16x2(pf[4], pf[5]);
+        w.w = pack_bf16x2(pf[6], pf[7]);
+        const int row = warp * 32 + lane, kc = c + c8, chunk = (kc & 63) >> 3;  // 128-B swizzle
+        *reinterpret_cast<uint4*>(s.p[kc >> 6] + row * 128 + ((chunk ^ (row & 7)) << 4)) = w;
+      }
+    }
+    l += ps;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic stores) -> the tensor core
+    tc::fence_before();
     __syncthreads();
-    // S = Q K^T for this warp's 16 rows x 64 keys (8 n-chunks of 8 keys)
-    float sc[8][4];
+    tc::fence_after();
+    if (tid == 0) {
 #pragma unroll
-    for (int nc = 0; nc < 8; ++nc) {
-      sc[nc][0] = sc[nc][1] = sc[nc][2] = sc[nc][3] = 0.f;
-      const int key = nc * 8 + lane / 4;
-#pragma unroll
-      for (int kc = 0; kc < 8; ++kc) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[key * kKS + kc * 16 + cq]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sK[key * kKS + kc * 16 + cq + 8]);
-        mma_bf16(sc[nc], qa[kc], b0, b1);
+      for (int kk = 0; kk < kAK / 16; ++kk) {  // O += P V over the block's 128 keys
+        const uint64_t ad = tc::sdesc_sw128(tc::smem_u32(s.p[kk >> 2])) + static_cast<uint64_t>((kk & 3) * 2);
+        const uint64_t bd = sdesc_sw128_mn(tc::smem_u32(s.v[sl][0]) + static_cast<uint32_t>(kk * 16 * 128),
+                                           static_cast<uint32_t>(kABox));
+        tc::mma_f16<1>(tmem + 128u, ad, bd, idesc_pv, (b | kk) != 0 ? 1u : 0u);
       }
+      tc::commit(&s.pvbar);
     }
-    // causal mask + online softmax (rows r_lo / r_lo+8; this thread holds keys nc*8 + cq, +1)
-    float mx0 = -INFINITY, mx1 = -INFINITY;
+    __syncwarp();
+    tc::mbar_wait(&s.pvbar, static_cast<uint32_t>(b) & 1u);
+    tc::fence_after();
+    if (tid == 0 && b + 2 < nblk) load_kv(b + 2);  // the slot's K and V have been consumed
+  }
+  {  // the warp reads its rows' O (warp-collective), the rows of this tile's queries are stored
+    const bool store = qrow <= q_last;
+    const float il = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = out + static_cast<int64_t>(store ? qrow : 0) * kD + head * kHd;
 #pragma unroll
-    for (int nc = 0; nc < 8; ++nc) {
+    for (int c = 0; c < kHd; c += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(t_o + static_cast<uint32_t>(c), r);
+      tc::tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int key = k0 + nc * 8 + cq + j;
-        const bool kv = (nc * 8 + cq + j) < nk;
-        sc[nc][j] = (kv && key <= qrow0) ? sc[nc][j] * scale_log2 : -INFINITY;
-        sc[nc][2 + j] = (kv && key <= qrow1) ? sc[nc][2 + j] * scale_log2 : -INFINITY;
-        mx0 = fmaxf(mx0, sc[nc][j]);
-        mx1 = fmaxf(mx1, sc[nc][2 + j]);
-      }
-    }
-#pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-    }
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float c0 = (mn0 == -INFINITY) ? 1.f : exp2f(m0 - mn0);
-    const float c1 = (mn1 == -INFINITY) ? 1.f : exp2f(m1 - mn1);
-    float ps0 = 0.f, ps1 = 0.f;
-#pragma unroll
-    for (int nc = 0; nc < 8; ++nc) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        sc[nc][j] = (sc[nc][j] == -INFINITY) ? 0.f : exp2f(sc[nc][j] - mn0);
-        sc[nc][2 + j] = (sc[nc][2 + j] == -INFINITY) ? 0.f : exp2f(sc[nc][2 + j] - mn1);
-        ps0 += sc[nc][j];
-        ps1 += sc[nc][2 + j];
-      }
-    }
-#pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
-      ps0 += __shfl_xor_sync(0xffffffffu, ps0, off);
-      ps1 += __shfl_xor_sync(0xffffffffu, ps1, off);
-    }
-    l0 = l0 * c0 + ps0;
-    l1 = l1 * c1 + ps1;
-    m0 = mn0;
-    m1 = mn1;
-#pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      o[n][0] *= c0;
-      o[n][1] *= c0;
-      o[n][2] *= c1;
-      o[n][3] *= c1;
-    }
-    // O += P V: P (16 x 64 keys) as A fragments, V^T rows as B fragments (16 n-chunks of 8 dims)
-#pragma unroll
-    for (int kc = 0; kc < 4; ++kc) {
-      uint32_t pa[4];
-      pa[0] = pack2(sc[2 * kc][0], sc[2 * kc][1]);
-      pa[1] = pack2(sc[2 * kc][2], sc[2 * kc][3]);
-      pa[2] = pack2(sc[2 * kc + 1][0], sc[2 * kc + 1][1]);
-      pa[3] = pack2(sc[2 * kc + 1][2], sc[2 * kc + 1][3]);
-#pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        const int dim = n * 8 + lane / 4;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sVt[dim * kVS + kc * 16 + cq]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sVt[dim * kVS + kc * 16 + cq + 8]);
-        mma_bf16(o[n], pa, b0, b1);
+      for (int c8 = 0; c8 < 32; c8 += 8) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(r[c8 + 0]) * il, __uint_as_float(r[c8 + 1]) * il);
+        w.y = pack_bf16x2(__uint_as_float(r[c8 + 2]) * il, __uint_as_float(r[c8 + 3]) * il);
+        w.z = pack_bf16x2(__uint_as_float(r[c8 + 4]) * il, __uint_as_float(r[c8 + 5]) * il);
+        w.w = pack_bf16x2(__uint_as_float(r[c8 + 6]) * il, __uint_as_float(r[c8 + 7]) * il);
+        if (store) *reinterpret_cast<uint4*>(dst + c + c8) = w;
       }
     }
   }
-  // normalise and store rows r_lo, r_lo + 8 (columns n*8 + cq, +1)
-  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
-#pragma unroll
-  for (int n = 0; n < 16; ++n) {
-    const int col = head * kHd + n * 8 + cq;
-    if (r_lo < nq)
-      *reinterpret_cast<uint32_t*>(&out[static_cast<int64_t>(qrow0) * kD + col]) = pack2(o[n][0] * i0, o[n][1] * i0);
-    if (r_lo + 8 < nq)
-      *reinterpret_cast<uint32_t*>(&out[static_cast<int64_t>(qrow1) * kD + col]) = pack2(o[n][2] * i1, o[n][3] * i1);
-  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<1>(tmem, 256);
 }
 
-// Query-tile table: for each sequence, ceil(len/32) tiles (seq id, first row). Built on the device.
-__global__ void router_tiles_kernel(const int32_t* __restrict__ seq_starts, int nseq, int32_t* __restrict__ tile_seq,
-                                    int32_t* __restrict__ tile_q0, int32_t* __restrict__ ntiles_out) {
+// 128-query tile table for the tcgen05 attention (as router_tiles_kernel).
+__global__ void router_tiles128_kernel(const int32_t* __restrict__ seq_starts, int nseq, int32_t* __restrict__ tile_seq,
+                                       int32_t* __restrict__ tile_q0, int32_t* __restrict__ ntiles_out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int n = 0;
   for (int s = 0; s < nseq; ++s)
-    for (int q = seq_starts[s]; q < seq_starts[s + 1]; q += kQT) {
+    for (int q = seq_starts[s]; q < seq_starts[s + 1]; q += kAQ) {
       tile_seq[n] = s;
       tile_q0[n] = q;
       ++n;
@@ -530,7 +573,7 @@ readme_status router_tail(int64_t T, const RouterWeights& w, float eps, float* l
 
 size_t router_ws_bytes(int64_t T, int32_t nseq) {
   const size_t act = align_up(static_cast<size_t>(T) * kD * 2, 256);
-  const size_t tiles = align_up(static_cast<size_t>(T / kQT + nseq + 1) * sizeof(int32_t), 256);
+  const size_t tiles = align_up(static_cast<size_t>(T / kAQ + nseq + 1) * sizeof(int32_t), 256);
   return 256 + 8 * act + 2 * tiles + 256 + act + ffn_layer_ready_bytes(T, 1) + 256;
 }
 
@@ -549,7 +592,7 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
                                     uint32_t* dev_status, cudaStream_t st, const RoutePlanOut* plan) {
   if (T == 0) return README_OK;
   const size_t act = align_up(static_cast<size_t>(T) * kD * 2, 256);
-  const size_t tiles_b = align_up(static_cast<size_t>(T / kQT + nseq + 1) * sizeof(int32_t), 256);
+  const size_t tiles_b = align_up(static_cast<size_t>(T / kAQ + nseq + 1) * sizeof(int32_t), 256);
   char* p = static_cast<char*>(ws);
   int32_t* offs = reinterpret_cast<int32_t*>(p);
   p += 256;
@@ -575,12 +618,28 @@ readme_status launch_router_forward(const int32_t* ids, int64_t T, const int32_t
   README_TRY(launch_gemm_2cta(1, a, T, kD, 3 * kD, 1, 1, offs, w.wqkv, nullptr, qkv, nullptr, nullptr, st));
   router_rope_kernel<<<gblocks, 32 * wpb, 0, st>>>(qkv, T, seq_starts, nseq);
   README_CUDA(cudaGetLastError());
-  router_tiles_kernel<<<1, 1, 0, st>>>(seq_starts, nseq, tile_seq, tile_q0, ntiles);
-  README_CUDA(cudaGetLastError());
-  const int64_t max_tiles = T / kQT + nseq;
-  dim3 ag(static_cast<unsigned>(max_tiles), kHeads);
-  router_attention_kernel<<<ag, 128, 0, st>>>(qkv, seq_starts, tile_seq, tile_q0, ntiles, att);
-  README_CUDA(cudaGetLastError());
+  {
+    static std::once_flag once[64];
+    static cudaError_t attr_err[64];
+    int dev = 0;
+    README_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::call_once(once[dev], [&] {
+      attr_err[dev] = cudaFuncSetAttribute(router_attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kAttnSmem));
+    });
+    if (attr_err[dev] != cudaSuccess) return cuda_fail(attr_err[dev], "cudaFuncSetAttribute(router_attention_tc_kernel)");
+    CUtensorMap mq;
+    if (!tc::make_map_2d(&mq, qkv, 3 * kD, static_cast<uint64_t>(T), 64, 128)) {
+      set_error("cuTensorMapEncodeTiled failed for the router's qkv");
+      return README_ERR_CUDA;
+    }
+    router_tiles128_kernel<<<1, 1, 0, st>>>(seq_starts, nseq, tile_seq, tile_q0, ntiles);
+    README_CUDA(cudaGetLastError());
+    dim3 ag(static_cast<unsigned>(T / kAQ + nseq), kHeads);
+    router_attention_tc_kernel<<<ag, 128, kAttnSmem, st>>>(mq, seq_starts, tile_seq, tile_q0, ntiles, att);
+    README_CUDA(cudaGetLastError());
+  }
   return router_tail(T, w, eps, logits, offs, h0, a, att, h1, h2, hff, ready, dev_status, st, plan);
 }
 
@@ -594,7 +653,7 @@ readme_status launch_router_step(const int32_t* ids, int64_t n, const int32_t* s
                                  float eps, float* logits, void* ws, uint32_t* dev_status, cudaStream_t st) {
   if (n == 0) return README_OK;
   const size_t act = align_up(static_cast<size_t>(n) * kD * 2, 256);
-  const size_t tiles_b = align_up(static_cast<size_t>(n / kQT + 2) * sizeof(int32_t), 256);
+  const size_t tiles_b = align_up(static_cast<size_t>(n / kAQ + 2) * sizeof(int32_t), 256);
   char* p = static_cast<char*>(ws);
   int32_t* offs = reinterpret_cast<int32_t*>(p);
   p += 256;

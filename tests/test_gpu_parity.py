@@ -963,6 +963,24 @@ def test_router_forward_route_fused(rd, knob, k, impl):
     assert np.all(ref[np.arange(T), gpu_ids] >= top[:, -1] - 2.0 * tol)
 
 
+def test_router_long_sequence_tcgen05_attention(rd):
+    """The prefill attention on tcgen05/TMEM (128-query tiles, 128-key blocks, O accumulated in TMEM with the
+    base moved only by > 2^8): a 4096-token request (32 key blocks, the paper's sequence length) beside ragged
+    ones, every logit within the bf16 rule of the fp64 router oracle."""
+    from oracle import router
+    vocab, N = 32000, 8
+    W = {kk: synth.to_torch(v, "bf16") for kk, v in synth.router_weights(vocab=vocab, n_experts=N, seed=197).items()}
+    lens = [4096, 129, 1, 255]
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(starts[-1])
+    ids = synth.token_ids(T, vocab=vocab, seed=198)
+    lg = rd.router_forward(torch.from_numpy(ids).to(DEV), torch.from_numpy(starts).to(DEV),
+                           {kk: v.to(DEV) for kk, v in W.items()})
+    torch.cuda.synchronize()
+    ref = router.forward(ids, starts, W)
+    assert rel_err(_np(lg).astype(np.float64), ref) <= BF16_TOL
+
+
 def test_router_causal_on_gpu(rd):
     """Appending tokens to a sequence never changes the GPU logits of its prefix (bitwise: the kernels
     process each query row against keys <= it in a fixed order)."""
