@@ -91,7 +91,6 @@ struct Fuse {
   const int32_t* src;                 // [rows] expert-contiguous row -> token (= dest^-1, k == 1)
   int rows;                           // T
   const __nv_bfloat16* residual;      // [T, N] or null (GEMM2 scatter only)
-  int lab;                            // experiment knobs (README_LAB): bit0 skip output stores, bit1 N-fastest order
 };
 
 // Epilogue staging (per epilogue warp: 32 rows x 128 B; 16-byte chunks XOR-swizzled by row & 7 so the
@@ -197,7 +196,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint32_t phase = 0;
     int gcur = 0;
     for (int t = pair; t < ntiles; t += npairs) {
-      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, false);
       const int e = tl.g % E;
       const int a_rows = tl.m256 ? 128 : 64;
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
@@ -235,7 +234,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       uint32_t phase = 0;
       int gcur = 0, i = 0;
       for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
+        const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, false);
         const uint32_t idesc = tl.m256 ? idesc256 : idesc128;
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
@@ -269,7 +268,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int q = warp & 3;
     int gcur = 0, i = 0;
     for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, (fz.lab & 2) != 0);
+      const Tile tl = decode_tile(s, t, nseg, kBnOut, gcur, NT, false);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
@@ -287,7 +286,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         n_windows = 1;
         out_off = (q >> 1) * (kBnOut / 2);
       }
-      const bool valid = row_in_tile < tl.rows && !(fz.lab & 1);
+      const bool valid = row_in_tile < tl.rows;
       int64_t orow_idx = tl.m0 + row_in_tile;
       bool valid_row = valid;
       if constexpr (kMode == 1 && kFuse == 1) {  // k == 1: expert row r holds token src[r] (identity if null)
@@ -316,7 +315,7 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             stage_row_bf16x32(stg, lane, c / 8, v);
           }
           stage_flush(stg, lane, valid ? reinterpret_cast<uint64_t>(orow + hcol0) : 0ull, (N - hcol0) * 2,
-                      (fz.lab & 8) != 0);
+                      false);
         } else {
 #pragma unroll 1
           for (int c0 = 0; c0 < 128; c0 += 64) {
@@ -333,18 +332,15 @@ ffn_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               stage_row_bf16x32(stg, lane, c / 8, v);
             }
             stage_flush(stg, lane, valid_row ? reinterpret_cast<uint64_t>(orow + col0) : 0ull, (N - col0) * 2,
-                        (fz.lab & 8) != 0);
+                        false);
           }
         }
       }
       tc::fence_before();
       __syncwarp();
       // The MMA only needs this warp's TMEM reads finished (tcgen05.wait::ld + fence above), not its global
-      // stores, so the arrive is relaxed (lab bit 2 restores release semantics for A/B measurement).
-      if (lane == 0) {
-        if (fz.lab & 4) tc::mbar_arrive_cluster(&s.tempty[acc], 0);
-        else tc::mbar_arrive_cluster_relaxed(&s.tempty[acc], 0);
-      }
+      // stores, so the arrive is relaxed.
+      if (lane == 0) tc::mbar_arrive_cluster_relaxed(&s.tempty[acc], 0);
     }
   }
 
@@ -1036,7 +1032,7 @@ readme_status launch_gemm_2cta(int mode, const __nv_bfloat16* A, int64_t rows, i
   const int pairs = num_sms() / 2;  // no inter-CTA waits here: the grid need not be co-resident
   const int64_t tiles = mt_ub * ((N + (mode == 0 ? 127 : 255)) / (mode == 0 ? 128 : 256));
   const int grid = 2 * static_cast<int>(tiles < pairs ? tiles : pairs);
-  const Fuse fz{src, static_cast<int>(rows), residual, knob(Knob::kFfnLab)};
+  const Fuse fz{src, static_cast<int>(rows), residual};
   if (mode == 0)
     ffn_gemm2_kernel<0, 0><<<grid, kThreads, kSmemBytes, st>>>(mA, mB0, mB1, K, N, E, nseg, offsets, out, fz);
   else if (src == nullptr && residual == nullptr)
@@ -1134,7 +1130,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   la.dev_status = dev_status;
   const int spin = knob(Knob::kFfnSpin);
   la.spin_limit = spin <= 0 ? 1u : (spin >= 31 ? (1u << 31) : (1u << spin));
-  la.fz = Fuse{src, static_cast<int>(rows), residual, 0};
+  la.fz = Fuse{src, static_cast<int>(rows), residual};
   la.expert_slot = expert_slot;
   la.pdl = pdl ? (xready ? 2 : 1) : 0;
   la.xready = xready;

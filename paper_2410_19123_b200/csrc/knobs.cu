@@ -37,7 +37,6 @@ constexpr KnobDef kDefs[static_cast<int>(Knob::kCount)] = {
     {"ffn_pairs", "README_FFN_PAIRS", 0},          // 0 all co-resident pairs, else at most n CTA pairs
     {"ffn_askip", "README_FFN_ASKIP", 1},          // second CTA skips A loads of tiles with <= 64 rows
     {"ffn_order", "README_FFN_ORDER", 0},          // 1: gate/up tiles N-tile fastest
-    {"ffn_lab", "README_LAB", 0},                  // split-launch lab bits (0: none)
     {"ffn_swap", "README_FFN_SWAP", -1},           // -1 auto, else segment tails of <= n rows run swap-AB
     {"ffn_spin", "README_FFN_SPIN", 25},           // log2 of the readiness-poll limit (timeout -> dev_status)
 };
