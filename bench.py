@@ -225,6 +225,60 @@ def timed_output_check(y_dev, sample, yref, dev_status):
             "what": "y of the timed graph replays vs the fp64 oracle on the cpu_baseline sample tokens"}
 
 
+def ep_g1_record(cfg, T, dev, args, timed):
+    """Both expert-parallel paths at G = 1 (a one-rank NCCL group on this GPU, MASTER_ADDR 127.0.0.1)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_19123_b200 import ep
+    own = not dist.is_initialized()
+    if own:
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    out = {}
+    try:
+        layer, lg = ep.PeerEPLayer.from_config(cfg, T, dist.group.WORLD, dev)
+
+        def step():
+            layer.route(lg)
+            layer.layer(residual=True)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(args.warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        ms = float(np.mean(timed(g.replay, args.steps)))
+        out["peer_memory"] = {"ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3),
+                              "dev_status": int(layer.dev_status.item()), "mode": "cuda_graph_replay"}
+        layer.close()
+        del layer
+        torch.cuda.empty_cache()
+        nl = ep.EPMoELayer.from_config(cfg, T, dist.group.WORLD, dev)
+        for _ in range(args.warmup):
+            nl.step()
+        torch.cuda.synchronize()
+        ms = float(np.mean(timed(nl.step, args.steps)))
+        out["nccl"] = {"ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3), "mode": "eager (host split sizes)"}
+        del nl
+        torch.cuda.empty_cache()
+    finally:
+        if own:
+            dist.destroy_process_group()
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -1080,6 +1134,13 @@ def main():
                             "algorithmic": f"6*T_rank*k*H*d = {f_rank:.4g} FLOP per rank per step",
                             "peak_source": f"{pk_src} bf16 burst (MEASURED_PEAKS.json)"}
     line["clocks"] = clk.summary()
+
+    if world == 1 and args.config == 5 and not args.no_variants:
+        # config 5's expert-parallel machinery at G = 1 on this GPU (a one-rank process group): the fused
+        # peer-memory step (route + count publish + plan, dispatch with the all-to-all stores, the FFN whose down
+        # epilogue returns rows, three flag phases) and the NCCL all-to-all step, on the same 65536 tokens —
+        # the per-step cost of the EP machinery beside the plain layer above
+        line["ep_g1"] = ep_g1_record(cfg, T, dev, args, timed)
 
     if world == 1 and args.config == 2 and not args.no_variants:
         # SURVEY §8(d) config-2 variants: the d = D/8 = 1376 partition experts, Markov-locality routing
