@@ -28,4 +28,4 @@ cat $O/summary.txt
 # compute-sanitizer over the FFN, route and permutation tests (full-size cases excluded)
 run sanitize_mem 1500 compute-sanitizer --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "not full and not config and not starved and not offload and not stack"
 run sanitize_sync 1500 compute-sanitizer --tool synccheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "ffn_variants or tile_edges or teacher_forced"
-tail -3 $O/sanitize_mem.log $O/sanitize_sync.log
+tail -n 3 $O/sanitize_mem.log; tail -n 3 $O/sanitize_sync.log
