@@ -391,6 +391,13 @@ readme_status readme_debug_set_knob(const char* name, int32_t value);
 readme_status readme_debug_hold_sms(int32_t n_ctas, int64_t ns, readme_stream_t stream);
 readme_status readme_debug_get_knob(const char* name, int32_t* value);
 readme_status readme_debug_reset_knob(const char* name);
+/* Measurement only: register a device buffer of npairs * max_tiles * 8 uint64 into which the single-launch
+   expert FFN records, for the first max_tiles tiles of every CTA pair (record [pair][i][0..7]): 0 %globaltimer
+   when the MMA warp starts the tile, 1/2 its SM clock then and after issuing the tile's last MMA, 3/4 the
+   clock when the leader's first epilogue warp sees the accumulator full / has stored it, 5 %globaltimer at
+   that point, 6 the MMA warp's cycles waiting on loaded stages in the tile, 7 the tile index | (cycles the
+   MMA warp waited for a free accumulator) << 32. NULL (or max_tiles <= 0) stops it. */
+void readme_debug_tile_trace(void* dev_buf, int32_t max_tiles);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,8 @@ namespace {
 thread_local char g_err[512] = {0};
 }
 uint64_t* g_trace_buf = nullptr;
+uint64_t* g_tile_trace = nullptr;
+int32_t g_tile_trace_max = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -157,6 +159,12 @@ int readme_version(void) { return README_VERSION; }
 // [4] expert FFN last CTA end (max), [5] route start (min), [6] route end (max). The caller initialises
 // min slots to ~0 and max slots to 0. Not thread-safe; not for production use.
 void readme_debug_trace(void* dev_buf) { g_trace_buf = static_cast<uint64_t*>(dev_buf); }
+
+// Measurement only: per-tile records of the single-launch expert FFN (layout in include/readme.h).
+void readme_debug_tile_trace(void* dev_buf, int32_t max_tiles) {
+  g_tile_trace = max_tiles > 0 ? static_cast<uint64_t*>(dev_buf) : nullptr;
+  g_tile_trace_max = max_tiles > 0 ? max_tiles : 0;
+}
 
 // Measurement only: a one-thread kernel that stores %globaltimer into slot `slot` (8..15) of the registered
 // trace buffer, stream-ordered (marks where a timed region starts / ends on the device clock).

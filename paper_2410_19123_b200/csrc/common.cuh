@@ -86,6 +86,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // dispatch / route / expert FFN kernels record %globaltimer extremes into it (slot meanings in capi.cu).
 // Null by default: the kernels then skip it entirely.
 extern uint64_t* g_trace_buf;
+extern uint64_t* g_tile_trace;  // per-tile records of the single-launch FFN (readme_debug_tile_trace)
+extern int32_t g_tile_trace_max;
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

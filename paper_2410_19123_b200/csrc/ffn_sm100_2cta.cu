@@ -42,6 +42,7 @@ constexpr int kXokWords = 64;       // m-tiles whose x readiness is cached in sh
 // so the ring holds more stages (more weight bytes in flight per SM).
 constexpr int kStageAD = 64 * 128;
 constexpr int64_t kDecodeRows = 1024;  // launches up to this many rows use the 128-row m-tile variant
+constexpr int64_t kDynRows = 16384;    // 256-row m-tile launches up to this many rows: dynamic order, merged tails
 
 template <int S, int SA>
 struct __align__(8) SmemT {
@@ -388,16 +389,43 @@ struct LayerArgs {
             // dispatch is still writing later experts' rows (the wait moves to the kernel's end)
   const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
+  uint64_t* ttrace;        // measurement only (readme_debug_tile_trace): [pair][ttrace_max][8], normally null
+  int ttrace_max;
   int askip;               // tiles of <= 64 rows: the second CTA skips its A loads (knob ffn_askip)
   int order;               // lab: 1 = gate/up tiles N-tile fastest (knob ffn_order)
   int swap_rows;           // segment tails of <= swap_rows rows run as swap-AB tiles (knob ffn_swap; 0 = none)
+  int merge;               // 256-row m-tiles: segment tails ride on full m-tiles (knob ffn_merge; 0 = separate)
+  int dyn;                 // dynamic tile order: tiles after each pair's first claimed from tile_ctr (knob ffn_dyn)
+  uint32_t* tile_ctr;      // zeroed word of the readiness region (dyn)
+  int claim_ahead;         // dyn: K steps before the end of a tile's loads at which the next tile is claimed
 };
 
 struct LTile {
   int mode, g, mt, mid, m0, rows, n0;  // mid = global m-tile id (readiness counter index)
   bool m256;  // M = 256 pair MMA (each CTA 128 A rows), else M = 128 (64 rows per CTA)
   bool swap;  // swap-AB tail tile: weights are the MMA's M side, the tile's rows its N side
+  int tm0, trows;  // merged tail (256-row m-tiles): trows (<= 64) more rows from tm0, run swap-AB off this
+                   // tile's weight stages; 0 = none
 };
+
+constexpr int kTailMax = 64;  // rows of a merged segment tail (one swap-AB MMA of N <= 64 per K step)
+constexpr int kMaxTails = 2;  // merged tails per segment at most
+
+// m-tiles of a segment of R rows. With merging (256-row m-tiles): floor(R / 256) full m-tiles carry the
+// remainder as tails of <= 64 rows (one per full m-tile, at most kMaxTails) when it fits, else the remainder
+// is an m-tile of its own, as without merging. Every m-tile streams the expert's whole weight tile through its
+// SMs whatever its rows, so a separate tail tile cost as many SM cycles as a full one (~530 per K step); a
+// merged tail costs its swap-AB MMAs only, ~190 cycles per K step whatever its rows (4 MMAs re-reading the
+// 16 KB weight stage): worth it for one or two tails, not three (tile trace, profiles/SUMMARY.md r02).
+__device__ __forceinline__ bool seg_merges(int R) {
+  const int nf = R >> 8, rem = R & 255;
+  return rem > 0 && rem <= kTailMax * (nf < kMaxTails ? nf : kMaxTails);
+}
+template <int kMT>
+__device__ __forceinline__ int seg_mtiles(int R, bool merge) {
+  if (kMT == 256 && merge && seg_merges(R)) return R >> 8;
+  return (R + kMT - 1) / kMT;
+}
 
 constexpr int kBN1 = 128;  // h columns per gate/up tile ([gate 64 | up 64] rows per CTA)
 constexpr int kBN2 = 256;  // output columns per down tile (128 W_down rows per CTA)
@@ -417,7 +445,8 @@ struct Cursor {
 
 template <int kMT>
 __device__ __forceinline__ LTile decode_ltile(const int32_t* __restrict__ offs, int t, int nseg, int T1, int NT1,
-                                             int NT2, int swap_rows, Cursor& c, bool nfast = false) {
+                                             int NT2, int swap_rows, Cursor& c, bool nfast = false,
+                                             bool merge = false) {
   LTile tl;
   const int phase = t < T1 ? 0 : 1;
   const int NT = phase ? NT2 : NT1;
@@ -428,25 +457,36 @@ __device__ __forceinline__ LTile decode_ltile(const int32_t* __restrict__ offs, 
     c.mbase = 0;
   }
   int lo = __ldg(offs + c.g), hi = __ldg(offs + c.g + 1);
-  int mt_g = (hi - lo + kMT - 1) / kMT;
+  int mt_g = seg_mtiles<kMT>(hi - lo, merge);
   while (t >= c.start + mt_g * NT && c.g + 1 < nseg) {
     c.start += mt_g * NT;
     c.mbase += mt_g;
     ++c.g;
     lo = hi;
     hi = __ldg(offs + c.g + 1);
-    mt_g = (hi - lo + kMT - 1) / kMT;
+    mt_g = seg_mtiles<kMT>(hi - lo, merge);
   }
   const int local = t - c.start;
   // m-tile fastest (default) or, for gate/up tiles with nfast (lab knob ffn_order = 1), N-tile fastest
   const bool nf = nfast && phase == 0;
   const int nt = nf ? local % NT : local / mt_g, mt = nf ? local / NT : local % mt_g;
+  const int R = hi - lo;
   tl.mode = phase;
   tl.g = c.g;
   tl.mt = mt;
   tl.mid = c.mbase + mt;
   tl.m0 = lo + mt * kMT;
-  tl.rows = min(kMT, hi - lo - mt * kMT);
+  tl.rows = min(kMT, R - mt * kMT);
+  tl.tm0 = 0;
+  tl.trows = 0;
+  if (kMT == 256 && merge && seg_merges(R)) {
+    const int nfull = R >> 8, rem = R & 255;
+    if (mt < (rem + kTailMax - 1) / kTailMax) {
+      // chunk mt of the remainder rides on full m-tile mt
+      tl.tm0 = lo + (nfull << 8) + mt * kTailMax;
+      tl.trows = min(kTailMax, rem - mt * kTailMax);
+    }
+  }
   tl.m256 = tl.rows > 128;
   tl.swap = tl.rows <= swap_rows;  // only a segment's last m-tile can be that short
   tl.n0 = nt * (phase == 0 ? kBN1 : kBN2);
@@ -470,81 +510,101 @@ __device__ __forceinline__ void sched_give_up(const LayerArgs& la) {
   __threadfence();
 }
 
-// Epilogue of a swap-AB tile (a segment tail of <= 64 rows): this CTA's TMEM lane = weight row (gate/up: 4 x
-// [16 gate | the same 16 up] neurons, one group per epilogue warp; down: 128 output columns), column j = the
-// tile's row m0 + j. Processed 32 columns at a time. Same fp32 values and roundings as the normal epilogue.
+// Epilogue of a swap-AB tile (a segment tail of <= 64 rows, standalone or merged into a full m-tile): this
+// CTA's TMEM lane = weight row (gate/up: 4 x [16 gate | the same 16 up] neurons, one group per epilogue warp;
+// down: 128 output columns), column j = the tile's row m0 + j. Both 32-column chunks are read first; with
+// hi_bar (a merged tail, which borrows the other accumulator's columns [192, 256)) the warp then releases them
+// before the stores. Same fp32 values and roundings as the normal epilogue.
 template <int kFuse>
-__device__ __forceinline__ void swap_epilogue(const LayerArgs& la, const LTile& tl, uint32_t tacc, uint32_t cta,
-                                              int q, int lane, bool store) {
+__device__ __forceinline__ void swap_chunk(const LayerArgs& la, const LTile& tl, const uint32_t (&r)[32], int c,
+                                           uint32_t cta, int q, int lane, bool store) {
   const int H = la.H, d = la.d;
-  for (int c = 0; c < tl.rows; c += 32) {  // warp-uniform
-    uint32_t r[32];
-    tc::tmem_ld32(tacc + static_cast<uint32_t>(c), r);
-    tc::tmem_wait_ld();
-    if (tl.mode == 0) {
-      // lanes 0-15 hold gate, 16-31 up of neurons n; lanes 0-15 finish columns c..c+15, lanes 16-31 c+16..c+31
-      const bool lo = lane < 16;
-      const int neuron = tl.n0 + 64 * static_cast<int>(cta) + 16 * q + (lane & 15);
-      const bool ok = store && neuron < d;
-      __nv_bfloat16* hcol = la.h + neuron;
+  if (tl.mode == 0) {
+    // lanes 0-15 hold gate, 16-31 up of neurons n; lanes 0-15 finish columns c..c+15, lanes 16-31 c+16..c+31
+    const bool lo = lane < 16;
+    const int neuron = tl.n0 + 64 * static_cast<int>(cta) + 16 * q + (lane & 15);
+    const bool ok = store && neuron < d;
+    __nv_bfloat16* hcol = la.h + neuron;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float send = __uint_as_float(lo ? r[16 + j] : r[j]);
-        const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-        const float g = lo ? __uint_as_float(r[j]) : recv, u = lo ? recv : __uint_as_float(r[16 + j]);
-        const int tok = c + (lo ? j : 16 + j);
-        if (ok && tok < tl.rows) hcol[static_cast<int64_t>(tl.m0 + tok) * d] = __float2bfloat16_rn(tc::silu(g) * u);
-      }
-    } else {
-      const int col = tl.n0 + 128 * static_cast<int>(cta) + 32 * q + lane;
-      const bool ok = store && col < H;
+    for (int j = 0; j < 16; ++j) {
+      const float send = __uint_as_float(lo ? r[16 + j] : r[j]);
+      const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+      const float g = lo ? __uint_as_float(r[j]) : recv, u = lo ? recv : __uint_as_float(r[16 + j]);
+      const int tok = c + (lo ? j : 16 + j);
+      if (ok && tok < tl.rows) hcol[static_cast<int64_t>(tl.m0 + tok) * d] = __float2bfloat16_rn(tc::silu(g) * u);
+    }
+  } else {
+    const int col = tl.n0 + 128 * static_cast<int>(cta) + 32 * q + lane;
+    const bool ok = store && col < H;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int tok = c + j;
-        if (tok >= tl.rows) break;  // warp-uniform
-        const int64_t rr = tl.m0 + tok;
-        __nv_bfloat16* orow;
-        const __nv_bfloat16* rrow = nullptr;
-        bool vrow = true;
-        if constexpr (kFuse == 2) {
-          const int64_t v = static_cast<int64_t>(__ldg(la.fz.src + rr));
-          vrow = v >= 0 && v < la.vrows * la.npeer;
-          const int p = vrow ? static_cast<int>(v / la.vrows) : 0;
-          const int64_t i = vrow ? v - p * la.vrows : 0;
-          __nv_bfloat16* py = la.peer_y[0];
-          const __nv_bfloat16* pr = la.peer_res[0];
+    for (int j = 0; j < 32; ++j) {
+      const int tok = c + j;
+      if (tok >= tl.rows) break;  // warp-uniform
+      const int64_t rr = tl.m0 + tok;
+      __nv_bfloat16* orow;
+      const __nv_bfloat16* rrow = nullptr;
+      bool vrow = true;
+      if constexpr (kFuse == 2) {
+        const int64_t v = static_cast<int64_t>(__ldg(la.fz.src + rr));
+        vrow = v >= 0 && v < la.vrows * la.npeer;
+        const int p = vrow ? static_cast<int>(v / la.vrows) : 0;
+        const int64_t i = vrow ? v - p * la.vrows : 0;
+        __nv_bfloat16* py = la.peer_y[0];
+        const __nv_bfloat16* pr = la.peer_res[0];
 #pragma unroll
-          for (int jj = 1; jj < kMaxPeers; ++jj)
-            if (p == jj) {
-              py = la.peer_y[jj];
-              pr = la.peer_res[jj];
-            }
-          orow = py + i * H;
-          rrow = pr ? pr + i * H : nullptr;
-        } else {
-          int64_t oi = rr;
-          if constexpr (kFuse == 1) {
-            oi = la.fz.src ? static_cast<int64_t>(__ldg(la.fz.src + rr)) : rr;
-            vrow = oi >= 0 && oi < la.fz.rows;
-            if (!vrow) oi = 0;
-            rrow = la.fz.residual ? la.fz.residual + oi * H : nullptr;
+        for (int jj = 1; jj < kMaxPeers; ++jj)
+          if (p == jj) {
+            py = la.peer_y[jj];
+            pr = la.peer_res[jj];
           }
-          orow = la.y + oi * H;
+        orow = py + i * H;
+        rrow = pr ? pr + i * H : nullptr;
+      } else {
+        int64_t oi = rr;
+        if constexpr (kFuse == 1) {
+          oi = la.fz.src ? static_cast<int64_t>(__ldg(la.fz.src + rr)) : rr;
+          vrow = oi >= 0 && oi < la.fz.rows;
+          if (!vrow) oi = 0;
+          rrow = la.fz.residual ? la.fz.residual + oi * H : nullptr;
         }
-        float val = __uint_as_float(r[j]);
-        if (ok && vrow) {
-          if (rrow) val += __bfloat162float(rrow[col]);
-          orow[col] = __float2bfloat16_rn(val);
-        }
+        orow = la.y + oi * H;
+      }
+      float val = __uint_as_float(r[j]);
+      if (ok && vrow) {
+        if (rrow) val += __bfloat162float(rrow[col]);
+        orow[col] = __float2bfloat16_rn(val);
       }
     }
   }
 }
 
+// Arrive (relaxed, on the leader's copy) once this warp's TMEM reads before it have completed.
+__device__ __forceinline__ void release_cols(uint64_t* bar, int lane) {
+  tc::fence_before();
+  __syncwarp();
+  if (lane == 0) tc::mbar_arrive_cluster_relaxed(bar, 0);
+}
+
+template <int kFuse>
+__device__ __forceinline__ void swap_epilogue(const LayerArgs& la, const LTile& tl, uint32_t tacc, uint32_t cta,
+                                              int q, int lane, bool store, uint64_t* hi_bar = nullptr) {
+  uint32_t r0[32], r1[32];
+  const bool two = tl.rows > 32;  // warp-uniform (rows <= 64)
+  tc::tmem_ld32(tacc, r0);
+  if (two) tc::tmem_ld32(tacc + 32u, r1);
+  tc::tmem_wait_ld();
+  if (hi_bar) release_cols(hi_bar, lane);
+  swap_chunk<kFuse>(la, tl, r0, 0, cta, q, lane, store);
+  if (two) swap_chunk<kFuse>(la, tl, r1, 32, cta, q, lane, store);
+}
+
 // Shared memory of the single-launch kernel: only the TMA ring, its barriers and the x-readiness cache (the
-// per-segment tables live in the cursor walk, the epilogue stores straight from registers), so the ring holds
-// 7 stages of 32 KB per CTA (256-row m-tiles) or 9 of 24 KB (128-row m-tiles): the v2 profile of this round
-// showed the MMA warp waiting on TMA data ~40 % of its time with 6 stages (profiles/SUMMARY.md).
+// per-segment tables live in the cursor walk, the epilogue stores straight from registers). 256-row m-tiles:
+// 6 stages of 36 KB per CTA (A 16 KB + a 4 KB slot for a merged tail's rows + B 16 KB); 128-row m-tiles
+// (decode): 9 stages of 24 KB.
+constexpr int kTQ = 4;           // tile-id queue depth (dynamic tile order)
+constexpr int kTQConsumers = 10;  // peer producer + MMA warp + 2 x 4 epilogue warps
+
 template <int S, int SA>
 struct __align__(8) SmemLT {
   uint8_t a[S][SA];
@@ -553,12 +613,24 @@ struct __align__(8) SmemLT {
   uint64_t empty[S];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  // hi_free[b]: accumulator b's columns [192, 256) drained by the epilogue (8 warp arrivals per use). Users
+  // of those columns, in tile order: the main accumulator of a 256-row tile in b, and the merged tail of a
+  // tile whose main accumulator is the other one.
+  uint64_t hi_free[2];
+  // dynamic tile order (la.dyn): the leader's producer claims tiles from a global counter and publishes each
+  // id to both CTAs' queues; the peer's producer, the MMA warp and the epilogue warps pop them in order
+  uint64_t tq_full[kTQ];   // per CTA: id written (one release arrive by the leader's producer)
+  uint64_t tq_empty[kTQ];  // leader: id read by all 10 consumers
+  int tq[kTQ];
   uint32_t tmem_base;
   uint32_t xok[kXokWords];  // pdl == 2: bit per m-tile, this CTA's A rows seen ready
 };
-constexpr int kStagesL = 7;
+constexpr int kStagesL = 6;
 constexpr int kStagesLD = 9;
-using SmemL = SmemLT<kStagesL, kStageA>;
+constexpr int kTailSlot = 16384;             // offset of the merged-tail rows inside a 256-row stage's A slot
+constexpr int kStageAL = kStageA + 4096;     // <= 32 tail rows x 128 B per CTA
+constexpr int kMaxDefer = 3;                 // K stages whose tail MMAs may wait for the borrowed columns
+using SmemL = SmemLT<kStagesL, kStageAL>;
 using SmemLD = SmemLT<kStagesLD, kStageAD>;
 constexpr size_t kSmemBytesL = sizeof(SmemL) + 1024;
 constexpr size_t kSmemBytesLD = sizeof(SmemLD) + 1024;
@@ -584,72 +656,160 @@ __device__ __forceinline__ void store_row_bf16x32(__nv_bfloat16* dst, const floa
 // h = silu(g) * u, down tiles store y (y_sorted, the fused combine y[src[r]] + residual, or the source rank's
 // row over peer memory). row_in_tile = this thread's row, ncols / acc_off = the accumulator columns it holds
 // (all 256 for M = 256, half for the M = 128 "2x2" layout). valid = the row exists and nothing aborted.
+// Gate/up columns: windows of 128 = [64 gate | the same 64 up] (h columns n0 + window * 64 + [0, 64)).
+// hi_bar (M = 256): columns [192, 256) are read first and released on it (a merged tail of the next tile
+// borrows them), then the rest.
 template <int kFuse>
 __device__ __forceinline__ void drain_acc(const LayerArgs& la, const LTile& tl, uint32_t tacc, int row_in_tile,
-                                          int ncols, int acc_off, bool valid) {
+                                          int ncols, int acc_off, bool valid, uint64_t* hi_bar, int lane) {
   const int H = la.H, d = la.d;
   const int64_t r = tl.m0 + row_in_tile;
+  uint32_t hi0[32], hi1[32];  // columns [192, 256) when read first
+  if (hi_bar) {
+    tc::tmem_ld32(tacc + 192u, hi0);
+    tc::tmem_ld32(tacc + 224u, hi1);
+    tc::tmem_wait_ld();
+    release_cols(hi_bar, lane);
+  }
   if (tl.mode == 0) {
-    // windows of 128 columns: [gate 64 | up 64] of h columns n0 + (window) * 64 + [0, 64)
     __nv_bfloat16* orow = la.h + r * d;
     for (int w = 0; w < ncols / 128; ++w) {
       const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
       const int hcol0 = tl.n0 + (acc_off + w * 128) / 2;
-#pragma unroll 1
+      const bool upreg = hi_bar && w == 1;  // window 1's up half already in registers
+#pragma unroll
       for (int c = 0; c < 64; c += 32) {
         uint32_t gr[32], ur[32];
         tc::tmem_ld32(wbase + c, gr);
-        tc::tmem_ld32(wbase + 64 + c, ur);
+        if (!upreg) tc::tmem_ld32(wbase + 64 + c, ur);
         tc::tmem_wait_ld();
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t u = upreg ? (c == 0 ? hi0[j] : hi1[j]) : ur[j];
+          v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(u);
+        }
         if (valid) store_row_bf16x32(orow + hcol0 + c, v, d - (hcol0 + c));
       }
     }
+    return;
+  }
+  __nv_bfloat16* orow;
+  const __nv_bfloat16* rrow = nullptr;
+  bool valid_row = valid;
+  if constexpr (kFuse == 2) {
+    const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
+    valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
+    const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
+    const int64_t ii = valid_row ? v - p * la.vrows : 0;
+    __nv_bfloat16* py = la.peer_y[0];
+    const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+    for (int j = 1; j < kMaxPeers; ++j)
+      if (p == j) {
+        py = la.peer_y[j];
+        pr = la.peer_res[j];
+      }
+    orow = py + ii * H;
+    rrow = pr ? pr + ii * H : nullptr;
   } else {
     int64_t orow_idx = r;
-    bool valid_row = valid;
-    __nv_bfloat16* orow;
-    const __nv_bfloat16* rrow = nullptr;
-    if constexpr (kFuse == 2) {
-      const int64_t v = valid ? static_cast<int64_t>(__ldg(la.fz.src + r)) : -1;
-      valid_row = valid && v >= 0 && v < la.vrows * la.npeer;
-      const int p = valid_row ? static_cast<int>(v / la.vrows) : 0;
-      const int64_t ii = valid_row ? v - p * la.vrows : 0;
-      __nv_bfloat16* py = la.peer_y[0];
-      const __nv_bfloat16* pr = la.peer_res[0];
-#pragma unroll
-      for (int j = 1; j < kMaxPeers; ++j)
-        if (p == j) {
-          py = la.peer_y[j];
-          pr = la.peer_res[j];
-        }
-      orow = py + ii * H;
-      rrow = pr ? pr + ii * H : nullptr;
-    } else {
-      if constexpr (kFuse == 1) {
-        orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
-        valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
-      }
-      orow = la.y + orow_idx * H;
-      rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
+    if constexpr (kFuse == 1) {
+      orow_idx = valid ? (la.fz.src ? __ldg(la.fz.src + r) : r) : 0;
+      valid_row = valid && orow_idx >= 0 && orow_idx < la.fz.rows;
     }
-#pragma unroll 1
-    for (int c = 0; c < ncols; c += 32) {
-      const int col = tl.n0 + acc_off + c;
-      uint32_t vr[32];
-      tc::tmem_ld32(tacc + static_cast<uint32_t>(c), vr);
-      tc::tmem_wait_ld();
-      float v[32];
+    orow = la.y + orow_idx * H;
+    rrow = (kFuse == 1 && la.fz.residual) ? la.fz.residual + orow_idx * H : nullptr;
+  }
+  auto chunk = [&](int c, const uint32_t (&vr)[32]) {
+    const int col = tl.n0 + acc_off + c;
+    float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
-      if (valid_row) {
-        if (rrow) add_bf16x32(rrow + col, v, H - col);
-        store_row_bf16x32(orow + col, v, H - col);
-      }
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[j]);
+    if (valid_row) {
+      if (rrow) add_bf16x32(rrow + col, v, H - col);
+      store_row_bf16x32(orow + col, v, H - col);
+    }
+  };
+  if (hi_bar) {
+    chunk(192, hi0);
+    chunk(224, hi1);
+  }
+  const int nlo = hi_bar ? 192 : ncols;
+#pragma unroll 1
+  for (int c = 0; c < nlo; c += 32) {
+    uint32_t vr[32];
+    tc::tmem_ld32(tacc + static_cast<uint32_t>(c), vr);
+    tc::tmem_wait_ld();
+    chunk(c, vr);
+  }
+}
+
+// Epilogue of a merged gate/up tail. Its MMAs are two M = 128 pair MMAs (A = this CTA's 64 gate rows, then
+// its 64 up rows of the tile's own weight stage; N = the tail's rows rounded up to 16), so in the "2x2"
+// layout lane l < 64 holds neuron l for tail rows [0, N/2), lane 64 + l the same neuron for rows [N/2, N), with
+// gate at columns [0, N/2) of the borrowed region and up at [32, 32 + N/2): both factors in the same lane.
+// Warp q: neurons 32 (q & 1) + lane, tail rows (q >> 1) * N/2 + [0, N/2). Both loads first, then the columns
+// are released (hi_bar) before the stores.
+__device__ __forceinline__ void tail_gu_epilogue(const LayerArgs& la, const LTile& tt, uint32_t tacc, uint32_t cta,
+                                                 int q, int lane, bool store, uint64_t* hi_bar) {
+  const int d = la.d;
+  const int half = ((tt.rows + 15) & ~15) / 2;
+  uint32_t gr[32], ur[32];
+  tc::tmem_ld32(tacc, gr);
+  tc::tmem_ld32(tacc + 32u, ur);
+  tc::tmem_wait_ld();
+  release_cols(hi_bar, lane);
+  const int neuron = tt.n0 + 64 * static_cast<int>(cta) + 32 * (q & 1) + lane;
+  const int tok0 = (q >> 1) * half;
+  if (!store || neuron >= d) return;
+  __nv_bfloat16* hcol = la.h + neuron;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int tok = tok0 + j;
+    if (j >= half || tok >= tt.rows) break;  // warp-uniform
+    hcol[static_cast<int64_t>(tt.m0 + tok) * d] =
+        __float2bfloat16_rn(tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]));
+  }
+}
+
+// Tile-id queue of the dynamic tile order (one per CTA, kTQ slots). Consumers pop in order; the leader's
+// producer pushes after every consumer released the slot. Ids >= the tile count end every role's loop.
+struct TileQ {
+  int slot = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++slot == kTQ) {
+      slot = 0;
+      ph ^= 1u;
     }
   }
+};
+// The leader CTA's slot is a plain shared store + release arrive; the peer's is an st.async that completes
+// transaction bytes on the peer's barrier, so no consumer needs a cluster-scope acquire (whose L1 invalidate
+// made the read-only offsets loads of the next tile decode miss).
+// The consumer's release of a slot is a relaxed arrive once the id is in a register (the shuffle needs the
+// loaded value): a release arrive would first wait for all of the warp's outstanding global stores (the
+// epilogue's rows) — measured as ~2K idle SM cycles per tile in the MMA pipe.
+template <class SM>
+__device__ __forceinline__ int tq_pop(SM& s, TileQ& q, int lane) {
+  tc::mbar_wait(&s.tq_full[q.slot], q.ph);
+  const int t = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile int*>(&s.tq[q.slot]), 0);
+  if (lane == 0) tc::mbar_arrive_cluster_relaxed(&s.tq_empty[q.slot], 0);
+  q.next();
+  return t;
+}
+template <class SM>
+__device__ __forceinline__ void tq_push(SM& s, TileQ& q, int t, int lane) {
+  tc::mbar_wait(&s.tq_empty[q.slot], q.ph ^ 1u);
+  if (lane == 0) {
+    tc::arrive_expect_tx_cluster(&s.tq_full[q.slot], 1, 4u);
+    tc::st_async_cluster_u32(&s.tq[q.slot], &s.tq_full[q.slot], 1, static_cast<uint32_t>(t));
+    *reinterpret_cast<volatile int*>(&s.tq[q.slot]) = t;
+    tc::mbar_arrive(&s.tq_full[q.slot]);
+  }
+  __syncwarp();
+  q.next();
 }
 
 template <int kFuse, int kMT>
@@ -662,7 +822,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   using SM = typename std::conditional<kMT == 256, SmemL, SmemLD>::type;
   constexpr int kS = kMT == 256 ? kStagesL : kStagesLD;  // ring stages
-  constexpr int kSA = kMT == 256 ? kStageA : kStageAD;   // A bytes per stage per CTA
+  constexpr int kSA = kMT == 256 ? kStageAL : kStageAD;  // A bytes per stage per CTA (+ tail slot at 256)
+  const bool merge = kMT == 256 && la.merge != 0;
   static_assert(kMT == 256 || kMT == 128, "kMT");
   SM& s = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
@@ -683,7 +844,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     tc::prefetch_tmap(&tmU);
     tc::prefetch_tmap(&tmH);
     tc::prefetch_tmap(&tmD);
-    if (la.swap_rows > 0) {
+    if (la.swap_rows > 0 || kMT == 256) {
       tc::prefetch_tmap(&tmX16);
       tc::prefetch_tmap(&tmH16);
       tc::prefetch_tmap(&tmG16);
@@ -693,7 +854,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
   // total m-tiles (every thread: nseg reads of the read-only offsets, no shared table)
   int mtiles = 0;
-  for (int g = 0; g < nseg; ++g) mtiles += (__ldg(offs + g + 1) - __ldg(offs + g) + kMT - 1) / kMT;
+  for (int g = 0; g < nseg; ++g) mtiles += seg_mtiles<kMT>(__ldg(offs + g + 1) - __ldg(offs + g), merge);
   if (tid == 0) {
     for (int i = 0; i < kS; ++i) {
       tc::mbar_init(&s.full[i], 1);
@@ -702,6 +863,11 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&s.tfull[i], 1);
       tc::mbar_init(&s.tempty[i], 8);
+      tc::mbar_init(&s.hi_free[i], 8);
+    }
+    for (int i = 0; i < kTQ; ++i) {
+      tc::mbar_init(&s.tq_full[i], 1);
+      tc::mbar_init(&s.tq_empty[i], kTQConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -718,7 +884,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   if (la.pdl) {
     if (warp == 0 && lane == 0 && pair < T1) {
       Cursor c;
-      const LTile tl = decode_ltile<kMT>(offs, pair, nseg, T1, NT1, NT2, la.swap_rows, c, la.order != 0);
+      const LTile tl = decode_ltile<kMT>(offs, pair, nseg, T1, NT1, NT2, la.swap_rows, c, la.order != 0, merge);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       const int nr = tl.n0 + 64 * static_cast<int>(cta);
       const int kbs = KB1 < kPrefetchK ? KB1 : kPrefetchK;
@@ -740,8 +906,22 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint32_t phase = 0;
     Cursor cur;
     const uint32_t full0 = tc::mapa(&s.full[0], 0);  // the leader's barriers, as cluster addresses
-    for (int t = pair; t < ntiles; t += npairs) {
-      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
+    TileQ tq;
+    const bool dyn = la.dyn != 0;
+    // every pair's first tile is its index; with the dynamic order the leader's producer claims the next one
+    // kClaimAhead K steps before the end of this tile's loads (~2 ring depths before the tile's MMAs end: late
+    // enough that the claim order follows the pairs' finishing order, early enough to hide the atomic) and
+    // publishes it once this tile's loads are issued
+    for (int t = pair; t < ntiles;) {
+      uint32_t claim = 0;
+      const bool claimer = dyn && leader;
+      bool claimed = !claimer;
+      auto claim_next = [&]() {
+        if (lane == 0) claim = atomicAdd(la.tile_ctr, 1u);
+        claimed = true;
+      };
+      int t_next = t + npairs;
+      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0, merge);
       const int e = la.expert_slot ? __ldg(la.expert_slot + tl.g % E) : tl.g % E;
       // Activation rows this CTA stages per K step: 128 (M = 256), 64 (M = 128) or, for a swap-AB tile, half
       // of its N = rows rounded up to 16 (in 16-row boxes)
@@ -749,24 +929,30 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const int a_rows = tl.swap ? nsw / 2 : (tl.m256 ? 128 : 64);
       const int a_row0 = tl.m0 + static_cast<int>(cta) * a_rows;
       const int nact = (a_rows + 15) / 16;  // swap tiles: 16-row activation boxes
+      // merged tail: half of its N = trows rounded up to 16 per CTA, 16-row boxes into the stage's tail slot
+      const int t_rows = ((tl.trows + 15) & ~15) / 2;
+      const int t_row0 = tl.tm0 + static_cast<int>(cta) * t_rows;
+      const int tact = (t_rows + 15) / 16;
       // A tile of ≤ 64 rows: every row the second CTA would stage is past the tile's end, so it skips its A
       // load (its MMA rows read stale shared memory; row m of the product depends on A row m only and rows
       // past tl.rows are never stored). Knob ffn_askip = 0 loads them anyway (A/B).
       const bool a_skip = la.askip && !tl.swap && !tl.m256 && tl.rows <= 64;
       const uint32_t bytes = tl.swap ? 2u * static_cast<uint32_t>(nact * 16 * 128 + 128 * 128)
-                                     : 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128) -
+                                     : 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128 + tact * 2048) -
                                            (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
       if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
-        // padding: their products are never stored, so they are not waited for)
+        // padding: their products are never stored, so they are not waited for), merged tail rows included
         const int mid = tl.mid;
         const bool cached = mid < kXokWords * 32 && (s.xok[mid >> 5] >> (mid & 31) & 1u);
         if (!cached) {
           const int lo = a_row0, hi = min(a_row0 + a_rows, tl.m0 + tl.rows);
+          const int tlo = t_row0, thi = min(t_row0 + t_rows, tl.tm0 + tl.trows);
           uint32_t spins = 0;
           for (;;) {
             bool ok = true;
             for (int r = lo + lane; r < hi; r += kWarp) ok = ok && ld_acquire_u32(la.xready + r) != 0u;
+            for (int r = tlo + lane; r < thi; r += kWarp) ok = ok && ld_acquire_u32(la.xready + r) != 0u;
             if (__all_sync(0xffffffffu, ok)) break;
             __nanosleep(64);
             if (++spins >= la.spin_limit) {
@@ -812,21 +998,26 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             stage = 0;
             phase ^= 1;
           }
+          if (!claimed && kb == KB - la.claim_ahead) claim_next();
+        }
+      };
+      // gate/up weight rows of a swap-AB tile as 4 x [16 gate | the same 16 up], so each epilogue warp's 32 TMEM
+      // lanes hold both factors of its 16 neurons
+      auto load_gu16 = [&](uint8_t* sb, uint32_t fb, int k0) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          tc::tma_load_3d_2sm(&tmG16, sb + (32 * q4) * 128, fb, k0, nrg + 16 * q4, e);
+          tc::tma_load_3d_2sm(&tmU16, sb + (32 * q4 + 16) * 128, fb, k0, nrg + 16 * q4, e);
         }
       };
       if (tl.swap) {
         // swap-AB tile: the activations are the MMA's B side (nsw/2 rows here, 16-row boxes); the weights its
-        // A side. Gate/up weight rows go in as 4 x [16 gate | the same 16 up] so each epilogue warp's 32 TMEM
-        // lanes hold both factors of its 16 neurons.
+        // A side.
         const CUtensorMap* mA16 = tl.mode == 0 ? &tmX16 : &tmH16;
         if (tl.mode == 0) {
           kloop(KB1, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
             for (int i = 0; i < nact; ++i) tc::tma_load_2d_2sm(mA16, sa + i * 2048, fb, k0, a_row0 + 16 * i);
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              tc::tma_load_3d_2sm(&tmG16, sb + (32 * q4) * 128, fb, k0, nrg + 16 * q4, e);
-              tc::tma_load_3d_2sm(&tmU16, sb + (32 * q4 + 16) * 128, fb, k0, nrg + 16 * q4, e);
-            }
+            load_gu16(sb, fb, k0);
           });
         } else {
           kloop(KB2, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
@@ -835,12 +1026,32 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             tc::tma_load_3d_2sm(&tmD, sb + 64 * 128, fb, k0, nrd + 64, e);
           });
         }
+      } else if (tl.trows > 0) {
+        // full m-tile carrying a merged tail: A (128 rows), the tail's rows (tail slot), the weights
+        if (tl.mode == 0) {
+          kloop(KB1, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            tc::tma_load_2d_2sm(&tmX, sa, fb, k0, a_row0);
+            tc::tma_load_2d_2sm(&tmX, sa + 64 * 128, fb, k0, a_row0 + 64);
+            for (int i = 0; i < tact; ++i) tc::tma_load_2d_2sm(&tmX16, sa + kTailSlot + i * 2048, fb, k0, t_row0 + 16 * i);
+            tc::tma_load_3d_2sm(&tmG, sb, fb, k0, nrg, e);
+            tc::tma_load_3d_2sm(&tmU, sb + 64 * 128, fb, k0, nrg, e);
+          });
+        } else {
+          kloop(KB2, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
+            tc::tma_load_2d_2sm(&tmH, sa, fb, k0, a_row0);
+            tc::tma_load_2d_2sm(&tmH, sa + 64 * 128, fb, k0, a_row0 + 64);
+            for (int i = 0; i < tact; ++i) tc::tma_load_2d_2sm(&tmH16, sa + kTailSlot + i * 2048, fb, k0, t_row0 + 16 * i);
+            tc::tma_load_3d_2sm(&tmD, sb, fb, k0, nrd, e);
+            tc::tma_load_3d_2sm(&tmD, sb + 64 * 128, fb, k0, nrd + 64, e);
+          });
+        }
       } else {
         const bool loadA = !(a_skip && cta == 1), A2 = tl.m256;
-        if (tl.mode == 0) {  // 64 rows of W_gate then the same rows of W_up
+        if (tl.mode == 0) {
           kloop(KB1, [&](uint8_t* sa, uint8_t* sb, uint32_t fb, int k0) {
             if (loadA) tc::tma_load_2d_2sm(&tmX, sa, fb, k0, a_row0);
             if (A2) tc::tma_load_2d_2sm(&tmX, sa + 64 * 128, fb, k0, a_row0 + 64);
+            // 64 rows of W_gate then the same rows of W_up
             tc::tma_load_3d_2sm(&tmG, sb, fb, k0, nrg, e);
             tc::tma_load_3d_2sm(&tmU, sb + 64 * 128, fb, k0, nrg, e);
           });
@@ -853,6 +1064,12 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           });
         }
       }
+      if (claimer) {
+        if (!claimed) claim_next();  // tiles shorter than claim_ahead K steps
+        t_next = static_cast<int>(__shfl_sync(0xffffffffu, claim, 0)) + npairs;
+        tq_push(s, tq, t_next, lane);  // the end marker (>= ntiles) too
+      }
+      t = dyn && !leader ? tq_pop(s, tq, lane) : t_next;
     }
   } else if (warp == 1) {
     if (leader) {
@@ -865,22 +1082,83 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       uint32_t phase = 0;
       Cursor cur;
       int i = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++i) {
-        const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
+      int huse0 = 0, huse1 = 0;  // uses of each accumulator's columns [192, 256) issued so far (hi_free phases)
+      auto next_use = [&](int b) { return b ? huse1++ : huse0++; };
+      TileQ tq;
+      const bool dyn = la.dyn != 0;
+      for (int t = pair; t < ntiles; t = dyn ? tq_pop(s, tq, lane) : t + npairs, ++i) {
+        const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0, merge);
         // swap-AB tile: M = 256 weight rows (128 per CTA, from the B slots), N = rows rounded up to 16 (from the
         // A slots): operands exchanged, accumulator lane = weight row, column = the tile's row
         const uint32_t idesc = tl.swap ? tc::idesc_bf16(256, (tl.rows + 15) & ~15) : (tl.m256 ? idesc256 : idesc128);
         const int acc = i & 1;
         const uint32_t use = static_cast<uint32_t>(i >> 1);
+        uint64_t* trec = (la.ttrace && i < la.ttrace_max) ? la.ttrace + (static_cast<int64_t>(pair) * la.ttrace_max + i) * 8 : nullptr;
+        const uint64_t c_wait0 = trec ? clock64() : 0;
         tc::mbar_wait_cluster(&s.tempty[acc], (use & 1u) ^ 1u);
+        if (tl.m256) {  // columns [192, 256): the previous tile's merged tail may still hold them
+          const int n = next_use(acc);
+          tc::mbar_wait_cluster(&s.hi_free[acc], static_cast<uint32_t>(n & 1) ^ 1u);
+        }
         tc::fence_after();
+        uint64_t c_full = 0;
+        if (trec && lane == 0) {
+          const uint64_t c = clock64();
+          trec[0] = globaltimer_ns();
+          trec[1] = c;
+          trec[7] = static_cast<uint64_t>(t) | ((c - c_wait0) << 32);
+        }
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
         const int KB = tl.mode == 0 ? KB1 : KB2;
         // +1 in a descriptor's address field = +16 B: stage strides and the 32-B K steps are constants
         const uint64_t a0 = tl.swap ? bdesc0 : adesc0, b0 = tl.swap ? adesc0 : bdesc0;
         const uint32_t astep = tl.swap ? (kStageB >> 4) : (kSA >> 4), bstep = tl.swap ? (kSA >> 4) : (kStageB >> 4);
+        // A merged tail (M = 256 weight rows from the B slot x N = its rows from the stage's tail slot) goes to
+        // the other accumulator's columns [192, 256) once the epilogue has drained their previous user; until
+        // then up to kMaxDefer stages keep their tail MMAs (and their slot) pending.
+        const bool tail = tl.trows > 0;
+        const int oth = acc ^ 1;
+        const uint32_t t_tmem = tmem_base + static_cast<uint32_t>(oth * 256 + 192);
+        // down tails: one M = 256 swap-AB MMA per K step (lane = output column); gate/up tails: two M = 128 ones,
+        // the CTA's 64 gate rows then its 64 up rows, into columns +0 / +32 (both factors of a neuron in one lane)
+        const uint32_t tidesc = tl.mode == 0 ? tc::idesc_bf16(128, (tl.trows + 15) & ~15)
+                                             : tc::idesc_bf16(256, (tl.trows + 15) & ~15);
+        const bool gu_tail = tl.mode == 0;
+        uint32_t tpar = 0;
+        bool tok = true;
+        if (tail) {
+          const int n = next_use(oth);
+          tpar = static_cast<uint32_t>(n & 1) ^ 1u;
+          tok = false;
+        }
+        int pend = 0, pstage = stage, pkb = 0;
+        auto issue_tails = [&]() {
+          for (int p = 0; p < pend; ++p) {
+            int st = pstage + p;
+            if (st >= kS) st -= kS;
+            const int kbp = pkb + p;
+            const uint64_t wd = bdesc0 + static_cast<uint64_t>(st * (kStageB >> 4));
+            const uint64_t td = adesc0 + static_cast<uint64_t>(st * (kSA >> 4) + (kTailSlot >> 4));
+            if (tc::elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < kBK / kUK; ++kk) {
+                const uint32_t acc_flag = (kbp | kk) != 0 ? 1u : 0u;
+                tc::mma_f16<2>(t_tmem, wd + static_cast<uint64_t>(kk * 2), td + static_cast<uint64_t>(kk * 2), tidesc,
+                               acc_flag);
+                if (gu_tail)  // the up rows: 64 rows (8 KB) further into the weight stage
+                  tc::mma_f16<2>(t_tmem + 32u, wd + static_cast<uint64_t>((64 * 128 >> 4) + kk * 2),
+                                 td + static_cast<uint64_t>(kk * 2), tidesc, acc_flag);
+              }
+              tc::commit_2sm_mc(&s.empty[st], 0x3);
+            }
+            __syncwarp();
+          }
+          pend = 0;
+        };
         for (int kb = 0; kb < KB; ++kb) {
+          const uint64_t c0 = trec ? clock64() : 0;
           tc::mbar_wait_cluster(&s.full[stage], phase);
+          if (trec) c_full += clock64() - c0;
           tc::fence_after();
           const uint64_t ad = a0 + static_cast<uint64_t>(stage * astep), bd = b0 + static_cast<uint64_t>(stage * bstep);
           if (tc::elect_one()) {
@@ -888,16 +1166,44 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             for (int kk = 0; kk < kBK / kUK; ++kk)
               tc::mma_f16<2>(d_tmem, ad + static_cast<uint64_t>(kk * 2), bd + static_cast<uint64_t>(kk * 2), idesc,
                              (kb | kk) != 0 ? 1u : 0u);
-            tc::commit_2sm_mc(&s.empty[stage], 0x3);
+            if (!tail) tc::commit_2sm_mc(&s.empty[stage], 0x3);
           }
           __syncwarp();
+          if (tail) {
+            if (pend == 0) {
+              pstage = stage;
+              pkb = kb;
+            }
+            ++pend;
+            if (!tok) {
+              bool ok = __all_sync(0xffffffffu, tc::mbar_test_cluster(&s.hi_free[oth], tpar));
+              if (!ok && pend >= kMaxDefer) {
+                tc::mbar_wait_cluster(&s.hi_free[oth], tpar);
+                ok = true;
+              }
+              if (ok) tc::fence_after();
+              tok = ok;
+            }
+            if (tok) issue_tails();
+          }
           if (++stage == kS) {
             stage = 0;
             phase ^= 1;
           }
         }
+        if (tail && pend > 0) {
+          if (!tok) {
+            tc::mbar_wait_cluster(&s.hi_free[oth], tpar);
+            tc::fence_after();
+          }
+          issue_tails();
+        }
         if (tc::elect_one()) tc::commit_2sm_mc(&s.tfull[acc], 0x3);
         __syncwarp();
+        if (trec && lane == 0) {
+          trec[2] = clock64();
+          trec[6] = c_full;
+        }
       }
     }
   } else {
@@ -905,12 +1211,17 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     const int q = warp & 3;
     Cursor cur;
     int i = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++i) {
-      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0);
+    TileQ tq;
+    const bool dyn = la.dyn != 0;
+    for (int t = pair; t < ntiles; t = dyn ? tq_pop(s, tq, lane) : t + npairs, ++i) {
+      const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0, merge);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
       tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
       tc::fence_after();
+      uint64_t* trec = (la.ttrace && leader && q == 2 && lane == 0 && i < la.ttrace_max)
+                           ? la.ttrace + (static_cast<int64_t>(pair) * la.ttrace_max + i) * 8 : nullptr;
+      if (trec) trec[3] = clock64();
       // a readiness wait of this launch gave up: this tile may have been computed from unready rows, so it
       // (and every later tile) stores nothing
       const bool aborted = __shfl_sync(0xffffffffu, lane == 0 ? ld_volatile_u32(la.abort) : 0u, 0) != 0u;
@@ -927,8 +1238,21 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         ncols = kN / 2;
         acc_off = (q >> 1) * (kN / 2);
       }
+      if (tl.trows > 0) {  // merged tail first: it frees the other accumulator's columns [192, 256)
+        LTile tt = tl;
+        tt.m0 = tl.tm0;
+        tt.rows = tl.trows;
+        const uint32_t ttacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>((acc ^ 1) * 256 + 192);
+        if (tl.mode == 0) tail_gu_epilogue(la, tt, ttacc, cta, q, lane, !aborted, &s.hi_free[acc ^ 1]);
+        else swap_epilogue<kFuse>(la, tt, ttacc, cta, q, lane, !aborted, &s.hi_free[acc ^ 1]);
+      }
       if (tl.swap) swap_epilogue<kFuse>(la, tl, tacc, cta, q, lane, !aborted);
-      else drain_acc<kFuse>(la, tl, tacc, row_in_tile, ncols, acc_off, row_in_tile < tl.rows && !aborted);
+      else drain_acc<kFuse>(la, tl, tacc, row_in_tile, ncols, acc_off, row_in_tile < tl.rows && !aborted,
+                                   tl.m256 ? &s.hi_free[acc] : nullptr, lane);
+      if (trec) {
+        trec[4] = clock64();
+        trec[5] = globaltimer_ns();
+      }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1058,9 +1382,9 @@ readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, 
 // Readiness region of the single-launch kernel: [down-tile counters: kMaxSeg + #128-row m-tiles][abort word]
 // [pad][x_sorted row flags: rows] (the flags are used when the gather dispatch precedes the FFN, pdl == 2);
 // one memset (or the route launch) zeroes all of it before every launch.
-int64_t ffn_layer_abort_index(int64_t rows) { return kMaxSeg + (rows + 127) / 128 + 1; }
+int64_t ffn_layer_abort_index(int64_t rows) { return kMaxSeg + (rows + 127) / 128 + 1; }  // then the tile counter
 size_t ffn_layer_xready_offset(int64_t rows) {
-  return align_up(static_cast<size_t>(ffn_layer_abort_index(rows) + 1) * sizeof(uint32_t), 256);
+  return align_up(static_cast<size_t>(ffn_layer_abort_index(rows) + 2) * sizeof(uint32_t), 256);
 }
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
   (void)nseg;
@@ -1097,7 +1421,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   const int kswap = knob(Knob::kFfnSwap);
   const int swap_rows = (kswap < 0 ? (mt == 256 ? 64 : 0) : std::min(64, kswap)) & ~15;
   CUtensorMap mX16 = mX, mH16 = mH, mG16 = mG, mU16 = mU;
-  if (ok && swap_rows > 0)
+  if (ok && (swap_rows > 0 || mt == 256))  // swap-AB tiles and merged tails: 16-row boxes
     ok = tc::make_map_2d(&mX16, xs, H, rows, kBK, 16) && tc::make_map_2d(&mH16, h, d, rows, kBK, 16) &&
          tc::make_map_3d(&mG16, wg, H, d, EW, kBK, 16) && tc::make_map_3d(&mU16, wu, H, d, EW, kBK, 16);
   if (!ok) {
@@ -1135,9 +1459,25 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   la.pdl = pdl ? (xready ? 2 : 1) : 0;
   la.xready = xready;
   la.trace = g_trace_buf;
+  la.ttrace = g_tile_trace;
+  la.ttrace_max = g_tile_trace_max;
   la.askip = knob(Knob::kFfnAskip) != 0;
   la.order = knob(Knob::kFfnOrder);
   la.swap_rows = swap_rows;
+  // Dynamic tile order (greedy: a pair claims its next tile near the end of its current one) and merged
+  // segment tails, together, for 256-row m-tile launches of <= kDynRows rows: there the last wave is a large
+  // part of each pair's ~25-60 tiles and the tails ~1 in 5 m-tiles; merged tails make tile costs uneven, which
+  // only the dynamic order balances (a static stride with merged tails left the pairs' end times ~90 us apart
+  // and re-read weights from DRAM). A/B on one box (scripts/ffn_lab.py, profiles/SUMMARY.md r02): -5 % at 2048
+  // rows, -6.7 % at 4096, -1.7 % at 8192, -0.8 % at 16384, but +1.4 % at 32768 and +3.4 % at 65536 (static
+  // rounds keep the pairs sharing a weight tile in lockstep), so larger launches keep the static order.
+  // Knobs ffn_dyn / ffn_merge = 0 | 1 force either.
+  const bool big = rows > kDynRows;
+  const int kdyn = knob(Knob::kFfnDyn), kmerge = knob(Knob::kFfnMerge);
+  la.dyn = kdyn < 0 ? (mt == 256 && !big ? 1 : 0) : (kdyn != 0 ? 1 : 0);
+  la.merge = mt == 256 && (kmerge < 0 ? la.dyn != 0 : kmerge != 0);
+  la.tile_ctr = la.abort + 1;
+  la.claim_ahead = std::max(1, knob(Knob::kFfnClaim));
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
     if (peers->npeer < 1 || peers->npeer > kMaxPeers || peers->vrows < 1 || !src) {

@@ -7,7 +7,7 @@ namespace readme {
 // knobs.cpp: lab/test switches, read from the environment once, overridable by readme_debug_set_knob.
 enum class Knob : int {
   kRoute, kRouteCluster, kRouteTile, kDispatch, kDispatchBulk, kCombineBulk, kPermUnrollD, kPermUnrollC,
-  kFfnKernel, kFfnMt, kFfnPairs, kFfnAskip, kFfnOrder, kFfnSwap, kFfnSpin, kCount
+  kFfnKernel, kFfnMt, kFfnPairs, kFfnAskip, kFfnOrder, kFfnSwap, kFfnSpin, kFfnMerge, kFfnDyn, kFfnClaim, kCount
 };
 int knob(Knob k);
 

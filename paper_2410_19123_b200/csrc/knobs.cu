@@ -39,6 +39,9 @@ constexpr KnobDef kDefs[static_cast<int>(Knob::kCount)] = {
     {"ffn_order", "README_FFN_ORDER", 0},          // 1: gate/up tiles N-tile fastest
     {"ffn_swap", "README_FFN_SWAP", -1},           // -1 auto, else segment tails of <= n rows run swap-AB
     {"ffn_spin", "README_FFN_SPIN", 25},           // log2 of the readiness-poll limit (timeout -> dev_status)
+    {"ffn_merge", "README_FFN_MERGE", -1},         // 256-row m-tiles: segment tails ride on full m-tiles (-1: with ffn_dyn)
+    {"ffn_dyn", "README_FFN_DYN", -1},             // -1 auto (dynamic order at <= 16384 rows of 256-row m-tiles), 0 static, 1 dynamic
+    {"ffn_claim", "README_FFN_CLAIM", 24},         // dynamic order: claim the next tile this many K steps before a tile's loads end
 };
 
 std::atomic<int> g_val[static_cast<int>(Knob::kCount)];

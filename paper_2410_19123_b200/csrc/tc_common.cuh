@@ -69,6 +69,24 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   } while (!done);
 }
 
+// Store a 32-bit word into cluster CTA `cta`'s shared memory at the offset of p as an async-proxy store that
+// completes 4 transaction bytes on that CTA's barrier `bar` (armed by arrive_expect_tx_cluster), so the reader
+// only needs the barrier's phase (no cluster-scope acquire, which costs an L1 invalidate).
+__device__ __forceinline__ void st_async_cluster_u32(const void* p, uint64_t* bar, uint32_t cta, uint32_t v) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(ra), "r"(v), "r"(rb)
+               : "memory");
+}
+// Arrive on cluster CTA `cta`'s barrier and expect `bytes` transaction bytes in the current phase.
+__device__ __forceinline__ void arrive_expect_tx_cluster(uint64_t* bar, uint32_t cta, uint32_t bytes) {
+  uint32_t rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rb), "r"(bytes)
+               : "memory");
+}
+
 // One lane of a converged warp (tcgen05.mma / commit are single-thread instructions: the whole warp walks
 // the issue loop, so descriptors stay in uniform registers, and the elected lane issues).
 __device__ __forceinline__ bool elect_one() {
@@ -262,7 +280,10 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ float silu(float z) { return z / (1.0f + __expf(-z)); }
+// silu(z) = z / (1 + e^-z) with the approximate division (MUFU.RCP + FMUL; within 2 ulp): the expert FFN's
+// gate/up epilogue shares its SM sub-partitions with the TMA-producer and MMA-issuer warps, so its instruction
+// count matters (an IEEE division is ~8 more instructions per element).
+__device__ __forceinline__ float silu(float z) { return __fdividef(z, 1.0f + __expf(-z)); }
 
 // ---- host: tensor maps ---------------------------------------------------------------------------------
 bool make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_in,

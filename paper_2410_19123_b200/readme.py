@@ -36,7 +36,7 @@ EXPORTS = ("readme_route_workspace_bytes", "readme_route", "readme_dispatch", "r
            "readme_ep_signal", "readme_ep_wait", "readme_ep_publish_counts", "readme_ep_plan", "readme_ep_dispatch",
            "readme_ep_expert_ffn",
            "readme_set_device", "readme_status_string", "readme_last_error",
-           "readme_version", "readme_debug_trace", "readme_debug_mark", "readme_debug_set_knob",
+           "readme_version", "readme_debug_trace", "readme_debug_tile_trace", "readme_debug_mark", "readme_debug_set_knob",
            "readme_debug_get_knob", "readme_debug_reset_knob", "readme_debug_hold_sms")
 
 
@@ -117,6 +117,7 @@ _SIGS = {
     "readme_last_error": (ctypes.c_char_p, []),
     "readme_version": (ctypes.c_int, []),
     "readme_debug_trace": (None, [_vp]),
+    "readme_debug_tile_trace": (None, [_vp, _i32]),
     "readme_debug_mark": (ctypes.c_int, [_i32, _vp]),
     "readme_debug_set_knob": (ctypes.c_int, [ctypes.c_char_p, _i32]),
     "readme_debug_get_knob": (ctypes.c_int, [ctypes.c_char_p, _vp]),

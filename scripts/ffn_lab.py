@@ -1,7 +1,8 @@
 """Expert FFN alone (readme_expert_ffn, one ffn_layer2 launch) at several batch sizes under library knob
 variants (readme_debug_set_knob; e.g. ffn_swap=0,64 or ffn_mt=128,256), CUDA-graph replays, L2 flushed
 before each, variants alternated round by round on the same box. Measurement only.
-Usage: python scripts/ffn_lab.py KNOB=a,b [T1 T2 ...]"""
+Usage: python scripts/ffn_lab.py KNOB=a,b [T1 T2 ...]
+       python scripts/ffn_lab.py "k1=a:k2=b,k1=c" [T ...]   (each comma-separated variant sets one or more knobs)"""
 import json
 import os
 import sys
@@ -12,8 +13,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2410_19123_b200 import readme as rd  # noqa: E402
 
-var, vals = sys.argv[1].split("=")
-vals = [int(v) for v in vals.split(",")]
+spec = sys.argv[1]
+if ":" in spec or spec.count("=") > 1:  # variants of several knobs each
+    vals = [v for v in spec.split(",")]
+    var = "variants"
+    settings = {v: [(kv.split("=")[0], int(kv.split("=")[1])) for kv in v.split(":")] for v in vals}
+else:
+    var, vv = spec.split("=")
+    vals = [int(v) for v in vv.split(",")]
+    settings = {v: [(var, v)] for v in vals}
 Ts = [int(t) for t in sys.argv[2:]] or [256, 512, 1024, 2048, 4096, 8192]
 H, E, d = 4096, 8, 5504
 g = torch.Generator(device="cuda").manual_seed(1)
@@ -33,7 +41,8 @@ for T in Ts:
     ws = torch.empty(rd.expert_ffn_workspace_bytes(T, H, E, d, torch.bfloat16), dtype=torch.uint8, device="cuda")
     graphs = {}
     for v in vals:
-        rd.set_knob(var, v)
+        for kn, kv in settings[v]:
+            rd.set_knob(kn, kv)
         fn = lambda: rd.expert_ffn(xs, plan.offsets, wg, wu, wd, out=ys, ws=ws)
         fn()
         torch.cuda.synchronize()
@@ -41,7 +50,8 @@ for T in Ts:
         with torch.cuda.graph(gr):
             fn()
         graphs[v] = gr
-    rd.reset_knob(var)
+        for kn, _ in settings[v]:
+            rd.reset_knob(kn)
     ms = {v: [] for v in vals}
     for _ in range(15):
         for v in vals:

@@ -262,18 +262,23 @@ FFN_KERNEL = {"merged": 0, "split": 1, "unfused": 2}
 
 
 def _set_kernel(knob, kernel):
-    """merged (single launch, 256-row m-tiles above 1024 rows) / merged-mt128 / merged-swap (segment tails of
-    <= 64 rows as swap-AB tiles) / merged-noswap / split (two launches)."""
+    """merged (single launch, 256-row m-tiles above 1024 rows, segment tails riding on full m-tiles) /
+    merged-mt128 / merged-mt256 / merged-swap (tails of <= 64 rows as their own swap-AB tiles) /
+    merged-noswap (tails as M = 128 tiles) / split (two launches)."""
     if kernel == "merged-mt128":
         knob("ffn_mt", 128)
+    elif kernel == "merged-mt256":
+        knob("ffn_mt", 256)
     elif kernel == "merged-swap":
+        knob("ffn_merge", 0)
         knob("ffn_swap", 64)
     elif kernel == "merged-noswap":
+        knob("ffn_merge", 0)
         knob("ffn_swap", 0)
     knob("ffn_kernel", FFN_KERNEL["split" if kernel == "split" else "merged"])
 
 
-KERNELS = ["merged", "merged-mt128", "merged-swap", "merged-noswap", "split"]
+KERNELS = ["merged", "merged-mt128", "merged-mt256", "merged-swap", "merged-noswap", "split"]
 
 
 @pytest.mark.parametrize("T,H,d,E,k,skew", [
@@ -345,10 +350,13 @@ def test_expert_ffn_tile_edges(rd, knob, kernel):
 
 # variants of the single-launch FFN that compute every output element from the same K-ordered MMAs:
 # (m-tile rows, second CTA skips A loads of <= 64-row tiles, max CTA pairs, gate/up N-tile-fastest order,
-# segment tails of <= n rows as swap-AB tiles)
-FFN_VARIANTS = [(256, 1, 0, 0, 0), (128, 1, 0, 0, 0), (128, 0, 0, 0, 0), (256, 0, 0, 0, 0), (256, 1, 3, 0, 0),
-                (128, 1, 1, 0, 0), (256, 1, 0, 1, 0), (128, 1, 0, 1, 0), (256, 1, 0, 0, 64), (128, 1, 0, 0, 64),
-                (256, 1, 0, 0, 32), (256, 1, 3, 0, 64), (128, 1, 1, 0, 48), (256, 0, 0, 1, 16)]
+# segment tails of <= n rows as swap-AB tiles, 256-row m-tiles carry merged tails, tile order: -1 auto /
+# 0 static / 1 dynamic)
+FFN_VARIANTS = [(256, 1, 0, 0, 0, 1, -1), (128, 1, 0, 0, 0, 1, -1), (128, 0, 0, 0, 0, 1, 1), (256, 0, 0, 0, 0, 0, 0),
+                (256, 1, 3, 0, 0, 1, -1), (128, 1, 1, 0, 0, 1, 1), (256, 1, 0, 1, 0, 1, 0), (128, 1, 0, 1, 0, 1, -1),
+                (256, 1, 0, 0, 64, 0, 1), (128, 1, 0, 0, 64, 1, -1), (256, 1, 0, 0, 32, 0, -1),
+                (256, 1, 3, 0, 64, 0, 0), (128, 1, 1, 0, 48, 1, -1), (256, 0, 0, 1, 16, 0, 1), (256, 1, 1, 0, 64, 1, -1),
+                (256, 1, 0, 1, 64, 1, 1), (256, 1, 2, 0, 64, 1, 0)]
 
 
 @pytest.mark.parametrize("T,d,skew", [(256, 5504, "zipf"), (2000, 264, None), (40, 136, "empty")])
@@ -362,7 +370,9 @@ def test_ffn_variants_bitwise_equal(rd, knob, T, d, skew):
     x, lg = x.to(DEV), torch.from_numpy(lg).to(DEV)
     wg, wu, wd = wg.to(DEV), wu.to(DEV), wd.to(DEV)
     outs = []
-    for mt, askip, pairs, order, swap in FFN_VARIANTS:
+    for mt, askip, pairs, order, swap, merge, dyn in FFN_VARIANTS:
+        knob("ffn_dyn", dyn)
+        knob("ffn_merge", merge)
         knob("ffn_swap", swap)
         knob("ffn_mt", mt)
         knob("ffn_askip", askip)
@@ -373,6 +383,53 @@ def test_ffn_variants_bitwise_equal(rd, knob, T, d, skew):
         ys = rd.expert_ffn(rd.dispatch(x, plan.dest, 1), plan.offsets, wg, wu, wd)
         outs.append((y, ys))
     torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1])
+
+
+# segment sizes around the tail merge: full 256-row m-tiles carrying remainders of 1..64 rows (one or two
+# tails), remainders past what is merged (three or more 64-row chunks, or more than the full m-tiles can carry:
+# their own M = 128 / M = 256 tile), exact multiples, empty and tiny segments
+MERGE_COUNTS = [257, 272, 273, 320, 512 + 65, 512 + 128, 768 + 192, 768 + 193, 1024 + 200, 256 + 65, 0, 5, 512,
+                256 + 63, 64, 1024 + 255]
+
+
+@pytest.mark.parametrize("H,d", [(256, 264), (4096, 384)])
+def test_ffn_merged_tails(rd, knob, H, d):
+    """256-row m-tiles with merged segment tails (the tail's swap-AB MMAs read the full m-tile's weight stages
+    and accumulate into the other accumulator's columns [192, 256)): vs the fp64 oracle, and bitwise equal to
+    tails as their own swap-AB tiles and as M = 128 tiles, through expert_ffn and the whole layer (gather
+    dispatch + row flags, fused residual scatter), on all pairs and on 1 and 3 CTA pairs."""
+    counts = MERGE_COUNTS
+    E = len(counts)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(off[-1])
+    xs = synth.to_torch(synth.tokens(rows, H, seed=21), "bf16").to(DEV)
+    wg, wu, wd = (synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=22))
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    offd = torch.from_numpy(off).to(DEV)
+    # logits that send exactly counts[e] tokens to expert e (the layer path routes them itself)
+    lg = np.full((rows, E), -5.0, dtype=np.float32)
+    lg[np.arange(rows), np.repeat(np.arange(E), counts)] = 5.0
+    perm = synth.rng(23, 0).permutation(rows)
+    lg = torch.from_numpy(lg[perm]).to(DEV)
+    x = xs  # token t goes to expert argmax(lg[t])
+    knob("ffn_mt", 256)
+    outs = []
+    for merge, swap, pairs, dyn in [(1, -1, 0, -1), (0, 64, 0, 0), (0, 0, 0, 1), (1, -1, 1, -1), (1, -1, 3, 0),
+                                    (1, -1, 0, 0), (1, -1, 2, 1)]:
+        knob("ffn_dyn", dyn)
+        knob("ffn_merge", merge)
+        knob("ffn_swap", swap)
+        knob("ffn_pairs", pairs)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        ys = rd.expert_ffn(xs, offd, *W, dev_status=st)
+        y, plan = rd.moe_layer(x, *W, logits=lg, residual=x)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0 and int(plan.dev_status.item()) == 0
+        outs.append((ys, y))
+    ref = oracle.expert_ffn(xs.cpu(), off, wg, wu, wd)
+    assert rel_err(_np(outs[0][0]), ref) <= BF16_TOL
     for o in outs[1:]:
         assert torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1])
 
