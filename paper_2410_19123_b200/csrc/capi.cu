@@ -93,18 +93,19 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
   return README_OK;
 }
 
-// Whether the dispatch runs in gather form with per-row readiness flags (the FFN overlapping it) or in
-// scatter form behind the FFN's whole-grid PDL wait. Gather pays off once the dispatch is long enough to
-// hide (config 2: -1..2 %, config 4: -3.6 %); for decode-sized batches (the dispatch is ~2 MB) the
-// scatter form measured ~3 us (1.5 %) faster per step (globaltimer traces, scripts/trace_lab.py), so it
-// stays below kGatherMinRows. Knob dispatch = 1 (scatter) | 2 (gather) overrides (A/B measurement).
-constexpr int64_t kGatherMinRows = 2048;
+// Whether the dispatch runs in gather form with per-row readiness flags (the FFN starting before it ends) or
+// in scatter form behind the FFN's whole-grid PDL wait. The gather form only overlaps while the FFN's CTAs
+// can be resident beside the dispatch's: with the FFN at 255 registers per thread (merged tails, dynamic tile
+// order) two of its warps fill an SM sub-partition's register file, so the FFN started only once the gather
+// kernel had ended; run inside the FFN launch instead (its epilogue warps gather the rows before their first
+// tile) the dispatch's traffic slowed the first tiles more than it saved. A/B on one box (bench.py, r02):
+// config 2 step 0.777 ms scatter / 0.786-0.789 fused / 0.796 gather kernel; config 4 58.05 / - / 58.85 ms.
+// So the default is scatter; knob dispatch = 2 (gather kernel) | 3 (gather inside the FFN) | 1 (scatter).
 bool gather_dispatch(int64_t rows) {
-  const int v = knob(Knob::kDispatch);
-  if (v == 1) return false;
-  if (v == 2) return true;
-  return rows >= kGatherMinRows;
+  (void)rows;
+  return knob(Knob::kDispatch) >= 2;
 }
+bool fused_gather_dispatch() { return knob(Knob::kDispatch) != 2; }
 
 // x_sorted row flags inside the FFN workspace (see ffn_layer_ready_bytes)
 uint32_t* ffn_xready(void* ws, int64_t rows, int32_t d, readme_dtype dt) {
@@ -114,7 +115,8 @@ uint32_t* ffn_xready(void* ws, int64_t rows, int32_t d, readme_dtype dt) {
 readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32_t H, int32_t E, int32_t d,
                       int32_t n_src, const int32_t* offsets, const void* w_gate, const void* w_up,
                       const void* w_down, const int32_t* src, const void* residual, void* out, void* ws,
-                      uint32_t* dev_status, cudaStream_t st, bool pdl = false, bool xready = false) {
+                      uint32_t* dev_status, cudaStream_t st, bool pdl = false, bool xready = false,
+                      const SelfDispatch* sd = nullptr) {
   readme_stream_t stream = reinterpret_cast<readme_stream_t>(st);
   if (merged_ffn(dt)) {
     uint32_t* ready = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + ffn_h_bytes(rows, d, dt));
@@ -123,7 +125,7 @@ readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32
                                  static_cast<const __nv_bfloat16*>(w_down), static_cast<__nv_bfloat16*>(ws),
                                  static_cast<__nv_bfloat16*>(out), src,
                                  static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st, nullptr, 0,
-                                 nullptr, pdl, xready ? ffn_xready(ws, rows, d, dt) : nullptr);
+                                 nullptr, pdl, xready ? ffn_xready(ws, rows, d, dt) : nullptr, sd);
   }
   README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
   return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, src, residual, out, stream);
@@ -405,6 +407,8 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
                        (!residual || aligned16(residual)),
                    "x, weights, residual and y must be 16-byte aligned");
   bool xready = false;
+  SelfDispatch sd_store{};
+  const SelfDispatch* sd = nullptr;  // a5 inside the FFN launch
   if (logits) {
     if (!src) src = src_ws;  // the fused path needs the inverse permutation
     README_TRY(check_route_call(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, ws_route,
@@ -423,7 +427,10 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
       xready = pdl && gather_dispatch(rows);
       README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                               ws_route, st, true, ready, ready_words));
-      if (xready)
+      if (xready && fused_gather_dispatch()) {
+        sd_store = SelfDispatch{static_cast<const __nv_bfloat16*>(x), src, k};
+        sd = &sd_store;
+      } else if (xready)
         README_TRY(launch_dispatch_gather(x, static_cast<size_t>(H) * dt_size(dt), rows, k, src, x_sorted,
                                           ffn_xready(ws_ffn, rows, d, dt), dev_status, st));
       else
@@ -443,11 +450,11 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
   if (fused) {
     // a6, then a7 with a8 fused into its epilogue: y[src[r]] = residual + h_r W_down^T (k == 1, weight 1).
     return run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, src, residual, y, ws_ffn,
-                   dev_status, reinterpret_cast<cudaStream_t>(stream), pdl, xready);
+                   dev_status, reinterpret_cast<cudaStream_t>(stream), pdl, xready, sd);
   }
   if (pdl) {
     README_TRY(run_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, nullptr, nullptr, y_sorted,
-                       ws_ffn, dev_status, reinterpret_cast<cudaStream_t>(stream), true, xready));
+                       ws_ffn, dev_status, reinterpret_cast<cudaStream_t>(stream), true, xready, sd));
   } else {
     README_TRY(readme_expert_ffn(x_sorted, dt, rows, H, E, d, 1, offsets, w_gate, w_up, w_down, y_sorted,
                                  dev_status, ws_ffn, ffn_ws_bytes(rows, d, dt), stream));

@@ -386,7 +386,14 @@ struct LayerArgs {
   int64_t vrows;
   int pdl;  // launched as a programmatic dependent of the dispatch: 1 = griddepcontrol.wait before reading
             // x_sorted; 2 = per-row readiness flags (xready) instead, so gate/up tiles start while the
-            // dispatch is still writing later experts' rows (the wait moves to the kernel's end)
+            // dispatch is still writing later experts' rows (the wait moves to the kernel's end); 3 = the
+            // kernel dispatches itself (dx below), as a programmatic dependent of the route
+  // pdl == 3 (a5 fused in): the epilogue warps, idle until the first accumulators are full, gather
+  // x_sorted[r] = x[dsrc[r] / dk] for r < drows in ascending waves and publish xready[r] per row
+  const uint4* dx;
+  const int32_t* dsrc;
+  void* dxs;     // x_sorted (the tensor map's buffer)
+  int dk, dvec;  // top-k; 16-byte vectors per row
   const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
   uint64_t* ttrace;        // measurement only (readme_debug_tile_trace): [pair][ttrace_max][8], normally null
@@ -673,23 +680,34 @@ __device__ __forceinline__ void drain_acc(const LayerArgs& la, const LTile& tl, 
   }
   if (tl.mode == 0) {
     __nv_bfloat16* orow = la.h + r * d;
-    for (int w = 0; w < ncols / 128; ++w) {
+    auto gu32 = [&](int hcol, const uint32_t (&gr)[32], const uint32_t (&ur)[32]) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(ur[j]);
+      if (valid) store_row_bf16x32(orow + hcol, v, d - hcol);
+    };
+    const int nw = ncols / 128;
+    if (hi_bar) {  // window 1 first: its up half is in registers
+      const int hcol1 = tl.n0 + (acc_off + 128) / 2;
+      uint32_t gr[32];
+      tc::tmem_ld32(tacc + 128u, gr);
+      tc::tmem_wait_ld();
+      gu32(hcol1, gr, hi0);
+      tc::tmem_ld32(tacc + 160u, gr);
+      tc::tmem_wait_ld();
+      gu32(hcol1 + 32, gr, hi1);
+    }
+#pragma unroll 1
+    for (int w = 0; w < (hi_bar ? 1 : nw); ++w) {
       const uint32_t wbase = tacc + static_cast<uint32_t>(w * 128);
       const int hcol0 = tl.n0 + (acc_off + w * 128) / 2;
-      const bool upreg = hi_bar && w == 1;  // window 1's up half already in registers
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 64; c += 32) {
         uint32_t gr[32], ur[32];
         tc::tmem_ld32(wbase + c, gr);
-        if (!upreg) tc::tmem_ld32(wbase + 64 + c, ur);
+        tc::tmem_ld32(wbase + 64 + c, ur);
         tc::tmem_wait_ld();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t u = upreg ? (c == 0 ? hi0[j] : hi1[j]) : ur[j];
-          v[j] = tc::silu(__uint_as_float(gr[j])) * __uint_as_float(u);
-        }
-        if (valid) store_row_bf16x32(orow + hcol0 + c, v, d - (hcol0 + c));
+        gu32(hcol0 + c, gr, ur);
       }
     }
     return;
@@ -773,6 +791,41 @@ __device__ __forceinline__ void tail_gu_epilogue(const LayerArgs& la, const LTil
   }
 }
 
+// a5 inside the expert FFN (pdl == 3): x_sorted[r] = x[src[r] / k], row r by warp r % nw of the grid's
+// epilogue warps (ascending waves: the first tiles' rows land first), 8 x 16 B loads in flight per lane, then
+// the row's flag (generic -> async proxy fence, release) for the producers' per-tile waits. Same per-row
+// protocol as dispatch_gather_kernel; a bad index is reported and its row still flagged.
+__device__ __forceinline__ void self_dispatch(const LayerArgs& la, int lane, int64_t gw, int64_t nw) {
+  constexpr int kU = 8;
+  const int vec = la.dvec;
+  const int64_t nrows = la.fz.rows;
+  uint4* xs = reinterpret_cast<uint4*>(la.dxs);
+  for (int64_t r = gw; r < nrows; r += nw) {
+    const int32_t sl = __ldg(la.dsrc + r);
+    if (sl < 0 || sl >= nrows) {
+      if (lane == 0 && la.dev_status) atomicOr(la.dev_status, README_DEV_BAD_INDEX);
+    } else {
+      const uint4* srow = la.dx + (sl / la.dk) * static_cast<int64_t>(vec);
+      uint4* drow = xs + r * vec;
+      int i = lane;
+      for (; i + (kU - 1) * kWarp < vec; i += kU * kWarp) {
+        uint4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = ld_nc_v4(srow + i + u * kWarp);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) st_v4(drow + i + u * kWarp, v[u]);
+      }
+      for (; i < vec; i += kWarp) st_v4(drow + i, ld_nc_v4(srow + i));
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(la.xready + r), "r"(1u) : "memory");
+    }
+  }
+}
+
 // Tile-id queue of the dynamic tile order (one per CTA, kTQ slots). Consumers pop in order; the leader's
 // producer pushes after every consumer released the slot. Ids >= the tile count end every role's loop.
 struct TileQ {
@@ -852,6 +905,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     }
   }
   if (warp == 1) tc::tmem_alloc<2>(&s.tmem_base, kTmemCols);
+  if (la.pdl == 3) tc::pdl_wait();  // the route's offsets and src
   // total m-tiles (every thread: nseg reads of the read-only offsets, no shared table)
   int mtiles = 0;
   for (int g = 0; g < nseg; ++g) mtiles += seg_mtiles<kMT>(__ldg(offs + g + 1) - __ldg(offs + g), merge);
@@ -940,7 +994,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint32_t bytes = tl.swap ? 2u * static_cast<uint32_t>(nact * 16 * 128 + 128 * 128)
                                      : 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128 + tact * 2048) -
                                            (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
-      if (tl.mode == 0 && la.pdl == 2) {
+      if (tl.mode == 0 && la.pdl >= 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
         // padding: their products are never stored, so they are not waited for), merged tail rows included
         const int mid = tl.mid;
@@ -1209,6 +1263,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   } else {
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
+    if (la.pdl == 3) self_dispatch(la, lane, static_cast<int64_t>(blockIdx.x) * 4 + (warp - 2),
+                                   static_cast<int64_t>(gridDim.x) * 4);
     Cursor cur;
     int i = 0;
     TileQ tq;
@@ -1397,8 +1453,12 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     __nv_bfloat16* y, const int32_t* src, const __nv_bfloat16* residual,
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
                                     const int32_t* expert_slot, int32_t n_slots, const PeerOut* peers,
-                                    bool pdl, const uint32_t* xready) {
+                                    bool pdl, const uint32_t* xready, const SelfDispatch* sd) {
   if (rows == 0) return README_OK;
+  if (sd && (!pdl || !xready || !sd->x || !sd->src || sd->k < 1 || (H * 2) % 16 != 0)) {
+    set_error("expert FFN self-dispatch needs PDL, row flags, x, src, k >= 1 and 16-byte rows");
+    return README_ERR_INVALID_ARG;
+  }
   if (nseg > kMaxSeg) {
     set_error("bf16 expert FFN supports at most %d segments (got %d)", kMaxSeg, nseg);
     return README_ERR_UNSUPPORTED;
@@ -1456,8 +1516,15 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   la.spin_limit = spin <= 0 ? 1u : (spin >= 31 ? (1u << 31) : (1u << spin));
   la.fz = Fuse{src, static_cast<int>(rows), residual};
   la.expert_slot = expert_slot;
-  la.pdl = pdl ? (xready ? 2 : 1) : 0;
+  la.pdl = sd ? 3 : (pdl ? (xready ? 2 : 1) : 0);
   la.xready = xready;
+  if (sd) {
+    la.dx = reinterpret_cast<const uint4*>(sd->x);
+    la.dsrc = sd->src;
+    la.dxs = const_cast<__nv_bfloat16*>(xs);
+    la.dk = sd->k;
+    la.dvec = H * 2 / 16;
+  }
   la.trace = g_trace_buf;
   la.ttrace = g_tile_trace;
   la.ttrace_max = g_tile_trace_max;

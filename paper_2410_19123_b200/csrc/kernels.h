@@ -90,6 +90,13 @@ struct PeerOut {
   int npeer;
   int64_t vrows;
 };
+// a5 fused into the single-launch FFN (launched as a programmatic dependent of the route): x_sorted[r] =
+// x[src[r] / k] gathered by the kernel's epilogue warps before their first tile, published per row in xready.
+struct SelfDispatch {
+  const __nv_bfloat16* x;  // [T, H] tokens
+  const int32_t* src;      // [T * k] slot of expert-contiguous row r
+  int32_t k;
+};
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg);
 size_t ffn_layer_xready_offset(int64_t rows);  // byte offset of the x_sorted row flags in `ready`
 
@@ -112,7 +119,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
                                     uint32_t* ready, uint32_t* dev_status, cudaStream_t st,
                                     const int32_t* expert_slot = nullptr, int32_t n_slots = 0,
                                     const PeerOut* peers = nullptr, bool pdl = false,
-                                    const uint32_t* xready = nullptr);
+                                    const uint32_t* xready = nullptr, const SelfDispatch* sd = nullptr);
 readme_status launch_gate_up_bf16(const __nv_bfloat16* xs, int64_t rows, int32_t H, int32_t E, int32_t d,
                                   int32_t nseg, const int32_t* offsets, const __nv_bfloat16* wg,
                                   const __nv_bfloat16* wu, __nv_bfloat16* h, cudaStream_t st);

@@ -27,7 +27,7 @@ constexpr KnobDef kDefs[static_cast<int>(Knob::kCount)] = {
     {"route", "README_ROUTE", 0},                  // 0 auto, 1 cluster (single launch), 2 lookback (multi-CTA)
     {"route_cluster", "README_ROUTE_CLUSTER", 0},  // 0 auto, else forced cluster size 1/2/4/8/16
     {"route_tile", "README_ROUTE_TILE", 0},        // 0 auto, else tokens per lookback tile
-    {"dispatch", "README_DISPATCH", 0},            // 0 auto, 1 scatter, 2 gather (inside moe_layer/stack)
+    {"dispatch", "README_DISPATCH", 0},            // 0 auto, 1 scatter, 2 gather kernel, 3 gather fused into the FFN (moe_layer)
     {"dispatch_bulk", "README_DISPATCH_BULK", -1}, // -1 auto, 0 warp-per-row, 1 bulk-copy scatter dispatch
     {"combine_bulk", "README_COMBINE_BULK", -1},   // -1 auto, 0 warp-per-row, 1 bulk-copy k=1 combine
     {"perm_unroll_d", "README_PERM_UNROLL_D", 4},  // 128-bit loads in flight per lane, scatter dispatch (4|8)
@@ -58,6 +58,7 @@ int parse_env(int i) {
     case Knob::kDispatch:
       if (strcmp(v, "scatter") == 0) return 1;
       if (strcmp(v, "gather") == 0) return 2;
+      if (strcmp(v, "fused") == 0) return 3;
       return 0;
     case Knob::kFfnKernel:
       if (strcmp(v, "split") == 0) return 1;

@@ -447,7 +447,7 @@ def _starve_setup(rd, T=8192, H=1024, d=1024, E=8):
     return x.to(DEV), lg, plan, xs, W, ref, n_hold
 
 
-def test_ffn_sm_starved_recovers(rd):
+def test_ffn_sm_starved_recovers(rd, knob):
     """140 of 148 SMs held by another stream's kernel for 0.3 s while the FFN launches: the few pairs that
     fit wait for the rest (bounded polls, far below the give-up limit) and the result is bitwise the
     uncontended one, dev_status clean."""
@@ -463,19 +463,22 @@ def test_ffn_sm_starved_recovers(rd):
     torch.cuda.synchronize()
     assert int(st.item()) == 0
     assert torch.equal(out, ref)
-    # the whole layer (gather dispatch with row flags, FFN behind it with PDL) under the same starvation
+    # the whole layer (dispatch, FFN behind it with PDL) under the same starvation: the default scatter
+    # dispatch, and the gather run by the FFN's own epilogue warps (row flags waited on per tile)
     y0, _ = rd.moe_layer(x, *W, logits=torch.from_numpy(lg).to(DEV), residual=x)
     torch.cuda.synchronize()
-    y1 = torch.full_like(y0, 7.0)
-    plan1 = rd.new_plan(x.shape[0], 8, 1, DEV)
-    torch.cuda.synchronize()
-    rd.debug_hold_sms(n_hold, 300_000_000, hold)
-    time.sleep(0.05)
-    with torch.cuda.stream(work):
-        rd.moe_layer(x, *W, logits=torch.from_numpy(lg).to(DEV), residual=x, plan=plan1, out=y1)
-    torch.cuda.synchronize()
-    assert int(plan1.dev_status.item()) == 0
-    assert torch.equal(y1, y0)
+    for form in (0, 3):
+        knob("dispatch", form)
+        y1 = torch.full_like(y0, 7.0)
+        plan1 = rd.new_plan(x.shape[0], 8, 1, DEV)
+        torch.cuda.synchronize()
+        rd.debug_hold_sms(n_hold, 300_000_000, hold)
+        time.sleep(0.05)
+        with torch.cuda.stream(work):
+            rd.moe_layer(x, *W, logits=torch.from_numpy(lg).to(DEV), residual=x, plan=plan1, out=y1)
+        torch.cuda.synchronize()
+        assert int(plan1.dev_status.item()) == 0
+        assert torch.equal(y1, y0)
 
 
 def test_ffn_sm_starved_gives_up_without_wrong_values(rd, knob):
@@ -514,18 +517,20 @@ def test_expert_ffn_segments_n_src(rd):
 
 # ---- whole layer -------------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("path", ["fused", "gather", "scatter", "lookback", "split", "unfused"])
+@pytest.mark.parametrize("path", ["fused", "gather-fused", "gather", "scatter", "lookback", "split", "unfused"])
 @pytest.mark.parametrize("dt,T,H,d,E,k", [("f32", 256, 64, 128, 8, 1), ("f32", 256, 64, 128, 8, 2),
                                            ("bf16", 1500, 512, 640, 8, 1), ("bf16", 600, 256, 256, 8, 2),
                                            ("bf16", 3000, 1024, 1376, 8, 1)])
 def test_moe_layer_end_to_end(rd, knob, path, dt, T, H, d, E, k):
     # fused: cluster route -> gather dispatch with per-row flags -> single-launch FFN waiting per tile;
     # lookback: multi-CTA route -> finalize fused into the dispatch -> FFN behind a whole-grid PDL wait
-    # gather / scatter force the dispatch form (by default gather from 2048 rows up)
+    # gather-fused / gather / scatter force the dispatch form (default: scatter, the FFN behind it as a PDL
+    # dependent; "gather" = the gather kernel publishing row flags, "gather-fused" = the same gather run by
+    # the FFN launch's own epilogue warps)
     if path == "lookback":
         knob("route", 2)
-    elif path in ("gather", "scatter"):
-        knob("dispatch", 2 if path == "gather" else 1)
+    elif path in ("gather-fused", "gather", "scatter"):
+        knob("dispatch", {"gather-fused": 3, "gather": 2, "scatter": 1}[path])
     elif path != "fused":
         knob("ffn_kernel", FFN_KERNEL[path])
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, dt, seed=T * 3 + 1)
@@ -535,6 +540,24 @@ def test_moe_layer_end_to_end(rd, knob, path, dt, T, H, d, E, k):
     yref, pref = oracle.moe_layer(x, lg, k, wg, wu, wd, residual=res)
     _check_plan(plan, pref, k)
     assert rel_err(_np(y), yref) <= (BF16_TOL if dt == "bf16" else F32_TOL)
+
+
+@pytest.mark.parametrize("T,k,d", [(2500, 1, 512), (1300, 2, 264), (700, 1, 5504)])
+def test_moe_layer_dispatch_forms_bitwise(rd, knob, T, k, d):
+    """a5 as a scatter kernel, as a gather kernel with per-row flags, and inside the FFN launch (its epilogue
+    warps gather the rows before their first tile): the same x_sorted, so the same layer output bit for bit,
+    clean dev_status."""
+    H, E = 4096 if d == 5504 else 512, 8
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "bf16", seed=T + k)
+    x, lg, W = x.to(DEV), torch.from_numpy(lg).to(DEV), [w.to(DEV) for w in (wg, wu, wd)]
+    outs = []
+    for form in (1, 2, 3):
+        knob("dispatch", form)
+        y, plan = rd.moe_layer(x, *W, k=k, logits=lg, residual=x)
+        torch.cuda.synchronize()
+        assert int(plan.dev_status.item()) == 0
+        outs.append(y)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
 
 
 def _fuzz_cases(n=24, seed=2410):
