@@ -5,9 +5,9 @@ Usage: python scripts/tile_trace_analyze.py RUN.json RECORDS.npy [MERGE=1]  (mea
 import json, numpy as np, sys
 d=json.load(open(sys.argv[1])); rec=np.load(sys.argv[2]).astype(np.uint64).astype(np.float64)
 MERGE=int(sys.argv[3]) if len(sys.argv)>3 else 1
-H,dd=4096,5504
+H,dd=d.get('H',4096),d.get('d',5504)
 counts=d['counts']; offs=np.concatenate([[0],np.cumsum(counts)])
-NT1,NT2=(dd+127)//128,(H+255)//256; KB1,KB2=H//64,(dd+63)//64
+NT1,NT2=(dd+127)//128,(H+255)//256; KB1,KB2=(H+63)//64,(dd+63)//64
 def seg_tiles(R):
     if not MERGE or R < 256: return [(min(256, R-256*m),0) for m in range((R+255)//256)]
     nf,rem=R>>8,R&255

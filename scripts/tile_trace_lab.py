@@ -17,14 +17,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2410_19123_b200 import readme as rd  # noqa: E402
 
-T, H, E, d = int(os.environ.get("TT_T", "8192")), 4096, 8, 5504
+T, H, E, d = int(os.environ.get("TT_T", "8192")), int(os.environ.get("TT_H", "4096")), 8, int(os.environ.get("TT_D", "5504"))
 K = int(os.environ.get("TT_K", "1"))
 REPS = int(os.environ.get("TT_REPS", "5"))
 MAXT = 64
 g = torch.Generator(device="cuda").manual_seed(1)
 wg = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wu = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
-wd = (torch.randn(E, H, d, device="cuda", generator=g) / 74).bfloat16()
+wd = (torch.randn(E, H, d, device="cuda", generator=g) / (d ** 0.5)).bfloat16()
 x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
 lg = torch.from_numpy(synth.router_logits(T, E)).cuda()
 plan = rd.new_plan(T, E, K, "cuda")
@@ -143,7 +143,7 @@ for it in range(REPS):
                       "full_wait_cyc": v[3] / v[0]} for k, v in sorted(per_kind.items())},
     })
 rd.lib().readme_debug_tile_trace(None, 0)
-out = {"T": T, "k": K, "counts": np.diff(offs).tolist(), "runs": res}
+out = {"T": T, "H": H, "d": d, "k": K, "counts": np.diff(offs).tolist(), "runs": res}
 os.makedirs("gpurun_out", exist_ok=True)
 np.save("gpurun_out/tile_trace_last.npy", tt.view(NP, MAXT, 8).cpu().numpy())
 print(json.dumps(out, indent=1))
