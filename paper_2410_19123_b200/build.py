@@ -53,7 +53,8 @@ def stale() -> bool:
 
 def _compile(src: str, verbose: bool) -> tuple[str, str]:
     obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
-    cmd = [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", obj]
+    # README_NVCC_EXTRA: extra nvcc flags for lab builds only (A/B of compile-time variants); unset normally
+    cmd = [nvcc()] + NVCC_FLAGS + os.environ.get("README_NVCC_EXTRA", "").split() + ["-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{' '.join(cmd)}\n{p.stdout}\n{p.stderr}")

@@ -865,8 +865,14 @@ __device__ __forceinline__ void tq_push(SM& s, TileQ& q, int t, int lane) {
   q.next();
 }
 
+// Lab builds only (README_NVCC_EXTRA=-DREADME_FFN_MAXREG=n): cap the single-launch kernel's registers.
+#ifdef README_FFN_MAXREG
+#define README_FFN_BOUNDS __maxnreg__(README_FFN_MAXREG)
+#else
+#define README_FFN_BOUNDS __launch_bounds__(kThreads, 1)
+#endif
 template <int kFuse, int kMT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) README_FFN_BOUNDS
 ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX16,

@@ -308,7 +308,10 @@ finalize_dispatch_kernel(const uint4* __restrict__ x, int vec, int64_t nslots, i
 // registers — hence ONE CTA of 12 warps per SM. The TMA (async proxy) reads x_sorted, hence the proxy
 // fence before the flag.
 constexpr int kGatherUnroll = 8;
-constexpr int kGatherThreads = 384;
+#ifndef README_GATHER_THREADS  // lab builds may shrink it (README_NVCC_EXTRA)
+#define README_GATHER_THREADS 384
+#endif
+constexpr int kGatherThreads = README_GATHER_THREADS;
 __global__ void __maxnreg__(64)
 dispatch_gather_kernel(const uint4* __restrict__ x, int vec, int64_t nrows, int k, const int32_t* __restrict__ src,
                        uint4* __restrict__ xs, uint32_t* __restrict__ xready, uint32_t* __restrict__ dev_status,
