@@ -826,6 +826,69 @@ __device__ __forceinline__ void self_dispatch(const LayerArgs& la, int lane, int
   }
 }
 
+// Epilogue of a merged down tail (same two-M = 128 layout as tail_gu_epilogue): lane l < 64 holds output column
+// n0 + 128 cta + l (first MMA, columns [0, N/2) of the region) and n0 + 128 cta + 64 + l (second, [32, 32 + N/2))
+// for tail rows [0, N/2), lane 64 + l the same columns for rows [N/2, N). Each row goes where the normal down
+// epilogue sends it (y_sorted, y[src[r]] + residual, or the source rank's row).
+template <int kFuse>
+__device__ __forceinline__ void tail_dn_epilogue(const LayerArgs& la, const LTile& tt, uint32_t tacc, uint32_t cta,
+                                                 int q, int lane, bool store, uint64_t* hi_bar) {
+  const int H = la.H;
+  const int half = ((tt.rows + 15) & ~15) / 2;
+  uint32_t ra[32], rb[32];
+  tc::tmem_ld32(tacc, ra);
+  tc::tmem_ld32(tacc + 32u, rb);
+  tc::tmem_wait_ld();
+  release_cols(hi_bar, lane);
+  if (!store) return;
+  const int cola = tt.n0 + 128 * static_cast<int>(cta) + 32 * (q & 1) + lane, colb = cola + 64;
+  const int tok0 = (q >> 1) * half;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int tok = tok0 + j;
+    if (j >= half || tok >= tt.rows) break;  // warp-uniform
+    const int64_t rr = tt.m0 + tok;
+    __nv_bfloat16* orow;
+    const __nv_bfloat16* rrow = nullptr;
+    bool vrow = true;
+    if constexpr (kFuse == 2) {
+      const int64_t v = static_cast<int64_t>(__ldg(la.fz.src + rr));
+      vrow = v >= 0 && v < la.vrows * la.npeer;
+      const int p = vrow ? static_cast<int>(v / la.vrows) : 0;
+      const int64_t i = vrow ? v - p * la.vrows : 0;
+      __nv_bfloat16* py = la.peer_y[0];
+      const __nv_bfloat16* pr = la.peer_res[0];
+#pragma unroll
+      for (int jj = 1; jj < kMaxPeers; ++jj)
+        if (p == jj) {
+          py = la.peer_y[jj];
+          pr = la.peer_res[jj];
+        }
+      orow = py + i * H;
+      rrow = pr ? pr + i * H : nullptr;
+    } else {
+      int64_t oi = rr;
+      if constexpr (kFuse == 1) {
+        oi = la.fz.src ? static_cast<int64_t>(__ldg(la.fz.src + rr)) : rr;
+        vrow = oi >= 0 && oi < la.fz.rows;
+        if (!vrow) oi = 0;
+        rrow = la.fz.residual ? la.fz.residual + oi * H : nullptr;
+      }
+      orow = la.y + oi * H;
+    }
+    if (!vrow) continue;
+    float va = __uint_as_float(ra[j]), vb = __uint_as_float(rb[j]);
+    if (cola < H) {
+      if (rrow) va += __bfloat162float(rrow[cola]);
+      orow[cola] = __float2bfloat16_rn(va);
+    }
+    if (colb < H) {
+      if (rrow) vb += __bfloat162float(rrow[colb]);
+      orow[colb] = __float2bfloat16_rn(vb);
+    }
+  }
+}
+
 // Tile-id queue of the dynamic tile order (one per CTA, kTQ slots). Consumers pop in order; the leader's
 // producer pushes after every consumer released the slot. Ids >= the tile count end every role's loop.
 struct TileQ {
@@ -1179,11 +1242,11 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const bool tail = tl.trows > 0;
         const int oth = acc ^ 1;
         const uint32_t t_tmem = tmem_base + static_cast<uint32_t>(oth * 256 + 192);
-        // down tails: one M = 256 swap-AB MMA per K step (lane = output column); gate/up tails: two M = 128 ones,
-        // the CTA's 64 gate rows then its 64 up rows, into columns +0 / +32 (both factors of a neuron in one lane)
-        const uint32_t tidesc = tl.mode == 0 ? tc::idesc_bf16(128, (tl.trows + 15) & ~15)
-                                             : tc::idesc_bf16(256, (tl.trows + 15) & ~15);
-        const bool gu_tail = tl.mode == 0;
+        // two M = 128 swap-AB pair MMAs per K step, the first 64 then the last 64 of the CTA's 128 weight rows
+        // (gate/up: its 64 gate rows, then its 64 up rows, so both factors of a neuron share a lane; down: output
+        // columns +0..63, +64..127), into columns +0 / +32 of the borrowed region. Per weight byte re-read they ran
+        // faster than one M = 256 MMA (~25 vs ~63 cycles per MMA, tile trace, profiles/SUMMARY.md r02).
+        const uint32_t tidesc = tc::idesc_bf16(128, (tl.trows + 15) & ~15);
         uint32_t tpar = 0;
         bool tok = true;
         if (tail) {
@@ -1205,9 +1268,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const uint32_t acc_flag = (kbp | kk) != 0 ? 1u : 0u;
                 tc::mma_f16<2>(t_tmem, wd + static_cast<uint64_t>(kk * 2), td + static_cast<uint64_t>(kk * 2), tidesc,
                                acc_flag);
-                if (gu_tail)  // the up rows: 64 rows (8 KB) further into the weight stage
-                  tc::mma_f16<2>(t_tmem + 32u, wd + static_cast<uint64_t>((64 * 128 >> 4) + kk * 2),
-                                 td + static_cast<uint64_t>(kk * 2), tidesc, acc_flag);
+                // the second 64 weight rows: 8 KB further into the stage
+                tc::mma_f16<2>(t_tmem + 32u, wd + static_cast<uint64_t>((64 * 128 >> 4) + kk * 2),
+                               td + static_cast<uint64_t>(kk * 2), tidesc, acc_flag);
               }
               tc::commit_2sm_mc(&s.empty[st], 0x3);
             }
@@ -1306,7 +1369,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         tt.rows = tl.trows;
         const uint32_t ttacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>((acc ^ 1) * 256 + 192);
         if (tl.mode == 0) tail_gu_epilogue(la, tt, ttacc, cta, q, lane, !aborted, &s.hi_free[acc ^ 1]);
-        else swap_epilogue<kFuse>(la, tt, ttacc, cta, q, lane, !aborted, &s.hi_free[acc ^ 1]);
+        else tail_dn_epilogue<kFuse>(la, tt, ttacc, cta, q, lane, !aborted, &s.hi_free[acc ^ 1]);
       }
       if (tl.swap) swap_epilogue<kFuse>(la, tl, tacc, cta, q, lane, !aborted);
       else drain_acc<kFuse>(la, tl, tacc, row_in_tile, ncols, acc_off, row_in_tile < tl.rows && !aborted,
