@@ -21,11 +21,11 @@ B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 run ncu_launch 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B
 EXTRA=sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum
 run ncu_ffn 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:ffn_layer2 -s 2 -c 1 -o $O/prof_ffn $B
-run ncu_perm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"route_cluster|dispatch_gather" -s 2 -c 2 -o $O/prof_perm $B
+run ncu_perm 900 ncu --set full --metrics $EXTRA --clock-control none --import-source on -k regex:"route_cluster|move_rows_bulk" -s 2 -c 2 -o $O/prof_perm $B
 B3="python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
 run ncu_dec 900 ncu --set full --metrics $EXTRA --clock-control none -k regex:ffn_layer2 -s 3 -c 1 -o $O/prof_dec $B3
 cat $O/summary.txt
 # compute-sanitizer over the FFN, route and permutation tests (full-size cases excluded)
 run sanitize_mem 1500 compute-sanitizer --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "not full and not config and not starved and not offload and not stack"
-run sanitize_sync 1500 compute-sanitizer --tool synccheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "ffn_variants or tile_edges or teacher_forced"
+run sanitize_sync 1500 compute-sanitizer --tool synccheck --error-exitcode 1 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "ffn_variants or tile_edges or teacher_forced or merged_tails or dispatch_forms"
 tail -n 3 $O/sanitize_mem.log; tail -n 3 $O/sanitize_sync.log
