@@ -26,7 +26,13 @@ wg = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wu = (torch.randn(E, d, H, device="cuda", generator=g) / 64).bfloat16()
 wd = (torch.randn(E, H, d, device="cuda", generator=g) / (d ** 0.5)).bfloat16()
 x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
-lg = torch.from_numpy(synth.router_logits(T, E)).cuda()
+U = int(os.environ.get("TT_U", "0"))  # > 0: tokens spread evenly over experts 0..U-1 (decode studies)
+if U > 0:
+    lgn = np.full((T, E), -4.0, dtype=np.float32)
+    lgn[np.arange(T), np.arange(T) % U] = 4.0
+    lg = torch.from_numpy(lgn).cuda()
+else:
+    lg = torch.from_numpy(synth.router_logits(T, E)).cuda()
 plan = rd.new_plan(T, E, K, "cuda")
 ws = torch.empty(rd.moe_layer_workspace_bytes(T, H, E, d, K, torch.bfloat16), dtype=torch.uint8, device="cuda")
 y = torch.empty_like(x)
