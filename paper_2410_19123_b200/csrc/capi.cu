@@ -100,7 +100,10 @@ readme_status zero_ready(void* ws, int64_t rows, int32_t d, readme_dtype dt, int
 // kernel had ended; run inside the FFN launch instead (its epilogue warps gather the rows before their first
 // tile) the dispatch's traffic slowed the first tiles more than it saved. A/B on one box (bench.py, r02):
 // config 2 step 0.777 ms scatter / 0.786-0.789 fused / 0.796 gather kernel; config 4 58.05 / - / 58.85 ms.
-// So the default is scatter; knob dispatch = 2 (gather kernel) | 3 (gather inside the FFN) | 1 (scatter).
+// The in-FFN gather was then paced (rows of the next segment copied while an epilogue warp waits for an
+// accumulator; one copied-row counter per segment instead of per-row flags): config 2 step 0.785-0.786 ms vs
+// 0.783-0.787 scatter on one box — level, not better. So the default stays scatter; knob dispatch = 2 (gather
+// kernel) | 3 (gather inside the FFN) | 1 (scatter).
 bool gather_dispatch(int64_t rows) {
   (void)rows;
   return knob(Knob::kDispatch) >= 2;

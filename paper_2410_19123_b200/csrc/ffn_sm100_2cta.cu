@@ -404,6 +404,7 @@ struct LayerArgs {
   int merge;               // 256-row m-tiles: segment tails ride on full m-tiles (knob ffn_merge; 0 = separate)
   int dyn;                 // dynamic tile order: tiles after each pair's first claimed from tile_ctr (knob ffn_dyn)
   uint32_t* tile_ctr;      // zeroed word of the readiness region (dyn)
+  uint32_t* seg_rows;      // pdl == 3: [nseg] rows of each segment copied so far (zeroed readiness words)
   int claim_ahead;         // dyn: K steps before the end of a tile's loads at which the next tile is claimed
 };
 
@@ -631,6 +632,7 @@ struct __align__(8) SmemLT {
   int tq[kTQ];
   uint32_t tmem_base;
   uint32_t xok[kXokWords];  // pdl == 2: bit per m-tile, this CTA's A rows seen ready
+  uint32_t segok[kMaxSeg / 32];  // pdl == 3: bit per segment, all its rows seen copied
 };
 constexpr int kStagesL = 6;
 constexpr int kStagesLD = 9;
@@ -791,37 +793,57 @@ __device__ __forceinline__ void tail_gu_epilogue(const LayerArgs& la, const LTil
   }
 }
 
-// a5 inside the expert FFN (pdl == 3): x_sorted[r] = x[src[r] / k], row r by warp r % nw of the grid's
-// epilogue warps (ascending waves: the first tiles' rows land first), 8 x 16 B loads in flight per lane, then
-// the row's flag (generic -> async proxy fence, release) for the producers' per-tile waits. Same per-row
-// protocol as dispatch_gather_kernel; a bad index is reported and its row still flagged.
-__device__ __forceinline__ void self_dispatch(const LayerArgs& la, int lane, int64_t gw, int64_t nw) {
+// a5 inside the expert FFN (pdl == 3): x_sorted[r] = x[src[r] / k]. Row r belongs to epilogue warp r % nw of
+// the grid; a warp copies its rows in ascending order while it waits for an accumulator, but only rows up to the
+// end of the segment after the one its awaited tile belongs to — so the 128 MB of row moves spread over the
+// gate/up phase (a segment's rows land while the previous segment's tiles run) instead of competing for HBM
+// with the first tiles' weights, and every row a running tile needs is copied by warps that are themselves
+// waiting on tiles of that segment or earlier (which complete: their rows were copied first). Rows left when
+// a warp runs out of tiles are copied before it exits. Per row: 8 x 16 B loads in flight per lane, then the
+// row's flag (generic -> async proxy fence, release) for the producers' per-tile waits; a bad index is
+// reported and its row still flagged.
+struct RowCopier {
+  int64_t next, step;  // this warp's next row, and the stride (epilogue warps in the grid)
+  int seg;             // segment of `next` (rows ascend, so a cursor)
+};
+__device__ __forceinline__ void copy_row(const LayerArgs& la, int64_t r, int lane, RowCopier& rc) {
   constexpr int kU = 8;
   const int vec = la.dvec;
   const int64_t nrows = la.fz.rows;
-  uint4* xs = reinterpret_cast<uint4*>(la.dxs);
-  for (int64_t r = gw; r < nrows; r += nw) {
-    const int32_t sl = __ldg(la.dsrc + r);
-    if (sl < 0 || sl >= nrows) {
-      if (lane == 0 && la.dev_status) atomicOr(la.dev_status, README_DEV_BAD_INDEX);
-    } else {
-      const uint4* srow = la.dx + (sl / la.dk) * static_cast<int64_t>(vec);
-      uint4* drow = xs + r * vec;
-      int i = lane;
-      for (; i + (kU - 1) * kWarp < vec; i += kU * kWarp) {
-        uint4 v[kU];
+  const int32_t sl = __ldg(la.dsrc + r);
+  if (sl < 0 || sl >= nrows) {
+    if (lane == 0 && la.dev_status) atomicOr(la.dev_status, README_DEV_BAD_INDEX);
+  } else {
+    const uint4* srow = la.dx + (sl / la.dk) * static_cast<int64_t>(vec);
+    uint4* drow = reinterpret_cast<uint4*>(la.dxs) + r * vec;
+    int i = lane;
+    for (; i + (kU - 1) * kWarp < vec; i += kU * kWarp) {
+      uint4 v[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) v[u] = ld_nc_v4(srow + i + u * kWarp);
+      for (int u = 0; u < kU; ++u) v[u] = ld_nc_v4(srow + i + u * kWarp);
 #pragma unroll
-        for (int u = 0; u < kU; ++u) st_v4(drow + i + u * kWarp, v[u]);
-      }
-      for (; i < vec; i += kWarp) st_v4(drow + i, ld_nc_v4(srow + i));
+      for (int u = 0; u < kU; ++u) st_v4(drow + i + u * kWarp, v[u]);
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(la.xready + r), "r"(1u) : "memory");
+    for (; i < vec; i += kWarp) st_v4(drow + i, ld_nc_v4(srow + i));
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncwarp();
+  while (rc.seg + 1 < la.nseg && r >= __ldg(la.offsets + rc.seg + 1)) ++rc.seg;
+  if (lane == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(la.seg_rows + rc.seg) : "memory");
+  }
+}
+// Wait for an accumulator phase, copying this warp's rows below `limit` meanwhile.
+__device__ __forceinline__ void wait_copying(const LayerArgs& la, uint64_t* bar, uint32_t parity, RowCopier& rc,
+                                             int64_t limit, int lane) {
+  while (!__all_sync(0xffffffffu, tc::mbar_test_cluster(bar, parity))) {
+    if (rc.next < limit) {
+      copy_row(la, rc.next, lane, rc);
+      rc.next += rc.step;
+    } else {
+      tc::mbar_wait_cluster(bar, parity);
+      break;
     }
   }
 }
@@ -960,6 +982,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   const uint32_t ready_target = static_cast<uint32_t>(NT1) * 8u;
 
   for (int i = tid; i < kXokWords; i += kThreads) s.xok[i] = 0u;
+  for (int i = tid; i < kMaxSeg / 32; i += kThreads) s.segok[i] = 0u;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmX);
     tc::prefetch_tmap(&tmG);
@@ -1063,7 +1086,27 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const uint32_t bytes = tl.swap ? 2u * static_cast<uint32_t>(nact * 16 * 128 + 128 * 128)
                                      : 2u * static_cast<uint32_t>(a_rows * 128 + 128 * 128 + tact * 2048) -
                                            (a_skip ? static_cast<uint32_t>(a_rows * 128) : 0u);
-      if (tl.mode == 0 && la.pdl >= 2) {
+      if (tl.mode == 0 && la.pdl == 3) {
+        // a5 inside this launch: wait until every row of the tile's segment is copied (one counter per
+        // segment, seen once per CTA), not per row: the per-row flag polls at every new m-tile cost the
+        // producer ~1.5 us each
+        const int g = tl.g;
+        if (!(s.segok[g >> 5] >> (g & 31) & 1u)) {
+          const uint32_t need = static_cast<uint32_t>(__ldg(offs + g + 1) - __ldg(offs + g));
+          uint32_t spins = 0;
+          while (ld_acquire_u32(la.seg_rows + g) < need) {
+            __nanosleep(64);
+            if (++spins >= la.spin_limit) {
+              if (lane == 0) sched_give_up(la);
+              break;
+            }
+          }
+          if (lane == 0) s.segok[g >> 5] |= 1u << (g & 31);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __syncwarp();
+        }
+      }
+      if (tl.mode == 0 && la.pdl == 2) {
         // wait until the dispatch has written this CTA's A rows of the tile (rows past the segment's end are
         // padding: their products are never stored, so they are not waited for), merged tail rows included
         const int mid = tl.mid;
@@ -1332,8 +1375,8 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
   } else {
     // ===== epilogue: warps 2..5 of both CTAs =====
     const int q = warp & 3;
-    if (la.pdl == 3) self_dispatch(la, lane, static_cast<int64_t>(blockIdx.x) * 4 + (warp - 2),
-                                   static_cast<int64_t>(gridDim.x) * 4);
+    RowCopier rc{static_cast<int64_t>(blockIdx.x) * 4 + (warp - 2), static_cast<int64_t>(gridDim.x) * 4, 0};
+    if (la.pdl != 3) rc.next = la.fz.rows;  // nothing to copy
     Cursor cur;
     int i = 0;
     TileQ tq;
@@ -1342,7 +1385,13 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       const LTile tl = decode_ltile<kMT>(offs, t, nseg, T1, NT1, NT2, la.swap_rows, cur, la.order != 0, merge);
       const int acc = i & 1;
       const uint32_t use = static_cast<uint32_t>(i >> 1);
-      tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
+      if (rc.next < la.fz.rows) {
+        // rows up to the end of the segment after this tile's (gate/up phase), or all of them (down phase)
+        const int64_t limit = tl.mode == 0 ? static_cast<int64_t>(__ldg(offs + min(tl.g + 2, nseg))) : la.fz.rows;
+        wait_copying(la, &s.tfull[acc], use & 1u, rc, limit, lane);
+      } else {
+        tc::mbar_wait_cluster(&s.tfull[acc], use & 1u);
+      }
       tc::fence_after();
       uint64_t* trec = (la.ttrace && leader && q == 2 && lane == 0 && i < la.ttrace_max)
                            ? la.ttrace + (static_cast<int64_t>(pair) * la.ttrace_max + i) * 8 : nullptr;
@@ -1390,6 +1439,7 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         }
       }
     }
+    for (; rc.next < la.fz.rows; rc.next += rc.step) copy_row(la, rc.next, lane, rc);  // rows not copied yet
   }
 
   if constexpr (kFuse == 2) __threadfence_system();  // remote rows performed before the ready signal
@@ -1507,9 +1557,10 @@ readme_status launch_down_bf16(const __nv_bfloat16* h, int64_t rows, int32_t H, 
 // Readiness region of the single-launch kernel: [down-tile counters: kMaxSeg + #128-row m-tiles][abort word]
 // [pad][x_sorted row flags: rows] (the flags are used when the gather dispatch precedes the FFN, pdl == 2);
 // one memset (or the route launch) zeroes all of it before every launch.
-int64_t ffn_layer_abort_index(int64_t rows) { return kMaxSeg + (rows + 127) / 128 + 1; }  // then the tile counter
+// then the tile counter, then kMaxSeg per-segment copied-row counters
+int64_t ffn_layer_abort_index(int64_t rows) { return kMaxSeg + (rows + 127) / 128 + 1; }
 size_t ffn_layer_xready_offset(int64_t rows) {
-  return align_up(static_cast<size_t>(ffn_layer_abort_index(rows) + 2) * sizeof(uint32_t), 256);
+  return align_up(static_cast<size_t>(ffn_layer_abort_index(rows) + 2 + kMaxSeg) * sizeof(uint32_t), 256);
 }
 size_t ffn_layer_ready_bytes(int64_t rows, int32_t nseg) {
   (void)nseg;
@@ -1613,6 +1664,7 @@ readme_status launch_ffn_layer_2cta(const __nv_bfloat16* xs, int64_t rows, int32
   la.dyn = kdyn < 0 ? (mt == 256 && !big ? 1 : 0) : (kdyn != 0 ? 1 : 0);
   la.merge = mt == 256 && (kmerge < 0 ? la.dyn != 0 : kmerge != 0);
   la.tile_ctr = la.abort + 1;
+  la.seg_rows = la.abort + 2;
   la.claim_ahead = std::max(1, knob(Knob::kFfnClaim));
   const int fuse = peers ? 2 : ((src || residual) ? 1 : 0);
   if (peers) {
