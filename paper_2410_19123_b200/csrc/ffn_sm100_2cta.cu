@@ -1,20 +1,23 @@
-// ffn_sm100_2cta.cu — a6/a7 grouped expert GEMMs on CTA pairs (tcgen05.mma.cta_group::2), bf16.
+// ffn_sm100_2cta.cu — a6/a7 (+ a8 for k = 1) grouped expert GEMMs on CTA pairs (tcgen05.mma.cta_group::2), bf16.
 //
-// Same math as ffn_sm100.cu (SwiGLU reading Q4):
-//     kMode 0:  h_r = silu(x_r . W_gate[e]^T) * (x_r . W_up[e]^T)      kMode 1:  y_r = h_r . W_down[e]^T
-// but each tile is computed by a CLUSTER OF TWO CTAs on two SMs of a TPC: one tcgen05.mma.cta_group::2
-// (issued by the even CTA) multiplies A rows held in both CTAs' shared memory by a 256-column B tile
-// whose halves live in the two CTAs, accumulating into both CTAs' TMEM. Per SM this halves the B bytes
-// staged per MMA (32 KB per 64-deep K stage instead of 48 KB), so a 6-deep TMA ring fits and the L2->SM
-// traffic per FLOP drops by a third — the v1 profile showed the MMA warp waiting on TMA data ~13 % of
-// the time with a 4-deep ring (profiles/SUMMARY.md).
+//     a6:  h_r = silu(x_r . W_gate[e]^T) * (x_r . W_up[e]^T)        a7:  y_r = h_r . W_down[e]^T
+// (PAPER.md:159 with the SwiGLU reading Q4; e = the expert owning row r's segment). Every tile is computed by a
+// CLUSTER OF TWO CTAs on the two SMs of a TPC: one tcgen05.mma.cta_group::2 (issued by the even CTA) multiplies
+// A rows held in both CTAs' shared memory by a 256-column B tile whose halves live in the two CTAs, accumulating
+// into both CTAs' TMEM — per SM 32 KB of TMA traffic per 64-deep K stage for a 256 x 256 pair tile.
 //
-// Tiles: 256 rows x 256 accumulator columns (M=256 MMA, each CTA 128 rows, TMEM lane = row). The last
-// tile of an expert with <= 128 remaining rows runs as an M=128 MMA (each CTA 64 rows; CUTLASS's "2x2"
-// TMEM layout: lanes 0-63 hold accumulator columns [0,128), lanes 64-127 columns [128,256) of the same
-// rows), so padding waste stays at the 128-row granularity of v1.
-// GEMM1 B operand per CTA r: 64 rows of W_gate then the same 64 rows of W_up (neurons n0+64r ..), so in
-// accumulator column space gate column c pairs with up column c+64 inside every 128-column window.
+// Two kernels:
+//   ffn_gemm2_kernel   one projection per launch (readme_expert_gate_up / readme_expert_down, the split form);
+//   ffn_layer2_kernel  the whole expert FFN in ONE persistent launch (readme_expert_ffn, moe_layer, moe_stack,
+//                      the permanent expert, expert parallelism): [gate/up tiles][down tiles], down tiles waiting
+//                      on per-m-tile readiness counters; 256-row m-tiles for prefill (segment tails of <= 64 rows
+//                      merged into full m-tiles, dynamic tile order, at <= 16384 rows) and 128-row m-tiles with a
+//                      9-stage ring for decode. DESIGN.md §6 has the design and the measurements behind it.
+// Tile shapes: 256 rows x 256 accumulator columns (M=256 MMA, each CTA 128 rows, TMEM lane = row); an m-tile of
+// <= 128 rows runs as an M=128 MMA (each CTA 64 rows; the "2x2" TMEM layout: lanes 0-63 hold accumulator
+// columns [0,128), lanes 64-127 columns [128,256) of the same rows). Gate/up B operand per CTA r: 64 rows of
+// W_gate then the same 64 rows of W_up (neurons n0+64r ..), so in accumulator column space gate column c pairs
+// with up column c+64 inside every 128-column window.
 #include <stdlib.h>
 
 #include <mutex>
