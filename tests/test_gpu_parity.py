@@ -588,6 +588,45 @@ def test_moe_layer_fuzz_bf16(rd, T, E, k, H, d):
     assert rel_err(_np(y), yref) <= BF16_TOL
 
 
+def _tail_fuzz_cases(n=12, seed=4103):
+    g = synth.rng(seed, 0)
+    out = []
+    for i in range(n):
+        E = int(g.integers(1, 13))
+        # segment sizes around multiples of 256 (remainders 0..255, some empty segments)
+        counts = [0 if g.random() < 0.1 else int(256 * g.integers(0, 6) + g.integers(0, 256)) for _ in range(E)]
+        if sum(counts) < 1100:  # above the decode size, so 256-row m-tiles (where tails merge) are used
+            counts[0] += 1100
+        out.append((i, counts, int(64 * g.integers(2, 9)), int(8 * g.integers(8, 49))))
+    return out
+
+
+@pytest.mark.parametrize("case,counts,H,d", _tail_fuzz_cases())
+def test_ffn_tail_fuzz_bitwise(rd, knob, case, counts, H, d):
+    """Seeded random segment sizes through the single-launch FFN: merged tails under the dynamic order (the
+    default below 16384 rows), merged tails under the static order, and separate tails under the static order
+    give the same bits; the default also vs the fp64 oracle."""
+    E = len(counts)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(off[-1])
+    xs = synth.to_torch(synth.tokens(rows, H, seed=300 + case), "bf16").to(DEV)
+    wg, wu, wd = (synth.to_torch(w, "bf16") for w in synth.expert_weights(E, d, H, seed=400 + case))
+    W = [w.to(DEV) for w in (wg, wu, wd)]
+    offd = torch.from_numpy(off).to(DEV)
+    outs = []
+    for merge, dyn in [(-1, -1), (1, 0), (0, 0), (1, 1)]:
+        knob("ffn_merge", merge)
+        knob("ffn_dyn", dyn)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        outs.append(rd.expert_ffn(xs, offd, *W, dev_status=st))
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
+    ref = oracle.expert_ffn(xs.cpu(), off, wg, wu, wd)
+    assert rel_err(_np(outs[0]), ref) <= BF16_TOL
+
+
 @pytest.mark.parametrize("T,E,k,H,d", _fuzz_cases(8, seed=19123))
 def test_moe_layer_fuzz_f32(rd, T, E, k, H, d):
     x, lg, wg, wu, wd = _ffn_case(T, H, d, E, k, "f32", seed=T * 5 + E + H + d)
