@@ -391,13 +391,13 @@ struct LayerArgs {
             // x_sorted; 2 = per-row readiness flags (xready) instead, so gate/up tiles start while the
             // dispatch is still writing later experts' rows (the wait moves to the kernel's end); 3 = the
             // kernel dispatches itself (dx below), as a programmatic dependent of the route
-  // pdl == 3 (a5 fused in): the epilogue warps, idle until the first accumulators are full, gather
-  // x_sorted[r] = x[dsrc[r] / dk] for r < drows in ascending waves and publish xready[r] per row
+  // pdl == 3 (a5 fused in): the epilogue warps gather x_sorted[r] = x[dsrc[r] / dk] while they wait for
+  // accumulators (copy_row / wait_copying) and count each segment's copied rows in seg_rows
   const uint4* dx;
   const int32_t* dsrc;
   void* dxs;     // x_sorted (the tensor map's buffer)
   int dk, dvec;  // top-k; 16-byte vectors per row
-  const uint32_t* xready;  // pdl == 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
+  const uint32_t* xready;  // pdl >= 2: [rows] flags, nonzero once row r of x_sorted is written (gather dispatch)
   uint64_t* trace;         // measurement only (readme_debug_trace), normally null
   uint64_t* ttrace;        // measurement only (readme_debug_tile_trace): [pair][ttrace_max][8], normally null
   int ttrace_max;
@@ -419,14 +419,14 @@ struct LTile {
                    // tile's weight stages; 0 = none
 };
 
-constexpr int kTailMax = 64;  // rows of a merged segment tail (one swap-AB MMA of N <= 64 per K step)
+constexpr int kTailMax = 64;  // rows of a merged segment tail (swap-AB MMAs of N <= 64 per K step)
 constexpr int kMaxTails = 2;  // merged tails per segment at most
 
 // m-tiles of a segment of R rows. With merging (256-row m-tiles): floor(R / 256) full m-tiles carry the
 // remainder as tails of <= 64 rows (one per full m-tile, at most kMaxTails) when it fits, else the remainder
 // is an m-tile of its own, as without merging. Every m-tile streams the expert's whole weight tile through its
 // SMs whatever its rows, so a separate tail tile cost as many SM cycles as a full one (~530 per K step); a
-// merged tail costs its swap-AB MMAs only, ~190 cycles per K step whatever its rows (4 MMAs re-reading the
+// merged tail costs its swap-AB MMAs only, ~190-250 cycles per K step whatever its rows (its MMAs re-read the
 // 16 KB weight stage): worth it for one or two tails, not three (tile trace, profiles/SUMMARY.md r02).
 __device__ __forceinline__ bool seg_merges(int R) {
   const int nf = R >> 8, rem = R & 255;
@@ -802,9 +802,9 @@ __device__ __forceinline__ void tail_gu_epilogue(const LayerArgs& la, const LTil
 // gate/up phase (a segment's rows land while the previous segment's tiles run) instead of competing for HBM
 // with the first tiles' weights, and every row a running tile needs is copied by warps that are themselves
 // waiting on tiles of that segment or earlier (which complete: their rows were copied first). Rows left when
-// a warp runs out of tiles are copied before it exits. Per row: 8 x 16 B loads in flight per lane, then the
-// row's flag (generic -> async proxy fence, release) for the producers' per-tile waits; a bad index is
-// reported and its row still flagged.
+// a warp runs out of tiles are copied before it exits. Per row: 8 x 16 B loads in flight per lane, then a
+// generic -> async proxy fence and a release add on its segment's copied-row counter (the producers wait for
+// a segment's count once per CTA); a bad index is reported and its row still counted.
 struct RowCopier {
   int64_t next, step;  // this warp's next row, and the stride (epilogue warps in the grid)
   int seg;             // segment of `next` (rows ascend, so a cursor)
@@ -1058,9 +1058,9 @@ ffn_layer2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     TileQ tq;
     const bool dyn = la.dyn != 0;
     // every pair's first tile is its index; with the dynamic order the leader's producer claims the next one
-    // kClaimAhead K steps before the end of this tile's loads (~2 ring depths before the tile's MMAs end: late
-    // enough that the claim order follows the pairs' finishing order, early enough to hide the atomic) and
-    // publishes it once this tile's loads are issued
+    // la.claim_ahead (knob ffn_claim, 24) K steps before the end of this tile's loads — late enough that the
+    // claim order follows the pairs' finishing order, early enough to hide the atomic — and publishes it once
+    // this tile's loads are issued
     for (int t = pair; t < ntiles;) {
       uint32_t claim = 0;
       const bool claimer = dyn && leader;
