@@ -1243,8 +1243,32 @@ def main():
             torch.cuda.current_stream().wait_stream(pipe.down)
 
         c_ms = float(np.median(timed(copies_only, 5)))
+
+        def copies_pattern():
+            # the pipeline's own schedule with the layer left out: K uploads back to back on the up stream,
+            # each batch's download on the down stream as soon as its upload is done
+            a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a0.record(pipe.up)
+            for i in range(args.steps):
+                with torch.cuda.stream(pipe.up):
+                    pipe.x[i % 2].copy_(x_h, non_blocking=True)
+                    pipe.lg[i % 2].copy_(lg_h, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(pipe.up)
+                pipe.down.wait_event(ev)
+                with torch.cuda.stream(pipe.down):
+                    ys_h[i % 2].copy_(pipe.y[i % 2], non_blocking=True)
+            b0.record(pipe.down)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(b0) / args.steps
+
+        pat_ms = copies_pattern()
         line["e2e"]["roofline"] = {"bound": "pcie", "copies_only_ms": c_ms, "frac": c_ms / p_ms,
-                                   "note": "the step's H2D and D2H bytes copied concurrently, nothing else"}
+                                   "pattern_ms": pat_ms, "frac_of_pattern": pat_ms / p_ms,
+                                   "note": "copies_only: one step's H2D and D2H bytes copied at once, nothing "
+                                           "else; pattern: the pipeline's K-batch copy schedule without the "
+                                           "layer (the bound the pipelined e2e number can reach on this box)"}
         del xd2
 
     if world > 1 and ep_mode == "peer" and not args.no_nccl_record:
