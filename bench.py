@@ -1234,6 +1234,10 @@ def main():
         xd2 = torch.empty_like(x_d)
 
         def copies_only():
+            # the copy streams start after the timing event on the current stream (without these waits they
+            # would begin during timed()'s L2 flush, before the start event, and the time would read short)
+            pipe.up.wait_stream(torch.cuda.current_stream())
+            pipe.down.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(pipe.up):
                 xd2.copy_(x_h, non_blocking=True)
                 lg_d.copy_(lg_h, non_blocking=True)
