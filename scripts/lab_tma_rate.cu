@@ -2,14 +2,13 @@
 // weight tiles, as a function of the number of streaming CTAs (one per SM), the ring depth and the copy form.
 //   mode 0: 3-D tiled boxes of 64 rows x 64 bf16 (128-B swizzle) from a K-major [N][K] matrix (the FFN's
 //           weight loads; rows K*2 bytes apart)
-//   mode 1: 1-D cp.async.bulk of 8 KB contiguous
+//   mode 1: 1-D cp.async.bulk of 8 KB contiguous (the first, non-cluster kernel; modes 2-4 below)
 // Each CTA streams `per_cta` bytes of its own region through a ring of S stages of 16 KB (2 boxes per stage);
 // a consumer thread releases each stage as soon as it lands (no compute). cold: L2 flushed before each run.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2410_19123_b200/csrc
 //        scripts/lab_tma_rate.cu paper_2410_19123_b200/csrc/tensor_maps.cu -o /tmp/tma_rate
 #include <cstdio>
 #include <cstdlib>
-#include <vector>
 
 #include "tc_common.cuh"
 
@@ -75,7 +74,9 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
 }
 
 // cluster of 2: mode 2 = each CTA issues ONE of a stage's two boxes with .multicast::cluster to both CTAs (each
-// CTA receives 16 KB per stage, issues 8 KB); mode 3 = same cluster, no multicast (each CTA loads both boxes);
+// CTA receives 16 KB per stage, issues 8 KB; a slot is refilled only after BOTH CTAs' consumers released it, so
+// this mode measures that cross-CTA release chain more than the multicast: 13-17 GB/s, not a TMA number);
+// mode 3 = same cluster, no multicast (each CTA loads both boxes);
 // mode 4 = one 128-row box per stage (16 KB per instruction), no cluster use
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64, 1)
     stream_mc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm128, int K,
