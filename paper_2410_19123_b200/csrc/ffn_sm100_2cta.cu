@@ -638,7 +638,10 @@ struct __align__(8) SmemLT {
   uint32_t segok[kMaxSeg / 32];  // pdl == 3: bit per segment, all its rows seen copied
 };
 constexpr int kStagesL = 6;
-constexpr int kStagesLD = 9;
+#ifndef README_STAGES_LD
+#define README_STAGES_LD 9  // lab builds may override (README_NVCC_EXTRA=-DREADME_STAGES_LD=n)
+#endif
+constexpr int kStagesLD = README_STAGES_LD;
 constexpr int kTailSlot = 16384;             // offset of the merged-tail rows inside a 256-row stage's A slot
 constexpr int kStageAL = kStageA + 4096;     // <= 32 tail rows x 128 B per CTA
 constexpr int kMaxDefer = 3;                 // K stages whose tail MMAs may wait for the borrowed columns
