@@ -616,7 +616,7 @@ def run_tiny(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config1_tiny", "T": T, "H": H, "E": E, "d": d, "k": k,
                        "note": "latency-bound (12.6 MFLOP); graph replay", "l2": L2Flush.NOTE},
-            "latency_us": t * 1e3, "gpu_launches": 4 * args.steps,  # route, dispatch, fp32 gate/up, fp32 down
+            "latency_us": t * 1e3, "gpu_launches": 2 * args.steps,  # route, one-launch fp32 FFN (a5 gather + a6 + a7 + a8)
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 

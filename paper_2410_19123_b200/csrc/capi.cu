@@ -130,6 +130,11 @@ readme_status run_ffn(const void* x_sorted, readme_dtype dt, int64_t rows, int32
                                  static_cast<const __nv_bfloat16*>(residual), ready, dev_status, st, nullptr, 0,
                                  nullptr, pdl, xready ? ffn_xready(ws, rows, d, dt) : nullptr, sd);
   }
+  if (dt == README_F32 && ffn_f32_fusable(H, d))  // small fp32 layers: a6 + a7 in one launch, h in shared memory
+    return launch_ffn_f32_fused(static_cast<const float*>(x_sorted), nullptr, nullptr, 1, rows, H, E, d, n_src * E,
+                                offsets, static_cast<const float*>(w_gate), static_cast<const float*>(w_up),
+                                static_cast<const float*>(w_down), static_cast<float*>(out), src,
+                                static_cast<const float*>(residual), st);
   README_TRY(readme_expert_gate_up(x_sorted, dt, rows, H, E, d, n_src, offsets, w_gate, w_up, ws, stream));
   return readme_expert_down(ws, dt, rows, H, E, d, n_src, offsets, w_down, src, residual, out, stream);
 }
@@ -430,6 +435,13 @@ readme_status readme_moe_layer(const void* x, readme_dtype dt, int64_t T, int32_
       xready = pdl && gather_dispatch(rows);
       README_TRY(launch_route(logits, logits_dt, T, E, k, topk_idx, topk_w, counts, offsets, dest, src, dev_status,
                               ws_route, st, true, ready, ready_words));
+      if (fused && dt == README_F32 && ffn_f32_fusable(H, d)) {
+        // small fp32 layer: a5 as a row gather inside the one-launch FFN (x[src[r] / k]), a8 in its epilogue
+        return launch_ffn_f32_fused(nullptr, static_cast<const float*>(x), src, k, rows, H, E, d, E, offsets,
+                                    static_cast<const float*>(w_gate), static_cast<const float*>(w_up),
+                                    static_cast<const float*>(w_down), static_cast<float*>(y), src,
+                                    static_cast<const float*>(residual), st);
+      }
       if (xready && fused_gather_dispatch()) {
         sd_store = SelfDispatch{static_cast<const __nv_bfloat16*>(x), src, k};
         sd = &sd_store;

@@ -71,6 +71,13 @@ readme_status launch_gate_up_f32(const float* xs, int64_t rows, int32_t H, int32
 readme_status launch_down_f32(const float* h, int64_t rows, int32_t H, int32_t E, int32_t d, int32_t nseg,
                               const int32_t* offsets, const float* wd, float* out, const int32_t* src,
                               const float* residual, cudaStream_t st);
+// a6 + a7 (+ fused combine: y[src[r]] (+ residual) when src is set; + a5 as a gather of x[gsrc[r] / k] when x
+// is set, else rows of xs) in one launch, for H, d <= 128 (ffn_f32_fusable); bitwise equal to the two launches
+bool ffn_f32_fusable(int32_t H, int32_t d);
+readme_status launch_ffn_f32_fused(const float* xs, const float* x, const int32_t* gsrc, int32_t k, int64_t rows,
+                                   int32_t H, int32_t E, int32_t d, int32_t nseg, const int32_t* offsets, const float* wg,
+                                   const float* wu, const float* wd, float* out, const int32_t* src,
+                                   const float* residual, cudaStream_t st);
 
 // ffn_sm100.cu / ffn_sm100_2cta.cu (tcgen05 / TMEM / TMA grouped GEMMs, bf16)
 readme_status launch_gemm_1cta(int mode, const __nv_bfloat16* A, int64_t rows, int32_t K, int32_t N, int32_t E,

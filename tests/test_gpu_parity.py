@@ -313,6 +313,31 @@ def test_expert_ffn_f32_config1(rd):
     assert rel_err(_np(ys), ref) <= F32_TOL
 
 
+@pytest.mark.parametrize("T,H,d,E", [(256, 64, 128, 8), (777, 128, 96, 5), (40, 32, 8, 3)])
+def test_f32_one_launch_ffn_bitwise(rd, T, H, d, E):
+    """Small fp32 layers (H, d <= 128) run a6 + a7 in one launch (h in shared memory) and, inside
+    readme_moe_layer with logits, gather their rows straight from x through src: bitwise equal to the two
+    separate launches (readme_expert_gate_up + readme_expert_down, the same fmaf order), to plan-in mode, and
+    within the fp32 rule of the oracle."""
+    x, lg, wg, wu, wd = _ffn_case(T, H, d, E, 1, "f32", seed=T + H + d)
+    res = synth.to_torch(synth.residual(T, H, seed=T + 5), "f32").to(DEV)
+    x, wg, wu, wd = x.to(DEV), wg.to(DEV), wu.to(DEV), wd.to(DEV)
+    lgt = torch.from_numpy(lg).to(DEV)
+    plan = rd.route(lgt, 1)
+    xs = rd.dispatch(x, plan.dest, 1)
+    ys = rd.expert_ffn(xs, plan.offsets, wg, wu, wd)
+    h = rd.expert_gate_up(xs, plan.offsets, wg, wu)
+    assert torch.equal(ys, rd.expert_down(h, plan.offsets, wd))
+    y, p2 = rd.moe_layer(x, wg, wu, wd, k=1, logits=lgt, residual=res)
+    assert torch.equal(p2.src, plan.src) and torch.equal(p2.offsets, plan.offsets)
+    assert torch.equal(y, rd.expert_down(h, plan.offsets, wd, src=plan.src, residual=res))
+    y_in, _ = rd.moe_layer(x, wg, wu, wd, k=1, plan=plan, residual=res)
+    assert torch.equal(y, y_in)
+    ref = oracle.combine(oracle.expert_ffn(xs.cpu(), plan.offsets.cpu().numpy(), wg.cpu(), wu.cpu(), wd.cpu()),
+                         plan.dest.cpu().numpy(), np.ones((T, 1)), 1, residual=res.cpu())
+    assert rel_err(_np(y), ref) <= F32_TOL
+
+
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 def test_gate_up_and_down_separately(rd, dt):
     """a6 and a7 each teacher-forced against the oracle; a7 with src scatters rows (fused combine)."""
