@@ -1293,6 +1293,23 @@ def main():
                                  "vs_fused": ms_per_step / n_per, "backend": dist.get_backend(),
                                  "mode": "NCCL all_to_all_single between the library's dispatch / grouped FFN / "
                                          "combine kernels, one count exchange per step, eager"}
+        # what the fused path timed, checked: its last replay's output (y + residual, rounded once in the down
+        # epilogue, in the arena) against the NCCL path on the same tokens (its combine adds the residual to the
+        # bf16 y, a second rounding), per token: max |a - b|_inf / |b|_inf over rows and ranks against the
+        # parity rule's 2e-2 (the two differ by the extra rounding: ~2^-8..2^-7 relative)
+        y_nccl = nl.layer(residual=nl.x)
+        torch.cuda.synchronize()
+        a_, b_ = layer.out.float(), y_nccl.float()
+        rel = ((a_ - b_).abs().amax(dim=1) / b_.abs().amax(dim=1).clamp_min(1e-6)).max()
+        chk = torch.tensor([float(rel.item()), float((a_ - b_).abs().max().item()),
+                            float(int(layer.dev_status.item()))], device=dev)
+        dist.all_reduce(chk, op=dist.ReduceOp.MAX)
+        line["ep_output_check"] = {"max_rel_err": float(chk[0].item()), "max_abs_diff": float(chk[1].item()),
+                                   "tol": 2e-2, "ok": bool(chk[0].item() <= 2e-2 and chk[2].item() == 0),
+                                   "dev_status": int(chk[2].item()),
+                                   "what": "every rank's output rows of the timed fused peer-memory step vs the "
+                                           "NCCL all-to-all path on the same tokens (per-token relative, max over "
+                                           "rows and ranks)"}
         del nl
         torch.cuda.empty_cache()
 

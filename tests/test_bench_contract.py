@@ -82,3 +82,4 @@ def test_bench_n2_line_on_one_gpu():
     assert d["config"]["workload"] == "config5_expert_parallel" and d["config"]["T_total"] == 65536
     assert d["config"]["T_per_gpu"] == 32768 and "peer-memory" in d["config"]["ep_exchange"]
     assert d["nccl_exchange"]["value"] > 0
+    assert d["ep_output_check"]["ok"] and d["ep_output_check"]["dev_status"] == 0
